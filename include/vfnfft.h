@@ -1,0 +1,127 @@
+/*
+ * vfnfft.h — C ABI of the B200-native 3D NFFT trafo (type-2 NUFFT).
+ *
+ * Drop-in boundary for the reference package `vortexfourier` (pure Python,
+ * /root/reference/pkg/src/vortexfourier).  The reference has no FFI of its
+ * own; these entry points are exactly what a ctypes / cffi binding of its
+ * hot path would bind, one per reference operation:
+ *
+ *   vfn_plan_create   <- NufftPlan.__init__        nufft.py:197-242
+ *                        (rescale_coeffs nufft.py:95-112, _kb_beta :152-156,
+ *                         _kb_transform :167-176, _oversampled_size :179-187)
+ *   vfn_plan_eval     <- NufftPlan.evaluate        nufft.py:244-272
+ *                        (_check_points :115-126, map_to_torus :81-92)
+ *   vfn_plan_destroy  <- (garbage collection of a NufftPlan)
+ *   vfn_rect_eval     <- eval_rectilinear          rectilinear.py:47-64
+ *                        (basis_matrix rectilinear.py:22-44)
+ *   vfn_map_to_torus  <- map_to_torus              nufft.py:81-92
+ *   vfn_plan_bin      <- (new) the cell-binning sort key and stable
+ *                        permutation
+ *   vfn_plan_grid     <- NufftPlan._grid           nufft.py:242 (inspection)
+ *   vfn_direct_eval   <- eval_direct               nufft.py:129-149 (exact NDFT)
+ *
+ * Conventions
+ *   - complex numbers are interleaved (re, im) doubles, numpy complex128;
+ *   - points are (M, 3) row-major doubles; coefficients are (N1, N2, N3)
+ *     C-order in the reference's centred order (index j <-> k = j - N/2);
+ *   - `on_device` != 0 means the pointer is CUDA device memory on the plan's
+ *     device, otherwise host memory (pinned host memory makes the copies
+ *     asynchronous);
+ *   - `stream` is a cudaStream_t (0 = legacy default stream);
+ *   - every call returns a vfn_status; vfn_last_error() gives the message of
+ *     the last failure on the calling thread.
+ *   - Inputs are never modified; the plan owns its device grid; outputs are
+ *     caller-owned.  A plan may be evaluated from one host thread at a time.
+ */
+#ifndef VFNFFT_H
+#define VFNFFT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  VFN_OK = 0,
+  VFN_ERR_INVALID = -1,   /* bad argument (message says which) -> ValueError */
+  VFN_ERR_OUTSIDE = -2,   /* a point lies outside [a, b); *first_bad_row set  */
+  VFN_ERR_CUDA = -3,      /* CUDA runtime error                               */
+  VFN_ERR_CUFFT = -4,     /* cuFFT error                                      */
+  VFN_ERR_CUBLAS = -5,    /* cuBLAS error                                     */
+  VFN_ERR_NOMEM = -6      /* device allocation failed                         */
+} vfn_status;
+
+typedef struct vfn_plan vfn_plan;
+
+/* Library / kernel version string (for logs). */
+const char* vfn_version(void);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* vfn_last_error(void);
+
+/* Build the oversampled, deconvolved grid for one spectral field.
+ *   nmodes  : N1, N2, N3 (each even, > 0)
+ *   a, b    : box corners, a[d] < b[d]
+ *   sigma   : oversampling; n_d = sigma * N_d must be an even integer >= N_d
+ *   m       : window half-width in cells, 1..13 (each point reads (2m+1)^3)
+ *   coeffs  : N1*N2*N3 complex128 (host or device, see on_device)         */
+int vfn_plan_create(vfn_plan** out, int device, const int64_t nmodes[3],
+                    const double a[3], const double b[3], double sigma, int m,
+                    const double* coeffs, int coeffs_on_device, void* stream);
+
+/* Evaluate the series at M points (nufft.py:244-272).
+ *   points : M*3 doubles; out : M complex128 in input order.
+ *   On VFN_ERR_OUTSIDE *first_bad_row holds the first offending row index
+ *   (NaN coordinates count as outside), and `out` is unspecified.         */
+int vfn_plan_eval(vfn_plan* plan, const double* points, int64_t M, double* out,
+                  int on_device, int64_t* first_bad_row, void* stream);
+
+int vfn_plan_destroy(vfn_plan* plan);
+
+/* Plan facts: n[3] oversampled sizes, beta; either pointer may be NULL. */
+int vfn_plan_info(const vfn_plan* plan, int64_t n_out[3], double* beta_out);
+
+/* Copy the (n1, n2, n3) oversampled grid (nufft.py:242 `_grid`) to host. */
+int vfn_plan_grid(vfn_plan* plan, double* out_host);
+
+/* The bin-sort of M points (new): key[i] of input row i, and
+ * perm = stable argsort(key) (sorted position -> input row).  Host or device
+ * buffers per on_device; keys are uint32, perm int32.                    */
+int vfn_plan_bin(vfn_plan* plan, const double* points, int64_t M, uint32_t* keys,
+                 int32_t* perm, int on_device, int64_t* first_bad_row, void* stream);
+
+/* zeta = mod((x - a)/(a - b), 1) - 1/2, bit-exact with numpy (nufft.py:81-92). */
+int vfn_map_to_torus(int device, const double a[3], const double b[3], const double* points,
+                     int64_t M, double* zeta, int on_device, void* stream);
+
+/* Rectilinear tensor-grid evaluation (rectilinear.py:47-64): out is
+ * (M1, M2, M3) complex128 C-order.  Coordinates must lie in [a_d, b_d)
+ * (checked by the caller, rectilinear.py:28-41).                        */
+int vfn_rect_eval(int device, const int64_t nmodes[3], const double a[3], const double b[3],
+                  const double* coeffs, const double* y1, int64_t M1, const double* y2,
+                  int64_t M2, const double* y3, int64_t M3, double* out, int on_device,
+                  void* stream);
+
+/* Exact series sum at M points, O(N1 N2 N3) per point (nufft.py:129-149).
+ * Each N_d <= 1024.  Same point/domain conventions as vfn_plan_eval.   */
+int vfn_direct_eval(int device, const int64_t nmodes[3], const double a[3], const double b[3],
+                    const double* coeffs, const double* points, int64_t M, double* out,
+                    int on_device, int64_t* first_bad_row, void* stream);
+
+/* Gather geometry vfn_plan_eval / vfn_plan_bin use for M points: the box
+ * and staging-tile sizes in cells that define the bin key. */
+int vfn_plan_geometry(const vfn_plan* plan, int64_t M, int box_out[3], int tile_out[3]);
+
+/* Kernel selection for vfn_plan_eval (benchmarks / A-B tests):
+ * 0 = automatic, 1 = simple thread-per-point gather, 2 = DMMA box gather. */
+int vfn_plan_set_gather(vfn_plan* plan, int variant);
+
+/* Device time (ms) of the last vfn_plan_eval's gather kernel and of the
+ * whole device-side evaluate, measured with CUDA events on its stream. */
+int vfn_plan_last_timing(const vfn_plan* plan, float* gather_ms, float* total_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VFNFFT_H */

@@ -1,0 +1,34 @@
+"""B200-native 3D NFFT trafo: drop-in for the hot path of the reference
+package `vortexfourier` (scattered-point and rectilinear-grid evaluation of a
+3D truncated Fourier series).  The evaluators run hand-written sm_100a
+kernels through the C ABI in include/vfnfft.h (libvfnfft.so, built in-tree).
+"""
+
+from .fourier import DomainBox, SpectralField, regular_grid
+from .nufft import (
+    AccuracyWarning,
+    NufftParams,
+    NufftPlan,
+    eval_direct,
+    eval_nufft,
+    map_to_torus,
+    rescale_coeffs,
+)
+from .rectilinear import basis_matrix, eval_rectilinear
+
+__all__ = [
+    "AccuracyWarning",
+    "DomainBox",
+    "NufftParams",
+    "NufftPlan",
+    "SpectralField",
+    "basis_matrix",
+    "eval_direct",
+    "eval_nufft",
+    "eval_rectilinear",
+    "map_to_torus",
+    "regular_grid",
+    "rescale_coeffs",
+]
+
+__version__ = "0.1.0"

@@ -1,0 +1,365 @@
+// extern "C" entry points of libvfnfft (see include/vfnfft.h).
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "vfn_internal.cuh"
+
+namespace vfn {
+const char* last_error_cstr();
+int extract_grid(vfn_plan* p, double2* out_dev, cudaStream_t s);
+}
+
+using namespace vfn;
+
+namespace {
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// oversampled size rule of nufft.py:179-187
+int oversampled(int64_t N, double sigma, int64_t* n) {
+  double target = sigma * (double)N;
+  double r = std::nearbyint(target);
+  int64_t ri = (int64_t)r;
+  if (std::fabs(target - r) > 1e-9 || ri % 2 != 0 || ri < N)
+    return fail(VFN_ERR_INVALID, "oversampling " + std::to_string(sigma) + " of " +
+                                     std::to_string(N) + " modes gives grid size " +
+                                     std::to_string(target) +
+                                     "; need an even integer no smaller than the mode count");
+  *n = ri;
+  return VFN_OK;
+}
+
+int check_box(const double a[3], const double b[3]) {
+  for (int d = 0; d < 3; ++d)
+    if (!(std::isfinite(a[d]) && std::isfinite(b[d]) && a[d] < b[d]))
+      return fail(VFN_ERR_INVALID, "domain bounds must be finite with a < b");
+  return VFN_OK;
+}
+
+int stage_in(DevBuf& buf, const void* src, size_t bytes, int on_device, const void** dev,
+             cudaStream_t s) {
+  if (on_device) {
+    *dev = src;
+    return VFN_OK;
+  }
+  VFN_CHECK(buf.ensure(bytes));
+  VFN_CUDA(cudaMemcpyAsync(buf.ptr, src, bytes, cudaMemcpyHostToDevice, s));
+  *dev = buf.ptr;
+  return VFN_OK;
+}
+
+int key_bits_for(int64_t nkeys) {
+  int bits = 1;
+  while (bits < 32 && ((int64_t)1 << bits) < nkeys) ++bits;
+  return bits;
+}
+
+}  // namespace
+
+namespace vfn {
+
+// Gather geometry: box/tile sizes by point density (K4).
+BinGeom choose_geometry(const vfn_plan* p, int64_t M) {
+  BinGeom g;
+  const double cells = (double)p->n[0] * (double)p->n[1] * (double)p->n[2];
+  const double density = M / cells;
+  const int K = ((2 * p->m + 1) + 3) / 4 * 4;  // DMMA k-extent
+  const int bk = K - 2 * p->m;                  // box depth in cells (2 or 4)
+  int bxy = density >= 1.0 ? 1 : 2;
+  g.box[0] = bxy;
+  g.box[1] = bxy;
+  g.box[2] = bk;
+  g.tile[0] = 4;
+  g.tile[1] = 4;
+  g.tile[2] = bk;
+  for (int d = 0; d < 3; ++d) {
+    g.ntile[d] = (int)((p->n[d] + g.tile[d] - 1) / g.tile[d]);
+    g.nbox[d] = g.tile[d] / g.box[d];
+  }
+  g.boxes_per_tile = g.nbox[0] * g.nbox[1] * g.nbox[2];
+  g.ntiles = (int64_t)g.ntile[0] * g.ntile[1] * g.ntile[2];
+  g.nboxes = g.ntiles * g.boxes_per_tile;
+  return g;
+}
+
+}  // namespace vfn
+
+extern "C" {
+
+const char* vfn_version(void) { return "vfnfft 0.1 (sm_100a)"; }
+
+const char* vfn_last_error(void) { return last_error_cstr(); }
+
+int vfn_plan_create(vfn_plan** out, int device, const int64_t nmodes[3], const double a[3],
+                    const double b[3], double sigma, int m, const double* coeffs,
+                    int coeffs_on_device, void* stream) {
+  if (!out || !nmodes || !a || !b || !coeffs) return fail(VFN_ERR_INVALID, "null argument");
+  *out = nullptr;
+  if (m < 1 || m > 13) return fail(VFN_ERR_INVALID, "cutoff must be in 1..13");
+  if (!(sigma >= 1.0)) return fail(VFN_ERR_INVALID, "oversampling must be >= 1");
+  VFN_CHECK(check_box(a, b));
+  for (int d = 0; d < 3; ++d)
+    if (nmodes[d] <= 0 || nmodes[d] % 2 != 0)
+      return fail(VFN_ERR_INVALID, "array dimensions must be even and positive");
+  DeviceGuard guard(device);
+  cudaStream_t s = as_stream(stream);
+  vfn_plan* p = new vfn_plan();
+  p->device = device;
+  p->sigma = sigma;
+  p->m = m;
+  for (int d = 0; d < 3; ++d) {
+    p->N[d] = nmodes[d];
+    p->a[d] = a[d];
+    p->b[d] = b[d];
+    int st = oversampled(nmodes[d], sigma, &p->n[d]);
+    if (st != VFN_OK) {
+      delete p;
+      return st;
+    }
+    if (p->n[d] > (1 << 20)) {
+      delete p;
+      return fail(VFN_ERR_INVALID, "oversampled grid too large");
+    }
+    p->map.a[d] = a[d];
+    p->map.b[d] = b[d];
+    p->map.amb[d] = a[d] - b[d];
+    p->map.nd[d] = (double)p->n[d];
+    p->map.n[d] = (int)p->n[d];
+    const int64_t pt = p->pad_tile[d];
+    p->P[d] = (p->n[d] + pt - 1) / pt * pt + 2 * m;
+  }
+  p->beta = kb_beta(m, sigma);
+  // window polynomial table
+  {
+    const int max_deg = 26;
+    std::vector<double> coef((size_t)(2 * m + 1) * (max_deg + 1));
+    p->poly.m = m;
+    p->poly.deg = fit_window_poly(m, p->beta, coef.data(), max_deg);
+    size_t bytes = sizeof(double) * (2 * m + 1) * (p->poly.deg + 1);
+    cudaError_t e = cudaMalloc(&p->poly.dev, bytes);
+    if (e == cudaSuccess) e = cudaMemcpy(p->poly.dev, coef.data(), bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      vfn_plan_destroy(p);
+      return fail(VFN_ERR_CUDA, std::string("window table: ") + cudaGetErrorString(e));
+    }
+  }
+  for (int i = 0; i < 4; ++i) cudaEventCreate(&p->ev[i]);
+  // coefficients to the device
+  const size_t cbytes = sizeof(double2) * nmodes[0] * nmodes[1] * nmodes[2];
+  DevBuf staging;
+  const void* cdev = nullptr;
+  int st = stage_in(staging, coeffs, cbytes, coeffs_on_device, &cdev, s);
+  if (st == VFN_OK) st = build_grid(p, static_cast<const double*>(cdev), s);
+  staging.release();
+  if (st != VFN_OK) {
+    std::string msg = vfn_last_error();
+    vfn_plan_destroy(p);
+    return fail(st, msg);
+  }
+  *out = p;
+  return VFN_OK;
+}
+
+int vfn_plan_destroy(vfn_plan* p) {
+  if (!p) return VFN_OK;
+  DeviceGuard guard(p->device);
+  if (p->grid) cudaFree(p->grid);
+  if (p->poly.dev) cudaFree(p->poly.dev);
+  DevBuf* bufs[] = {&p->pts, &p->out, &p->keys, &p->keys_sorted, &p->idx, &p->perm,
+                    &p->sort_tmp, &p->box_start, &p->items, &p->misc};
+  for (DevBuf* b : bufs) b->release();
+  for (int i = 0; i < 4; ++i)
+    if (p->ev[i]) cudaEventDestroy(p->ev[i]);
+  delete p;
+  return VFN_OK;
+}
+
+int vfn_plan_info(const vfn_plan* p, int64_t n_out[3], double* beta_out) {
+  if (!p) return fail(VFN_ERR_INVALID, "null plan");
+  if (n_out)
+    for (int d = 0; d < 3; ++d) n_out[d] = p->n[d];
+  if (beta_out) *beta_out = p->beta;
+  return VFN_OK;
+}
+
+int vfn_plan_geometry(const vfn_plan* p, int64_t M, int box_out[3], int tile_out[3]) {
+  if (!p || !box_out || !tile_out) return fail(VFN_ERR_INVALID, "null argument");
+  BinGeom g = choose_geometry(p, M);
+  for (int d = 0; d < 3; ++d) {
+    box_out[d] = g.box[d];
+    tile_out[d] = g.tile[d];
+  }
+  return VFN_OK;
+}
+
+int vfn_plan_set_gather(vfn_plan* p, int variant) {
+  if (!p || variant < 0 || variant > 2) return fail(VFN_ERR_INVALID, "bad gather variant");
+  p->gather_variant = variant;
+  return VFN_OK;
+}
+
+int vfn_plan_last_timing(const vfn_plan* p, float* gather_ms, float* total_ms) {
+  if (!p) return fail(VFN_ERR_INVALID, "null plan");
+  if (gather_ms) *gather_ms = p->last_gather_ms;
+  if (total_ms) *total_ms = p->last_total_ms;
+  return VFN_OK;
+}
+
+int vfn_plan_grid(vfn_plan* p, double* out_host) {
+  if (!p || !out_host) return fail(VFN_ERR_INVALID, "null argument");
+  DeviceGuard guard(p->device);
+  const size_t bytes = sizeof(double2) * p->n[0] * p->n[1] * p->n[2];
+  DevBuf tmp;
+  VFN_CHECK(tmp.ensure(bytes));
+  int st = extract_grid(p, tmp.as<double2>(), 0);
+  if (st == VFN_OK) {
+    cudaError_t e = cudaMemcpy(out_host, tmp.ptr, bytes, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) st = fail(VFN_ERR_CUDA, std::string("grid copy: ") + cudaGetErrorString(e));
+  }
+  tmp.release();
+  return st;
+}
+
+int vfn_map_to_torus(int device, const double a[3], const double b[3], const double* points,
+                     int64_t M, double* zeta, int on_device, void* stream) {
+  if (!a || !b || (M > 0 && (!points || !zeta))) return fail(VFN_ERR_INVALID, "null argument");
+  if (M < 0) return fail(VFN_ERR_INVALID, "negative point count");
+  VFN_CHECK(check_box(a, b));
+  if (M == 0) return VFN_OK;
+  DeviceGuard guard(device);
+  cudaStream_t s = as_stream(stream);
+  TorusMap tm;
+  for (int d = 0; d < 3; ++d) {
+    tm.a[d] = a[d];
+    tm.b[d] = b[d];
+    tm.amb[d] = a[d] - b[d];
+    tm.nd[d] = 1.0;
+    tm.n[d] = 1;
+  }
+  DevBuf in, outb;
+  const size_t bytes = sizeof(double) * 3 * M;
+  const void* pdev = nullptr;
+  VFN_CHECK(stage_in(in, points, bytes, on_device, &pdev, s));
+  double* zdev = zeta;
+  if (!on_device) {
+    VFN_CHECK(outb.ensure(bytes));
+    zdev = outb.as<double>();
+  }
+  VFN_CHECK(launch_torus(tm, static_cast<const double*>(pdev), M, zdev, s));
+  if (!on_device) VFN_CUDA(cudaMemcpyAsync(zeta, zdev, bytes, cudaMemcpyDeviceToHost, s));
+  VFN_CUDA(cudaStreamSynchronize(s));
+  in.release();
+  outb.release();
+  return VFN_OK;
+}
+
+// Shared front half of evaluate / bin: stage points, map+validate+key, sort.
+static int bin_points(vfn_plan* p, const double* points, int64_t M, int on_device,
+                      const BinGeom& g, const double** pts_dev, int64_t** bad_dev,
+                      cudaStream_t s) {
+  const void* pdev = nullptr;
+  VFN_CHECK(stage_in(p->pts, points, sizeof(double) * 3 * M, on_device, &pdev, s));
+  *pts_dev = static_cast<const double*>(pdev);
+  VFN_CHECK(p->misc.ensure(64));
+  *bad_dev = p->misc.as<int64_t>();
+  const int64_t sentinel = INT64_MAX;
+  VFN_CUDA(cudaMemcpyAsync(*bad_dev, &sentinel, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  VFN_CHECK(p->keys.ensure(sizeof(uint32_t) * M));
+  VFN_CHECK(p->keys_sorted.ensure(sizeof(uint32_t) * M));
+  VFN_CHECK(p->idx.ensure(sizeof(int32_t) * M));
+  VFN_CHECK(p->perm.ensure(sizeof(int32_t) * M));
+  VFN_CHECK(map_and_key(p, *pts_dev, M, g, p->keys.as<uint32_t>(), p->idx.as<int32_t>(), *bad_dev, s));
+  VFN_CHECK(sort_pairs(p, p->keys.as<uint32_t>(), p->keys_sorted.as<uint32_t>(),
+                       p->idx.as<int32_t>(), p->perm.as<int32_t>(), M, key_bits_for(g.nboxes), s));
+  return VFN_OK;
+}
+
+int vfn_plan_bin(vfn_plan* p, const double* points, int64_t M, uint32_t* keys, int32_t* perm,
+                 int on_device, int64_t* first_bad_row, void* stream) {
+  if (!p || (M > 0 && (!points || !keys || !perm))) return fail(VFN_ERR_INVALID, "null argument");
+  if (M < 0 || M > INT32_MAX) return fail(VFN_ERR_INVALID, "point count out of range");
+  if (first_bad_row) *first_bad_row = -1;
+  if (M == 0) return VFN_OK;
+  DeviceGuard guard(p->device);
+  cudaStream_t s = as_stream(stream);
+  BinGeom g = choose_geometry(p, M);
+  const double* pts_dev;
+  int64_t* bad_dev;
+  VFN_CHECK(bin_points(p, points, M, on_device, g, &pts_dev, &bad_dev, s));
+  cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  VFN_CUDA(cudaMemcpyAsync(keys, p->keys.ptr, sizeof(uint32_t) * M, k, s));
+  VFN_CUDA(cudaMemcpyAsync(perm, p->perm.ptr, sizeof(int32_t) * M, k, s));
+  int64_t bad = INT64_MAX;
+  VFN_CUDA(cudaMemcpyAsync(&bad, bad_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  VFN_CUDA(cudaStreamSynchronize(s));
+  if (bad != INT64_MAX) {
+    if (first_bad_row) *first_bad_row = bad;
+    return fail(VFN_ERR_OUTSIDE, "point (row " + std::to_string(bad) + ") lies outside the domain");
+  }
+  return VFN_OK;
+}
+
+int vfn_plan_eval(vfn_plan* p, const double* points, int64_t M, double* out, int on_device,
+                  int64_t* first_bad_row, void* stream) {
+  if (!p || (M > 0 && (!points || !out))) return fail(VFN_ERR_INVALID, "null argument");
+  if (M < 0 || M > INT32_MAX) return fail(VFN_ERR_INVALID, "point count out of range");
+  if (first_bad_row) *first_bad_row = -1;
+  if (M == 0) return VFN_OK;
+  DeviceGuard guard(p->device);
+  cudaStream_t s = as_stream(stream);
+  VFN_CUDA(cudaEventRecord(p->ev[0], s));
+  BinGeom g = choose_geometry(p, M);
+  const double* pts_dev;
+  int64_t* bad_dev;
+  VFN_CHECK(bin_points(p, points, M, on_device, g, &pts_dev, &bad_dev, s));
+  double2* out_dev = reinterpret_cast<double2*>(out);
+  if (!on_device) {
+    VFN_CHECK(p->out.ensure(sizeof(double2) * M));
+    out_dev = p->out.as<double2>();
+  }
+  VFN_CUDA(cudaEventRecord(p->ev[1], s));
+  bool used = false;
+  if (p->gather_variant != 1)
+    VFN_CHECK(gather_boxes(p, pts_dev, M, g, p->keys_sorted.as<uint32_t>(), p->perm.as<int32_t>(),
+                           out_dev, s, &used));
+  if (!used) {
+    if (p->gather_variant == 2) return fail(VFN_ERR_INVALID, "box gather unavailable for this plan");
+    VFN_CHECK(gather_simple(p, pts_dev, M, p->perm.as<int32_t>(), out_dev, s));
+  }
+  VFN_CUDA(cudaEventRecord(p->ev[2], s));
+  if (!on_device)
+    VFN_CUDA(cudaMemcpyAsync(out, out_dev, sizeof(double2) * M, cudaMemcpyDeviceToHost, s));
+  int64_t bad = INT64_MAX;
+  VFN_CUDA(cudaMemcpyAsync(&bad, bad_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  VFN_CUDA(cudaEventRecord(p->ev[3], s));
+  VFN_CUDA(cudaStreamSynchronize(s));
+  cudaEventElapsedTime(&p->last_gather_ms, p->ev[1], p->ev[2]);
+  cudaEventElapsedTime(&p->last_total_ms, p->ev[0], p->ev[3]);
+  if (bad != INT64_MAX) {
+    if (first_bad_row) *first_bad_row = bad;
+    return fail(VFN_ERR_OUTSIDE, "point (row " + std::to_string(bad) + ") lies outside the domain");
+  }
+  return VFN_OK;
+}
+
+int vfn_rect_eval(int device, const int64_t nmodes[3], const double a[3], const double b[3],
+                  const double* coeffs, const double* y1, int64_t M1, const double* y2,
+                  int64_t M2, const double* y3, int64_t M3, double* out, int on_device,
+                  void* stream) {
+  if (!nmodes || !a || !b || !coeffs || !out) return fail(VFN_ERR_INVALID, "null argument");
+  VFN_CHECK(check_box(a, b));
+  for (int d = 0; d < 3; ++d)
+    if (nmodes[d] <= 0 || nmodes[d] % 2 != 0)
+      return fail(VFN_ERR_INVALID, "mode counts must be positive and even");
+  if (M1 < 0 || M2 < 0 || M3 < 0) return fail(VFN_ERR_INVALID, "negative coordinate count");
+  if (M1 * M2 * M3 == 0) return VFN_OK;
+  DeviceGuard guard(device);
+  const double* y[3] = {y1, y2, y3};
+  const int64_t Mv[3] = {M1, M2, M3};
+  return rect_eval(device, nmodes, a, b, coeffs, y, Mv, out, on_device, as_stream(stream));
+}
+
+}  // extern "C"

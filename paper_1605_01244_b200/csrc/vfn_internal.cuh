@@ -1,0 +1,155 @@
+// Internal declarations shared by the vfnfft translation units.
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include "../../include/vfnfft.h"
+
+namespace vfn {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+
+#define VFN_CUDA(expr)                                                               \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess)                                                           \
+      return ::vfn::fail(VFN_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+#define VFN_CHECK(expr)          \
+  do {                           \
+    int _s = (expr);             \
+    if (_s != VFN_OK) return _s; \
+  } while (0)
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// Grow-only device buffer owned by a plan.
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t need) {
+    if (need <= bytes) return VFN_OK;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    size_t want = need + need / 8;
+    cudaError_t e = cudaMalloc(&ptr, want);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(VFN_ERR_NOMEM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+    }
+    bytes = want;
+    return VFN_OK;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const { return static_cast<T*>(ptr); }
+};
+
+// ---------------------------------------------------------------- geometry
+// Everything a kernel needs to map a point to its nearest oversampled cell,
+// bit-exactly as nufft.py:81-92 + :248-257 do it in numpy.
+struct TorusMap {
+  double a[3];
+  double amb[3];  // a - b, the divisor of map_to_torus (nufft.py:92)
+  double b[3];
+  double nd[3];   // n_d as double
+  int n[3];
+};
+
+// Box / tile geometry of the binned gather.
+struct BinGeom {
+  int box[3];     // gather-box size in cells
+  int tile[3];    // staging-tile size in cells (multiple of box)
+  int ntile[3];   // tiles per axis = ceil(n / tile)
+  int nbox[3];    // boxes per tile per axis
+  int boxes_per_tile;
+  int64_t ntiles;
+  int64_t nboxes;  // ntiles * boxes_per_tile
+};
+
+// Window polynomial table: w_j(delta) = sum_d coef[j*(deg+1) + d] delta^d,
+// j = 0..2m (offset c = j - m), approximating phi(delta - c) (nufft.py:159-164).
+struct WindowPoly {
+  int m = 0;
+  int deg = 0;
+  double* dev = nullptr;  // (2m+1)*(deg+1) doubles
+};
+
+}  // namespace vfn
+
+struct vfn_plan {
+  int device = 0;
+  int64_t N[3] = {0, 0, 0};
+  int64_t n[3] = {0, 0, 0};
+  double a[3], b[3];
+  double sigma = 2.0;
+  int m = 6;
+  double beta = 0.0;
+  vfn::TorusMap map;
+  vfn::WindowPoly poly;
+  // ghost-padded grid: P_d = ntile_d * tile_d + 2m, element (i0,i1,i2) holds
+  // g[(i0-m) mod n0, (i1-m) mod n1, (i2-m) mod n2]
+  int64_t P[3] = {0, 0, 0};
+  int pad_tile[3] = {8, 8, 8};  // grid padded to multiples of this
+  double2* grid = nullptr;
+  int gather_variant = 0;
+  // evaluate scratch (grow-only)
+  vfn::DevBuf pts, out, keys, keys_sorted, idx, perm, sort_tmp, box_start, items, misc;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  float last_gather_ms = 0.f, last_total_ms = 0.f;
+};
+
+namespace vfn {
+
+// ---------------------------------------------------------------- host math (vfn_host.cpp)
+double kb_beta(int m, double sigma);
+double bessel_i0(double x);
+// phi_hat(k) for k = j - N/2, j = 0..N-1 (nufft.py:167-176)
+void kb_hat_table(int64_t N, int64_t n, int m, double beta, double* out);
+// fit the window polynomials; returns degree, fills coef ((2m+1)*(deg+1))
+int fit_window_poly(int m, double beta, double* coef, int max_deg);
+
+// ---------------------------------------------------------------- launchers
+int build_grid(vfn_plan* p, const double* coeffs_dev, cudaStream_t s);
+int map_and_key(vfn_plan* p, const double* pts_dev, int64_t M, const BinGeom& g, uint32_t* keys,
+                int32_t* iota, int64_t* bad_dev, cudaStream_t s);
+int sort_pairs(vfn_plan* p, const uint32_t* keys_in, uint32_t* keys_out, const int32_t* vals_in,
+               int32_t* vals_out, int64_t M, int key_bits, cudaStream_t s);
+int launch_torus(const TorusMap& tm, const double* pts, int64_t M, double* zeta, cudaStream_t s);
+int gather_simple(vfn_plan* p, const double* pts_dev, int64_t M, const int32_t* perm,
+                  double2* out_dev, cudaStream_t s);
+int gather_boxes(vfn_plan* p, const double* pts_dev, int64_t M, const BinGeom& g,
+                 const uint32_t* keys_sorted, const int32_t* perm, double2* out_dev,
+                 cudaStream_t s, bool* used);
+int rect_eval(int device, const int64_t nmodes[3], const double a[3], const double b[3],
+              const double* coeffs, const double* y[3], const int64_t Mv[3], double* out,
+              int on_device, cudaStream_t s);
+
+BinGeom choose_geometry(const vfn_plan* p, int64_t M);
+
+}  // namespace vfn

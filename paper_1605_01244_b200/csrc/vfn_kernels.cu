@@ -1,0 +1,325 @@
+// Point mapping / binning (K0+K1), grid build (K2 deconvolve+pad, K3 cuFFT,
+// K3b ghost padding) and the simple thread-per-point gather (K4 v1).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "vfn_device.cuh"
+
+namespace vfn {
+
+// ------------------------------------------------------------------ K0 + K1
+// One pass over the points: domain check (first bad row by atomicMin,
+// nufft.py:115-126), nearest cell per axis, and the bin key.
+__global__ void k_map_key(const double* __restrict__ pts, int64_t M, TorusMap tm, BinGeom g,
+                          uint32_t* __restrict__ keys, int32_t* __restrict__ iota,
+                          unsigned long long* __restrict__ bad) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  int cell[3];
+  bool ok = true;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    double x = pts[3 * i + d];
+    ok = ok && inside(x, tm.a[d], tm.b[d]);
+    double delta;
+    cell[d] = nearest_cell(x, tm.a[d], tm.amb[d], tm.nd[d], tm.n[d], delta);
+  }
+  if (!ok) {
+    atomicMin(bad, (unsigned long long)i);
+    cell[0] = cell[1] = cell[2] = 0;  // any in-range key; the call fails anyway
+  }
+  int t[3], in[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    t[d] = cell[d] / g.tile[d];
+    in[d] = (cell[d] - t[d] * g.tile[d]) / g.box[d];
+  }
+  int64_t tile_id = ((int64_t)t[0] * g.ntile[1] + t[1]) * g.ntile[2] + t[2];
+  int box_id = (in[0] * g.nbox[1] + in[1]) * g.nbox[2] + in[2];
+  keys[i] = (uint32_t)(tile_id * g.boxes_per_tile + box_id);
+  if (iota) iota[i] = (int32_t)i;
+}
+
+__global__ void k_torus(const double* __restrict__ pts, int64_t M, TorusMap tm,
+                        double* __restrict__ zeta) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * M) return;
+  int d = (int)(i % 3);
+  zeta[i] = torus_coord(pts[i], tm.a[d], tm.amb[d]);
+}
+
+int map_and_key(vfn_plan* p, const double* pts, int64_t M, const BinGeom& g, uint32_t* keys,
+                int32_t* iota, int64_t* bad_dev, cudaStream_t s) {
+  if (M == 0) return VFN_OK;
+  int threads = 256;
+  int64_t blocks = (M + threads - 1) / threads;
+  k_map_key<<<(unsigned)blocks, threads, 0, s>>>(pts, M, p->map, g, keys, iota,
+                                                  reinterpret_cast<unsigned long long*>(bad_dev));
+  VFN_CUDA(cudaGetLastError());
+  return VFN_OK;
+}
+
+int launch_torus(const TorusMap& tm, const double* pts, int64_t M, double* zeta, cudaStream_t s) {
+  if (M == 0) return VFN_OK;
+  int threads = 256;
+  int64_t blocks = (3 * M + threads - 1) / threads;
+  k_torus<<<(unsigned)blocks, threads, 0, s>>>(pts, M, tm, zeta);
+  VFN_CUDA(cudaGetLastError());
+  return VFN_OK;
+}
+
+int sort_pairs(vfn_plan* p, const uint32_t* keys_in, uint32_t* keys_out, const int32_t* vals_in,
+               int32_t* vals_out, int64_t M, int key_bits, cudaStream_t s) {
+  size_t tmp = 0;
+  VFN_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys_in, keys_out, vals_in, vals_out,
+                                           (int)M, 0, key_bits, s));
+  VFN_CHECK(p->sort_tmp.ensure(tmp));
+  VFN_CUDA(cub::DeviceRadixSort::SortPairs(p->sort_tmp.ptr, tmp, keys_in, keys_out, vals_in,
+                                           vals_out, (int)M, 0, key_bits, s));
+  return VFN_OK;
+}
+
+// ------------------------------------------------------------------ K2
+// Deconvolution fused with the octant zero-pad (nufft.py:219-241): every
+// element of the n1 x n2 x n3 FFT input is written once; mode k lands at
+// index k mod n with value coeff * sign(k) / (phihat1 phihat2 phihat3) / vol^(1/2) / prod n.
+// fac_d[j] carries sign(k_d) / phihat_d(k_d) for centred index j.
+__global__ void k_deconv_pad(const double2* __restrict__ coeffs, int64_t N0, int64_t N1,
+                             int64_t N2, int64_t n0, int64_t n1, int64_t n2,
+                             const double* __restrict__ fac0, const double* __restrict__ fac1,
+                             const double* __restrict__ fac2, double scale,
+                             double2* __restrict__ out) {
+  const int64_t total = n0 * n1 * n2;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i2 = e % n2;
+    int64_t r = e / n2;
+    int64_t i1 = r % n1;
+    int64_t i0 = r / n1;
+    // index i holds wavenumber i (i < N/2) or i - n (i >= n - N/2)
+    int64_t j0 = i0 < N0 / 2 ? i0 + N0 / 2 : (i0 >= n0 - N0 / 2 ? i0 - n0 + N0 / 2 : -1);
+    int64_t j1 = i1 < N1 / 2 ? i1 + N1 / 2 : (i1 >= n1 - N1 / 2 ? i1 - n1 + N1 / 2 : -1);
+    int64_t j2 = i2 < N2 / 2 ? i2 + N2 / 2 : (i2 >= n2 - N2 / 2 ? i2 - n2 + N2 / 2 : -1);
+    double2 v = make_double2(0.0, 0.0);
+    if (j0 >= 0 && j1 >= 0 && j2 >= 0) {
+      double2 c = coeffs[(j0 * N1 + j1) * N2 + j2];
+      double f = fac0[j0] * fac1[j1] * fac2[j2] * scale;
+      v = make_double2(c.x * f, c.y * f);
+    }
+    out[e] = v;
+  }
+}
+
+// K3b: ghost-padded copy, P[i] = g[(i - m) mod n] per axis.
+__global__ void k_halo(const double2* __restrict__ g, int64_t n0, int64_t n1, int64_t n2,
+                       double2* __restrict__ P, int64_t P0, int64_t P1, int64_t P2, int m) {
+  const int64_t total = P0 * P1 * P2;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i2 = e % P2;
+    int64_t r = e / P2;
+    int64_t i1 = r % P1;
+    int64_t i0 = r / P1;
+    int64_t s0 = ((i0 - m) % n0 + n0) % n0;
+    int64_t s1 = ((i1 - m) % n1 + n1) % n1;
+    int64_t s2 = ((i2 - m) % n2 + n2) % n2;
+    P[e] = g[(s0 * n1 + s1) * n2 + s2];
+  }
+}
+
+// interior of the padded grid back to (n0, n1, n2)
+__global__ void k_unpad(const double2* __restrict__ P, int64_t P1, int64_t P2, int m,
+                        int64_t n0, int64_t n1, int64_t n2, double2* __restrict__ g) {
+  const int64_t total = n0 * n1 * n2;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i2 = e % n2;
+    int64_t r = e / n2;
+    int64_t i1 = r % n1;
+    int64_t i0 = r / n1;
+    g[e] = P[((i0 + m) * P1 + (i1 + m)) * P2 + (i2 + m)];
+  }
+}
+
+static int grid_blocks(int64_t total) {
+  int64_t b = (total + 255) / 256;
+  return (int)(b < 148 * 32 ? (b < 1 ? 1 : b) : 148 * 32);
+}
+
+int build_grid(vfn_plan* p, const double* coeffs_dev, cudaStream_t s) {
+  const int64_t N0 = p->N[0], N1 = p->N[1], N2 = p->N[2];
+  const int64_t n0 = p->n[0], n1 = p->n[1], n2 = p->n[2];
+  // sign(k)/phihat tables
+  std::vector<double> fac[3];
+  for (int d = 0; d < 3; ++d) {
+    fac[d].resize(p->N[d]);
+    kb_hat_table(p->N[d], p->n[d], p->m, p->beta, fac[d].data());
+    for (int64_t j = 0; j < p->N[d]; ++j) {
+      int64_t k = j - p->N[d] / 2;
+      double sign = (k % 2 == 0) ? 1.0 : -1.0;  // 1 - 2 (|k| mod 2)  (nufft.py:101-104)
+      fac[d][j] = sign / fac[d][j];
+    }
+  }
+  const double vol = (p->b[0] - p->a[0]) * (p->b[1] - p->a[1]) * (p->b[2] - p->a[2]);
+  const double scale = 1.0 / std::sqrt(vol) / ((double)n0 * (double)n1 * (double)n2);
+
+  double* dfac = nullptr;
+  double2* buf = nullptr;
+  cufftHandle plan = 0;
+  bool have_plan = false;
+  int status = VFN_OK;
+  auto cleanup = [&]() {
+    if (have_plan) cufftDestroy(plan);
+    if (buf) cudaFree(buf);
+    if (dfac) cudaFree(dfac);
+  };
+  const int64_t total = n0 * n1 * n2;
+  cudaError_t e = cudaMalloc(&dfac, sizeof(double) * (N0 + N1 + N2));
+  if (e == cudaSuccess) e = cudaMalloc(&buf, sizeof(double2) * total);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    cleanup();
+    return fail(VFN_ERR_NOMEM, std::string("grid allocation failed: ") + cudaGetErrorString(e));
+  }
+  std::vector<double> h(N0 + N1 + N2);
+  std::copy(fac[0].begin(), fac[0].end(), h.begin());
+  std::copy(fac[1].begin(), fac[1].end(), h.begin() + N0);
+  std::copy(fac[2].begin(), fac[2].end(), h.begin() + N0 + N1);
+  e = cudaMemcpyAsync(dfac, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) {
+    k_deconv_pad<<<grid_blocks(total), 256, 0, s>>>(
+        reinterpret_cast<const double2*>(coeffs_dev), N0, N1, N2, n0, n1, n2, dfac, dfac + N0,
+        dfac + N0 + N1, scale, buf);
+    e = cudaGetLastError();
+  }
+  if (e != cudaSuccess) {
+    cleanup();
+    return fail(VFN_ERR_CUDA, std::string("deconvolve/pad: ") + cudaGetErrorString(e));
+  }
+  // K3: unnormalised forward 3D FFT (nufft.py:242)
+  cufftResult r = cufftPlan3d(&plan, (int)n0, (int)n1, (int)n2, CUFFT_Z2Z);
+  if (r == CUFFT_SUCCESS) {
+    have_plan = true;
+    r = cufftSetStream(plan, s);
+  }
+  if (r == CUFFT_SUCCESS)
+    r = cufftExecZ2Z(plan, reinterpret_cast<cufftDoubleComplex*>(buf),
+                     reinterpret_cast<cufftDoubleComplex*>(buf), CUFFT_FORWARD);
+  if (r != CUFFT_SUCCESS) {
+    cleanup();
+    return fail(VFN_ERR_CUFFT, "cuFFT Z2Z forward failed (code " + std::to_string((int)r) + ")");
+  }
+  // K3b: ghost padding
+  const int64_t Ptot = p->P[0] * p->P[1] * p->P[2];
+  e = cudaMalloc(&p->grid, sizeof(double2) * Ptot);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    p->grid = nullptr;
+    cleanup();
+    return fail(VFN_ERR_NOMEM, std::string("padded grid allocation failed: ") + cudaGetErrorString(e));
+  }
+  k_halo<<<grid_blocks(Ptot), 256, 0, s>>>(buf, n0, n1, n2, p->grid, p->P[0], p->P[1], p->P[2],
+                                           p->m);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) status = fail(VFN_ERR_CUDA, std::string("grid build: ") + cudaGetErrorString(e));
+  cleanup();
+  return status;
+}
+
+int extract_grid(vfn_plan* p, double2* out_dev, cudaStream_t s) {
+  const int64_t total = p->n[0] * p->n[1] * p->n[2];
+  k_unpad<<<grid_blocks(total), 256, 0, s>>>(p->grid, p->P[1], p->P[2], p->m, p->n[0], p->n[1],
+                                             p->n[2], out_dev);
+  VFN_CUDA(cudaGetLastError());
+  return VFN_OK;
+}
+
+// ------------------------------------------------------------------ K4 v1
+// Thread per point (in binned order when a permutation is given): window
+// weights from the polynomial table, then the separable (2m+1)^3 contraction
+// in the reference's order, axis 3 innermost (nufft.py:264-271).
+template <int MC>
+__global__ void __launch_bounds__(128) k_gather_simple(const double* __restrict__ pts, int64_t M,
+                                                       const int32_t* __restrict__ perm,
+                                                       TorusMap tm, const double* __restrict__ poly,
+                                                       int deg, const double2* __restrict__ grid,
+                                                       int64_t P1, int64_t P2,
+                                                       double2* __restrict__ out) {
+  constexpr int W = 2 * MC + 1;
+  extern __shared__ double s_poly[];
+  for (int i = threadIdx.x; i < W * (deg + 1); i += blockDim.x) s_poly[i] = poly[i];
+  __syncthreads();
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= M) return;
+  int64_t p = perm ? (int64_t)perm[s] : s;
+  double w[3][W];
+  int cell[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    double delta;
+    cell[d] = nearest_cell(pts[3 * p + d], tm.a[d], tm.amb[d], tm.nd[d], tm.n[d], delta);
+#pragma unroll
+    for (int j = 0; j < W; ++j) w[d][j] = window_poly(s_poly, deg, j, delta);
+  }
+  // padded index of grid cell (c - m + j) is c + j
+  const double2* base = grid + ((int64_t)cell[0] * P1 + cell[1]) * P2 + cell[2];
+  double ar = 0.0, ai = 0.0;
+  for (int a = 0; a < W; ++a) {
+    double br = 0.0, bi = 0.0;
+    for (int b = 0; b < W; ++b) {
+      const double2* row = base + ((int64_t)a * P1 + b) * P2;
+      double cr = 0.0, ci = 0.0;
+#pragma unroll
+      for (int c = 0; c < W; ++c) {
+        double2 v = __ldg(row + c);
+        cr = fma(w[2][c], v.x, cr);
+        ci = fma(w[2][c], v.y, ci);
+      }
+      br = fma(w[1][b], cr, br);
+      bi = fma(w[1][b], ci, bi);
+    }
+    ar = fma(w[0][a], br, ar);
+    ai = fma(w[0][a], bi, ai);
+  }
+  out[p] = make_double2(ar, ai);
+}
+
+template <int MC>
+static void launch_simple(vfn_plan* pl, const double* pts, int64_t M, const int32_t* perm,
+                          double2* out, cudaStream_t s) {
+  int threads = 128;
+  int64_t blocks = (M + threads - 1) / threads;
+  size_t smem = sizeof(double) * (2 * MC + 1) * (pl->poly.deg + 1);
+  k_gather_simple<MC><<<(unsigned)blocks, threads, smem, s>>>(
+      pts, M, perm, pl->map, pl->poly.dev, pl->poly.deg, pl->grid, pl->P[1], pl->P[2], out);
+}
+
+int gather_simple(vfn_plan* p, const double* pts, int64_t M, const int32_t* perm, double2* out,
+                  cudaStream_t s) {
+  if (M == 0) return VFN_OK;
+  switch (p->m) {
+    case 1: launch_simple<1>(p, pts, M, perm, out, s); break;
+    case 2: launch_simple<2>(p, pts, M, perm, out, s); break;
+    case 3: launch_simple<3>(p, pts, M, perm, out, s); break;
+    case 4: launch_simple<4>(p, pts, M, perm, out, s); break;
+    case 5: launch_simple<5>(p, pts, M, perm, out, s); break;
+    case 6: launch_simple<6>(p, pts, M, perm, out, s); break;
+    case 7: launch_simple<7>(p, pts, M, perm, out, s); break;
+    case 8: launch_simple<8>(p, pts, M, perm, out, s); break;
+    case 9: launch_simple<9>(p, pts, M, perm, out, s); break;
+    case 10: launch_simple<10>(p, pts, M, perm, out, s); break;
+    case 11: launch_simple<11>(p, pts, M, perm, out, s); break;
+    case 12: launch_simple<12>(p, pts, M, perm, out, s); break;
+    case 13: launch_simple<13>(p, pts, M, perm, out, s); break;
+    default: return fail(VFN_ERR_INVALID, "cutoff must be in 1..13");
+  }
+  VFN_CUDA(cudaGetLastError());
+  return VFN_OK;
+}
+
+}  // namespace vfn

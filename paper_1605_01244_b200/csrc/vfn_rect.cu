@@ -1,0 +1,140 @@
+// K5: rectilinear tensor-grid evaluation (rectilinear.py:47-64) as three
+// exact separable 1D non-uniform passes.  Each pass contracts one mode with
+// its basis matrix E_d[m, k] = exp(2 pi i (y_m - a)(k - N/2)/(b - a))/sqrt(b - a)
+// (rectilinear.py:22-44), generated on the device; the contractions are plain
+// complex GEMMs (cuBLAS ZGEMM, FP64 tensor-core DMMA on sm_100a).
+#include <cublas_v2.h>
+
+#include <map>
+#include <mutex>
+
+#include "vfn_internal.cuh"
+
+namespace vfn {
+
+__global__ void k_basis(const double* __restrict__ y, int64_t M, int64_t N, double a, double width,
+                        double2* __restrict__ E) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= M * N) return;
+  int64_t m = e / N;
+  int64_t k = e % N - N / 2;
+  // phase / pi = 2 (y - a) k / (b - a); sincospi reduces the argument exactly
+  double t = (y[m] - a) / width;
+  double s, c;
+  sincospi(2.0 * t * (double)k, &s, &c);
+  double r = rsqrt(width);
+  E[e] = make_double2(c * r, s * r);
+}
+
+static cublasHandle_t handle_for(int device) {
+  static std::mutex mu;
+  static std::map<int, cublasHandle_t> handles;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = handles.find(device);
+  if (it != handles.end()) return it->second;
+  cublasHandle_t h = nullptr;
+  if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
+  cublasSetMathMode(h, CUBLAS_DEFAULT_MATH);
+  handles[device] = h;
+  return h;
+}
+
+#define VFN_BLAS(expr)                                                                        \
+  do {                                                                                        \
+    cublasStatus_t _b = (expr);                                                               \
+    if (_b != CUBLAS_STATUS_SUCCESS) {                                                        \
+      st = fail(VFN_ERR_CUBLAS, std::string(#expr) + " failed (" + std::to_string((int)_b) + ")"); \
+      goto done;                                                                              \
+    }                                                                                         \
+  } while (0)
+
+int rect_eval(int device, const int64_t nm[3], const double a[3], const double b[3],
+              const double* coeffs, const double* y[3], const int64_t Mv[3], double* out,
+              int on_device, cudaStream_t s) {
+  cublasHandle_t h = handle_for(device);
+  if (!h) return fail(VFN_ERR_CUBLAS, "cublasCreate failed");
+  const int64_t N0 = nm[0], N1 = nm[1], N2 = nm[2];
+  const int64_t M0 = Mv[0], M1 = Mv[1], M2 = Mv[2];
+  const size_t cb = sizeof(double2) * N0 * N1 * N2;
+  const size_t t1b = sizeof(double2) * N0 * N1 * M2;
+  const size_t t2b = sizeof(double2) * N0 * M1 * M2;
+  const size_t fb = sizeof(double2) * M0 * M1 * M2;
+  const size_t eb[3] = {sizeof(double2) * M0 * N0, sizeof(double2) * M1 * N1,
+                        sizeof(double2) * M2 * N2};
+  DevBuf C, T1, T2, F, E[3], Y[3];
+  int st = VFN_OK;
+  const double2 one = make_double2(1.0, 0.0), zero = make_double2(0.0, 0.0);
+  const double2* Cd = reinterpret_cast<const double2*>(coeffs);
+  double2* Fd = reinterpret_cast<double2*>(out);
+  const double* yd[3];
+  if (!on_device) {
+    if ((st = C.ensure(cb)) != VFN_OK) goto done;
+    if (cudaMemcpyAsync(C.ptr, coeffs, cb, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+      st = fail(VFN_ERR_CUDA, "coefficient upload failed");
+      goto done;
+    }
+    Cd = C.as<double2>();
+    if ((st = F.ensure(fb)) != VFN_OK) goto done;
+    Fd = F.as<double2>();
+  }
+  for (int d = 0; d < 3; ++d) {
+    yd[d] = y[d];
+    if (!on_device) {
+      if ((st = Y[d].ensure(sizeof(double) * Mv[d])) != VFN_OK) goto done;
+      if (cudaMemcpyAsync(Y[d].ptr, y[d], sizeof(double) * Mv[d], cudaMemcpyHostToDevice, s) !=
+          cudaSuccess) {
+        st = fail(VFN_ERR_CUDA, "coordinate upload failed");
+        goto done;
+      }
+      yd[d] = Y[d].as<double>();
+    }
+    if ((st = E[d].ensure(eb[d])) != VFN_OK) goto done;
+    {
+      int64_t tot = Mv[d] * nm[d];
+      k_basis<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(yd[d], Mv[d], nm[d], a[d], b[d] - a[d],
+                                                           E[d].as<double2>());
+    }
+  }
+  if ((st = T1.ensure(t1b)) != VFN_OK) goto done;
+  if ((st = T2.ensure(t2b)) != VFN_OK) goto done;
+  VFN_BLAS(cublasSetStream(h, s));
+  {
+    auto* e0 = reinterpret_cast<const cuDoubleComplex*>(E[0].ptr);
+    auto* e1 = reinterpret_cast<const cuDoubleComplex*>(E[1].ptr);
+    auto* e2 = reinterpret_cast<const cuDoubleComplex*>(E[2].ptr);
+    auto* al = reinterpret_cast<const cuDoubleComplex*>(&one);
+    auto* be = reinterpret_cast<const cuDoubleComplex*>(&zero);
+    // pass 1, mode 3: T1 (N0N1 x M2) = C (N0N1 x N2) E2^T
+    VFN_BLAS(cublasZgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)M2, (int)(N0 * N1), (int)N2, al, e2,
+                         (int)N2, reinterpret_cast<const cuDoubleComplex*>(Cd), (int)N2, be,
+                         T1.as<cuDoubleComplex>(), (int)M2));
+    // pass 2, mode 2 (batched over n0): T2_n0 (M1 x M2) = E1 (M1 x N1) T1_n0 (N1 x M2)
+    VFN_BLAS(cublasZgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)M2, (int)M1, (int)N1, al,
+                                       T1.as<cuDoubleComplex>(), (int)M2, N1 * M2, e1, (int)N1, 0,
+                                       be, T2.as<cuDoubleComplex>(), (int)M2, M1 * M2, (int)N0));
+    // pass 3, mode 1: F (M0 x M1M2) = E0 (M0 x N0) T2 (N0 x M1M2)
+    VFN_BLAS(cublasZgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)(M1 * M2), (int)M0, (int)N0, al,
+                         T2.as<cuDoubleComplex>(), (int)(M1 * M2), e0, (int)N0, be,
+                         reinterpret_cast<cuDoubleComplex*>(Fd), (int)(M1 * M2)));
+  }
+  if (!on_device && cudaMemcpyAsync(out, Fd, fb, cudaMemcpyDeviceToHost, s) != cudaSuccess) {
+    st = fail(VFN_ERR_CUDA, "result download failed");
+    goto done;
+  }
+  {
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) st = fail(VFN_ERR_CUDA, std::string("rectilinear: ") + cudaGetErrorString(e));
+  }
+done:
+  C.release();
+  T1.release();
+  T2.release();
+  F.release();
+  for (int d = 0; d < 3; ++d) {
+    E[d].release();
+    Y[d].release();
+  }
+  return st;
+}
+
+}  // namespace vfn

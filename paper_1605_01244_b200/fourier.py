@@ -1,0 +1,92 @@
+"""Boundary types of the hot path, with the reference's names and checks.
+
+`DomainBox` and `SpectralField` mirror the reference's types
+(fourier.py:56-91, :147-164, value checks :118-125) so that callers of the
+reference evaluators can pass the same objects.  Any object with `.a`/`.b`
+(domain) or `.domain`/`.coeffs` (field) attributes is accepted by duck typing,
+so reference instances work unchanged.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = ["DomainBox", "SpectralField", "regular_grid"]
+
+
+@dataclass(frozen=True)
+class DomainBox:
+    """Axis-aligned half-open box prod_d [a_d, b_d) (fourier.py:56-91)."""
+
+    a: tuple
+    b: tuple
+
+    def __post_init__(self):
+        a = tuple(float(v) for v in self.a)
+        b = tuple(float(v) for v in self.b)
+        if len(a) != 3 or len(b) != 3:
+            raise ValueError("DomainBox needs exactly three bounds per side")
+        for d in range(3):
+            if not (np.isfinite(a[d]) and np.isfinite(b[d])):
+                raise ValueError("domain bounds must be finite")
+            if not a[d] < b[d]:
+                raise ValueError(
+                    f"domain bounds must satisfy a < b, got [{a[d]}, {b[d]}) in direction {d}"
+                )
+        object.__setattr__(self, "a", a)
+        object.__setattr__(self, "b", b)
+
+    @property
+    def widths(self) -> np.ndarray:
+        return np.array(self.b) - np.array(self.a)
+
+    @property
+    def volume(self) -> float:
+        return float(np.prod(self.widths))
+
+    def contains(self, points: np.ndarray) -> np.ndarray:
+        pts = np.atleast_2d(np.asarray(points, dtype=float))
+        return np.all((pts >= np.asarray(self.a)) & (pts < np.asarray(self.b)), axis=1)
+
+
+def _check_values(values):
+    # fourier.py:118-125; CUDA torch tensors are kept on the device
+    mod = type(values).__module__
+    if mod.startswith("torch") and getattr(values, "is_cuda", False):
+        import torch
+
+        if values.dim() != 3:
+            raise ValueError(f"expected a 3D array, got shape {tuple(values.shape)}")
+        if any(v % 2 for v in values.shape):
+            raise ValueError(f"array dimensions must be even, got shape {tuple(values.shape)}")
+        return values.to(torch.complex128).contiguous()
+    values = np.asarray(values)
+    if values.ndim != 3:
+        raise ValueError(f"expected a 3D array, got shape {values.shape}")
+    for v in values.shape:
+        if v % 2 != 0:
+            raise ValueError(f"array dimensions must be even, got shape {values.shape}")
+    return np.ascontiguousarray(values, dtype=np.complex128)
+
+
+@dataclass(frozen=True)
+class SpectralField:
+    """Centred-order Fourier coefficients on a DomainBox (fourier.py:147-164)."""
+
+    domain: DomainBox
+    coeffs: np.ndarray
+
+    def __post_init__(self):
+        object.__setattr__(self, "coeffs", _check_values(self.coeffs))
+
+    def wavenumbers(self, axis: int) -> np.ndarray:
+        n = self.coeffs.shape[axis]
+        return np.arange(n) - n // 2
+
+
+def regular_grid(domain, size) -> list:
+    """x_d = a_d + j h_d, j = 0..N_d-1 (fourier.py:167-180)."""
+    size = tuple(int(v) for v in size)
+    return [np.linspace(domain.a[d], domain.b[d], size[d] + 1)[: size[d]] for d in range(3)]

@@ -1,0 +1,49 @@
+import os
+import sys
+
+import numpy as np
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if REPO not in sys.path:
+    sys.path.insert(0, REPO)
+
+GOLDEN = os.path.join(REPO, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and libvfnfft.so")
+
+
+def golden(name):
+    return np.load(os.path.join(GOLDEN, name))
+
+
+@pytest.fixture(scope="session")
+def unit_box():
+    from paper_1605_01244_b200 import DomainBox
+
+    return DomainBox((0.0, 0.0, 0.0), (1.0, 1.0, 1.0))
+
+
+@pytest.fixture(scope="session")
+def offset_box():
+    """Unequal widths and a shifted origin (reference tests/conftest.py:12-15)."""
+    from paper_1605_01244_b200 import DomainBox
+
+    return DomainBox((-1.5, 0.25, 2.0), (2.5, 1.25, 7.0))
+
+
+def random_spectral(domain, shape, seed):
+    from paper_1605_01244_b200 import SpectralField
+
+    rng = np.random.default_rng(seed)
+    return SpectralField(domain, rng.standard_normal(shape) + 1j * rng.standard_normal(shape))
+
+
+def rel_err(x, ref):
+    x = np.asarray(x)
+    ref = np.asarray(ref)
+    l2 = np.linalg.norm(x - ref) / np.linalg.norm(ref)
+    linf = np.abs(x - ref).max() / np.abs(ref).max()
+    return l2, linf

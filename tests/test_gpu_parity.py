@@ -1,0 +1,295 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the CPU oracle, on the same seeded inputs.
+
+Tolerances: integer/index work (torus map, nearest cell, bin key,
+permutation) is bit-exact; floating point must match the reference within
+1e-10 relative l2 / l-inf (north star), and in practice lands near 1e-14,
+which is what most asserts below pin.
+"""
+
+import warnings
+
+import numpy as np
+import pytest
+
+from conftest import golden, random_spectral, rel_err
+from oracle import nfft_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10  # north-star gate (relative l2 and l-inf vs the reference)
+
+
+@pytest.fixture(scope="module")
+def vfb():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1605_01244_b200 as pkg
+
+    return pkg
+
+
+def cases():
+    g = golden("nufft_cases.npz")
+    out = []
+    for i in range(int(g["ncases"])):
+        out.append({k.split("_", 1)[1]: g[k] for k in g.files if k.startswith(f"case{i}_")})
+    return out
+
+
+CASES = cases()
+
+
+def make_plan(vfb, c):
+    sigma, m = float(c["params"][0]), int(c["params"][1])
+    spec = vfb.SpectralField(vfb.DomainBox(tuple(c["a"]), tuple(c["b"])), c["coeffs"])
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        return spec, vfb.NufftPlan(spec, vfb.NufftParams(oversampling=sigma, cutoff=m, eps=0.999))
+
+
+# ---------------------------------------------------------------- K1 (bit-exact)
+
+
+def test_map_to_torus_bit_exact(vfb):
+    g = golden("torus_edges.npz")
+    box = vfb.DomainBox(tuple(g["a"]), tuple(g["b"]))
+    zeta = vfb.map_to_torus(g["points"], box)
+    np.testing.assert_array_equal(zeta, g["zeta"])
+
+
+def test_bin_sort_bit_exact_vs_cpu_stable_sort(vfb, offset_box):
+    g = golden("torus_edges.npz")
+    spec = random_spectral(vfb.DomainBox(tuple(g["a"]), tuple(g["b"])), (16, 16, 16), 7)
+    plan = vfb.NufftPlan(spec)
+    rng = np.random.default_rng(11)
+    pts = np.vstack([g["points"], rng.uniform(g["a"], g["b"], (20000, 3))])
+    keys, perm = plan.bin(pts)
+    box, tile = plan.geometry(len(pts))
+    ref_keys = O.bin_keys(pts, g["a"], g["b"], plan._n, box, tile)
+    np.testing.assert_array_equal(keys.astype(np.int64), ref_keys)
+    np.testing.assert_array_equal(perm, np.argsort(ref_keys, kind="stable"))
+
+
+def test_bin_sort_bit_exact_clustered(vfb):
+    g = golden("cluster_small.npz")
+    from paper_1605_01244_b200 import workloads
+
+    box = vfb.DomainBox(*workloads.VORTEX_BOX)
+    plan = vfb.NufftPlan(vfb.SpectralField(box, g["coeffs"]))
+    keys, perm = plan.bin(g["points"])
+    bx, tl = plan.geometry(len(g["points"]))
+    ref = O.bin_keys(g["points"], box.a, box.b, plan._n, bx, tl)
+    np.testing.assert_array_equal(keys.astype(np.int64), ref)
+    np.testing.assert_array_equal(perm, np.argsort(ref, kind="stable"))
+
+
+# ---------------------------------------------------------------- K2 + K3
+
+
+@pytest.mark.parametrize("i", [i for i, c in enumerate(CASES) if "grid" in c])
+def test_plan_grid_matches_reference(vfb, i):
+    c = CASES[i]
+    _, plan = make_plan(vfb, c)
+    l2, linf = rel_err(plan._grid, c["grid"])
+    assert l2 < 1e-13 and linf < 1e-13, (l2, linf)
+
+
+# ---------------------------------------------------------------- K4 end to end
+
+
+@pytest.mark.parametrize("i", range(len(CASES)))
+def test_evaluate_matches_reference(vfb, i):
+    c = CASES[i]
+    spec, plan = make_plan(vfb, c)
+    out = plan.evaluate(c["points"])
+    l2, linf = rel_err(out, c["nufft"])
+    m = int(c["params"][1])
+    tol = 1e-13 if m >= 3 else 1e-11
+    assert l2 < tol and linf < tol, (l2, linf)
+    # the reference's own accuracy budget vs the exact sum (test_nufft.py:136-146)
+    if m >= 6:
+        mass = np.abs(vfb.rescale_coeffs(spec)).sum()
+        assert np.abs(out - c["direct"]).max() <= 1e-12 * mass
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+def test_gather_variants_agree(vfb, variant):
+    c = CASES[0]
+    _, plan = make_plan(vfb, c)
+    try:
+        plan.set_gather(variant)
+        out = plan.evaluate(c["points"])
+    except ValueError as e:
+        pytest.skip(str(e))
+    l2, linf = rel_err(out, c["nufft"])
+    assert l2 < 1e-13 and linf < 1e-13
+
+
+def test_config1_full(vfb):
+    from paper_1605_01244_b200 import workloads
+
+    g = golden("config1.npz")
+    spec = vfb.SpectralField(vfb.DomainBox(*workloads.UNIT_BOX), workloads.coefficients("c1"))
+    out = vfb.NufftPlan(spec).evaluate(workloads.points("c1"))
+    l2, linf = rel_err(out, g["nufft"])
+    assert l2 < 1e-13 and linf < 1e-13, (l2, linf)
+    l2, linf = rel_err(out[:200], g["direct200"])
+    assert l2 < 1e-12 and linf < 1e-12
+
+
+def test_cluster_seam(vfb):
+    from paper_1605_01244_b200 import workloads
+
+    g = golden("cluster_small.npz")
+    spec = vfb.SpectralField(vfb.DomainBox(*workloads.VORTEX_BOX), g["coeffs"])
+    out = vfb.NufftPlan(spec).evaluate(g["points"])
+    l2, linf = rel_err(out, g["nufft"])
+    assert l2 < 1e-13 and linf < 1e-13, (l2, linf)
+    l2, linf = rel_err(out[:100], g["direct"])
+    assert l2 < 1e-11 and linf < 1e-11
+
+
+def test_edge_points(vfb):
+    """zeta = +1/2 and l0 == n rows (survey fact 5) evaluate like the oracle."""
+    g = golden("torus_edges.npz")
+    box = vfb.DomainBox(tuple(g["a"]), tuple(g["b"]))
+    spec = random_spectral(box, (16, 16, 16), 9)
+    out = vfb.NufftPlan(spec).evaluate(g["points"])
+    ref = O.nufft_eval(spec.coeffs, g["a"], g["b"], g["points"])
+    l2, linf = rel_err(out, ref)
+    assert l2 < 1e-13 and linf < 1e-13
+
+
+# ---------------------------------------------------------------- determinism / API
+
+
+def test_plan_reuse_is_bitwise_stable(vfb, offset_box):
+    spec = random_spectral(offset_box, (12, 12, 12), 81)
+    rng = np.random.default_rng(82)
+    pts_a = rng.uniform(offset_box.a, offset_box.b, (40, 3))
+    pts_b = rng.uniform(offset_box.a, offset_box.b, (25, 3))
+    plan = vfb.NufftPlan(spec)
+    first = plan.evaluate(pts_a)
+    plan.evaluate(pts_b)
+    np.testing.assert_array_equal(first, plan.evaluate(pts_a))
+    np.testing.assert_array_equal(first, vfb.eval_nufft(spec, pts_a))
+
+
+def test_batch_composition_invariance(vfb, offset_box):
+    """A point's value does not depend on which other points share the call."""
+    spec = random_spectral(offset_box, (16, 16, 16), 90)
+    rng = np.random.default_rng(91)
+    pts = rng.uniform(offset_box.a, offset_box.b, (30000, 3))
+    plan = vfb.NufftPlan(spec)
+    full = plan.evaluate(pts)
+    np.testing.assert_array_equal(full[:777], plan.evaluate(pts[:777]))
+    sel = rng.permutation(len(pts))[:5000]
+    np.testing.assert_array_equal(full[sel], plan.evaluate(pts[sel]))
+
+
+def test_torch_cuda_tensors_match_numpy(vfb, offset_box):
+    import torch
+
+    spec = random_spectral(offset_box, (16, 16, 16), 92)
+    rng = np.random.default_rng(93)
+    pts = rng.uniform(offset_box.a, offset_box.b, (5000, 3))
+    host = vfb.NufftPlan(spec).evaluate(pts)
+    dspec = vfb.SpectralField(offset_box, torch.as_tensor(spec.coeffs, device="cuda"))
+    dev = vfb.NufftPlan(dspec).evaluate(torch.as_tensor(pts, device="cuda"))
+    assert dev.is_cuda and dev.dtype == torch.complex128
+    np.testing.assert_array_equal(dev.cpu().numpy(), host)
+
+
+def test_empty_and_outside(vfb, unit_box):
+    spec = random_spectral(unit_box, (8, 8, 8), 83)
+    plan = vfb.NufftPlan(spec)
+    out = plan.evaluate(np.empty((0, 3)))
+    assert out.shape == (0,) and out.dtype == np.complex128
+    with pytest.raises(ValueError, match=r"point \[1.0, 0.5, 0.5\] \(row 0\) lies outside"):
+        plan.evaluate(np.array([[1.0, 0.5, 0.5]]))
+    with pytest.raises(ValueError, match=r"\(row 2\)"):
+        plan.evaluate(np.array([[0.1, 0.1, 0.1], [0.2, 0.2, 0.2], [np.nan, 0.5, 0.5], [2.0, 0, 0]]))
+    with pytest.raises(ValueError, match="outside"):
+        vfb.eval_direct(spec, np.array([[0.5, 0.5, 1.5]]))
+    # the plan stays usable after an error
+    assert plan.evaluate(np.array([[0.5, 0.5, 0.5]])).shape == (1,)
+
+
+def test_warnings_match_reference(vfb, unit_box):
+    spec = random_spectral(unit_box, (8, 8, 8), 57)
+    with pytest.warns(vfb.AccuracyWarning, match="degraded"):
+        vfb.NufftPlan(spec, vfb.NufftParams(cutoff=1))
+    with pytest.warns(vfb.AccuracyWarning, match="short of"):
+        vfb.NufftPlan(spec, vfb.NufftParams(cutoff=3, eps=1e-12))
+
+
+def test_error_decreases_with_cutoff(vfb, offset_box):
+    spec = random_spectral(offset_box, (16, 16, 16), 70)
+    rng = np.random.default_rng(2070)
+    pts = rng.uniform(offset_box.a, offset_box.b, (100, 3))
+    ref = vfb.eval_direct(spec, pts)
+    errs = []
+    for m in (2, 3, 4, 6, 8):
+        out = vfb.NufftPlan(spec, vfb.NufftParams(cutoff=m, eps=0.999)).evaluate(pts)
+        errs.append(np.abs(out - ref).max())
+    for lo, hi in zip(errs[1:], errs[:-1]):
+        assert lo <= hi * 1.1
+
+
+# ---------------------------------------------------------------- K6 / K5
+
+
+@pytest.mark.parametrize("i", [0, 1, 5])
+def test_direct_matches_reference(vfb, i):
+    c = CASES[i]
+    spec = vfb.SpectralField(vfb.DomainBox(tuple(c["a"]), tuple(c["b"])), c["coeffs"])
+    out = vfb.eval_direct(spec, c["points"])
+    l2, linf = rel_err(out, c["direct"])
+    assert l2 < 1e-13 and linf < 1e-13
+
+
+def test_rectilinear_matches_reference(vfb):
+    g = golden("rect_cases.npz")
+    for i in range(int(g["ncases"])):
+        box = vfb.DomainBox(tuple(g[f"case{i}_a"]), tuple(g[f"case{i}_b"]))
+        spec = vfb.SpectralField(box, g[f"case{i}_coeffs"])
+        out = vfb.eval_rectilinear(spec, [g[f"case{i}_y{d}"] for d in range(3)])
+        ref = g[f"case{i}_out"]
+        assert out.shape == ref.shape
+        l2, linf = rel_err(out, ref)
+        assert l2 < 1e-13 and linf < 1e-13, (i, l2, linf)
+
+
+def test_rectilinear_regular_grid_matches_fft(vfb, offset_box):
+    spec = random_spectral(offset_box, (12, 12, 12), 43)
+    axes = vfb.regular_grid(offset_box, spec.coeffs.shape)
+    out = vfb.eval_rectilinear(spec, axes)
+    # inverse DFT on the regular grid (fourier.py:191-196)
+    n = np.array(spec.coeffs.shape)
+    scale = float(np.prod(np.sqrt(offset_box.widths) / n))
+    ref = np.fft.ifftn(np.fft.ifftshift(spec.coeffs)) / scale
+    assert np.abs(out - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+# ---------------------------------------------------------------- full-size properties
+
+
+def test_config2_full_size(vfb):
+    """BASELINE config 2 (64^3 modes, 1e6 points): a 20k-point subset against
+    the oracle, the whole batch for determinism and batch invariance."""
+    from paper_1605_01244_b200 import workloads
+
+    coeffs = workloads.coefficients("c2")
+    pts = workloads.points("c2")
+    a, b = workloads.UNIT_BOX
+    spec = vfb.SpectralField(vfb.DomainBox(a, b), coeffs)
+    plan = vfb.NufftPlan(spec)
+    out = plan.evaluate(pts)
+    sub = np.random.default_rng(0).choice(len(pts), 20000, replace=False)
+    ref = O.nufft_eval(coeffs, a, b, pts[sub])
+    l2, linf = rel_err(out[sub], ref)
+    assert l2 < TOL and linf < TOL
+    assert l2 < 1e-13 and linf < 1e-13, (l2, linf)
+    np.testing.assert_array_equal(out[sub], plan.evaluate(pts[sub]))
