@@ -1,0 +1,463 @@
+#!/usr/bin/env python
+"""3D NFFT trafo throughput (points/s, fp64 complex) on B200, with its FP64
+roofline fraction and the reference CPU path timed beside it.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5]
+    python bench.py --impl reference ...      # CPU reference arm (oracle port)
+
+A "step" is one `NufftPlan.evaluate` over the workload's points (all ranks
+together), i.e. validate + map + bin-sort + gather on a built plan — the
+reference's own plan/evaluate split (nufft.py:190-196).  The plan (deconvolve,
+pad, 3D FFT) is built once per rank and reported separately.
+
+* ``value``   — points/s with points and results resident in HBM;
+* ``e2e``     — the same through the public API with pinned HOST buffers, H2D of
+                the points and D2H of the results inside the timed region;
+* ``roofline``— the gather kernel's algorithmic FP64 rate (2[(2m+1)^3+(2m+1)^2
+                +(2m+1)] FMA per point) over its CUDA-event time, against the
+                DFMA peak measured on this device by vfn_bench_fp64_peak;
+* ``cpu_baseline`` — the oracle port of the reference (oracle/nfft_oracle.py,
+                numpy, fork-sharded over all host cores) on a bounded sample.
+
+Multi-GPU (torchrun): rank 0 builds the coefficients and NCCL-broadcasts them;
+every rank builds its own replicated plan and evaluates a contiguous 1/N shard
+of the points (no data-path collective).  Timing is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+from paper_1605_01244_b200 import workloads  # noqa: E402
+
+METRIC = "3D NFFT trafo points/sec (fp64 complex)"
+SIGMA, CUTOFF = 2.0, 6
+
+
+def fma_per_point(m: int) -> int:
+    w = 2 * m + 1
+    return w ** 3 + w ** 2 + w
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--workload", choices=["c1", "c2", "c3", "c5"], default="c5")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--gather", type=int, default=0, help="0 auto, 1 simple, 2 box/DMMA")
+    return p.parse_args()
+
+
+def workload_config(name: str, n_gpus: int) -> dict:
+    w = workloads.WORKLOADS[name]
+    return {
+        "workload": f"{name}: N={w.modes[0]}^3 complex128 coefficients, M={w.npoints} "
+        f"{'Gaussian-cloud' if w.kind == 'cluster' else 'uniform'} points on "
+        f"{list(w.box[0])}..{list(w.box[1])}, sigma={SIGMA}, m={CUTOFF}",
+        "modes": list(w.modes),
+        "points": w.npoints,
+        "sigma": SIGMA,
+        "m": CUTOFF,
+        "parallelism": f"points sharded over {n_gpus} GPU(s), oversampled grid replicated",
+        "l2_flush": "none needed: per-step inputs (points) exceed the 126 MB L2"
+        if w.npoints * 24 > 2 * 126e6
+        else "inputs smaller than L2 (warm-L2 number)",
+    }
+
+
+# ---------------------------------------------------------------- CPU side
+
+
+_G = {}
+
+
+def _cpu_worker(args):
+    lo, hi, deadline = args
+    from oracle import nfft_oracle as O
+
+    g = _G
+    pts = g["pts"][lo:hi]
+    outs = []
+    done = 0
+    chunk = 2048
+    while done < len(pts) and time.perf_counter() < deadline:
+        part = pts[done : done + chunk]
+        outs.append(O.gather_eval(g["grid"], g["n"], CUTOFF, g["beta"], part, g["a"], g["b"]))
+        done += len(part)
+    return lo, done, (np.concatenate(outs) if outs else np.empty(0, np.complex128))
+
+
+def cpu_port_run(name: str, coeffs: np.ndarray, seconds: float, sample_cap: int = 8_000_000):
+    """The reference algorithm (oracle port) fork-sharded over every host core
+    (SURVEY 8d mode B): plan once, then each worker gathers a contiguous slice
+    of a sample of the workload's points until `seconds` run out."""
+    import multiprocessing as mp
+
+    from oracle import nfft_oracle as O
+
+    w = workloads.WORKLOADS[name]
+    a, b = w.box
+    cores = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    grid, n, beta = O.oversampled_grid(coeffs, a, b, SIGMA, CUTOFF)
+    plan_s = time.perf_counter() - t0
+    budget = int(min(sample_cap, max(cores * 3e4 * seconds, 20000)))
+    pts = cpu_sample_points(name, budget)
+    _G.update(grid=grid, n=n, beta=beta, a=a, b=b, pts=pts)
+    bounds = np.linspace(0, len(pts), cores + 1).astype(int)
+    ctx = mp.get_context("fork")
+    t1 = time.perf_counter()
+    deadline = t1 + seconds
+    with ctx.Pool(cores) as pool:
+        res = pool.map(_cpu_worker, [(bounds[i], bounds[i + 1], deadline) for i in range(cores)])
+    elapsed = time.perf_counter() - t1
+    count = sum(r[1] for r in res)
+    idx = np.concatenate([np.arange(r[0], r[0] + r[1]) for r in res])
+    vals = np.concatenate([r[2] for r in res])
+    _G.clear()
+    return {
+        "value": count / elapsed,
+        "points": count,
+        "seconds": elapsed,
+        "cores": cores,
+        "plan_s": plan_s,
+        "sample_points": pts[idx],
+        "sample_values": vals,
+    }
+
+
+def cpu_sample_points(name: str, count: int) -> np.ndarray:
+    w = workloads.WORKLOADS[name]
+    if w.kind == "cluster":
+        return workloads.points(name, count)
+    rng = np.random.default_rng(4000 + int(name[1:]))
+    return rng.uniform(-0.5, 0.5, (count, 3))
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, index: int):
+        self.lines = []
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                power.append(float(parts[6]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {
+            "sm_mhz": float(np.median(sm)) if sm else None,
+            "sm_max_mhz": max(mx) if mx else None,
+            "reasons": sorted(reasons),
+            "samples": len(sm),
+            "power_w_max": max(power) if power else None,
+        }
+
+
+# ---------------------------------------------------------------- GPU side
+
+
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1605_01244_b200 as vfb
+    from paper_1605_01244_b200 import _lib
+    from paper_1605_01244_b200.parallel import broadcast_coefficients, shard_range
+
+    name = args.workload
+    w = workloads.WORKLOADS[name]
+    world, rank, local = dist_setup(args)
+    dev = torch.device("cuda", local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # CPU baseline first (rank 0, N=1 only), before this process touches CUDA
+    coeffs_host = workloads.coefficients(name) if rank == 0 else None
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_port_run(name, coeffs_host, args.cpu_seconds)
+
+    # coefficients: rank 0 -> all ranks over NCCL (the one exchange per plan)
+    if rank == 0:
+        coeffs_dev = torch.as_tensor(coeffs_host).to(dev)
+    else:
+        coeffs_dev = torch.empty(w.modes, dtype=torch.complex128, device=dev)
+    coeffs_dev = broadcast_coefficients(coeffs_dev, src=0, group=None if world > 1 else False)
+    spec = vfb.SpectralField(vfb.DomainBox(*w.box), coeffs_dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    plan = vfb.NufftPlan(spec, vfb.NufftParams(SIGMA, CUTOFF))
+    torch.cuda.synchronize()
+    plan_ms = max_over_ranks((time.perf_counter() - t0) * 1e3)
+    if args.gather:
+        plan.set_gather(args.gather)
+
+    # this rank's shard of the points, resident in HBM
+    lo, hi = shard_range(w.npoints, world, rank)
+    M = hi - lo
+    if name == "c5":
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(2005 + 7919 * rank)
+        pts = torch.rand((M, 3), dtype=torch.float64, device=dev, generator=gen) - 0.5
+    else:
+        pts = torch.as_tensor(workloads.points(name)[lo:hi]).to(dev)
+    out = torch.empty(M, dtype=torch.complex128, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- device-resident timing
+    for _ in range(args.warmup):
+        plan.evaluate(pts, out=out)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(dev.index if dev.index is not None else 0)
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    gather_ms = []
+    e0.record(stream)
+    for _ in range(args.steps):
+        plan.evaluate(pts, out=out)
+        gather_ms.append(plan.last_timing()[0])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    step_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    g_ms = max_over_ranks(float(np.mean(gather_ms)))
+
+    # ---- end to end through the public API: pinned host in, pinned host out
+    pts_host = torch.empty((M, 3), dtype=torch.float64, pin_memory=True)
+    pts_host.copy_(pts)
+    out_host = torch.empty(M, dtype=torch.complex128, pin_memory=True)
+    pts_np, out_np = pts_host.numpy(), out_host.numpy()
+    plan.evaluate(pts_np, out=out_np)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = []
+    for _ in range(max(2, min(args.steps, 5))):
+        t0 = time.perf_counter()
+        plan.evaluate(pts_np, out=out_np)  # returns after the D2H has landed
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_step = max_over_ranks(float(np.mean(e2e_ms)))
+    same = bool(np.array_equal(out_np, out.cpu().numpy()))
+
+    # ---- roofline of the gather kernel (per rank, max-time rank)
+    peak = None
+    if rank == 0:
+        import ctypes
+
+        tf, mhz = ctypes.c_double(), ctypes.c_double()
+        _lib.check(_lib.load().vfn_bench_fp64_peak(dev.index or 0, 0.5, ctypes.byref(tf), ctypes.byref(mhz)))
+        peak = tf.value
+
+    total_points = w.npoints
+    value = total_points / (step_ms * 1e-3)
+    if rank != 0:
+        return
+    fl = 2.0 * fma_per_point(CUTOFF)
+    achieved = fl * M / (g_ms * 1e-3) / 1e12
+    result = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "points/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": step_ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic, seeded (SURVEY 8d recipe); no dataset exists for this benchmark",
+        "config": workload_config(name, world),
+        "e2e": {
+            "value": total_points / (e2e_step * 1e-3),
+            "unit": "points/s",
+            "h2d_bytes_per_step": int(total_points * 24),
+            "d2h_bytes_per_step": int(total_points * 16),
+            "ms_per_step": e2e_step,
+            "matches_device_result_bitwise": same,
+        },
+        "roofline": {
+            "bound": "fp64",
+            "kernel": "gather (K4)",
+            "achieved": achieved,
+            "peak": peak,
+            "unit": "TFLOP/s",
+            "frac": achieved / peak if peak else None,
+            "traffic": None,
+            "algorithmic": f"{int(fl)} flop/point = 2*((2m+1)^3+(2m+1)^2+(2m+1)) FMA at m={CUTOFF}; "
+            f"{M} points per launch",
+            "peak_source": "measured DFMA peak on this device (vfn_bench_fp64_peak, 0.5 s); "
+            "MEASURED_PEAKS.json has no FP64 figure",
+            "gather_ms": g_ms,
+            "gather_share_of_step": g_ms / step_ms,
+        },
+        "plan_build_ms": plan_ms,
+        "gpu_launches": None,
+        "clocks": clk,
+    }
+    result["gpu_launches"] = launches_per_step(plan, M) * args.steps
+    if cpu is not None:
+        sp = cpu["sample_points"]
+        gpu_vals = plan.evaluate(sp)
+        ref = cpu["sample_values"]
+        err_l2 = float(np.linalg.norm(gpu_vals - ref) / np.linalg.norm(ref))
+        err_inf = float(np.abs(gpu_vals - ref).max() / np.abs(ref).max())
+        result["cpu_baseline"] = {
+            "value": cpu["value"],
+            "unit": "points/s",
+            "cores": cpu["cores"],
+            "kind": "port",
+            "sample": f"{cpu['points']} points of the {name} distribution in {cpu['seconds']:.1f} s, "
+            f"oracle/nfft_oracle.py (numpy restatement of nufft.py:244-272) fork-sharded over "
+            f"{cpu['cores']} cores after a {cpu['plan_s']:.2f} s plan build; CPU {cpu_model()}",
+        }
+        result["parity_vs_cpu"] = {"points": int(len(ref)), "rel_l2": err_l2, "rel_linf": err_inf}
+    print(json.dumps(result), flush=True)
+
+
+def launches_per_step(plan, M: int) -> int:
+    """Kernels of ours launched by one evaluate: map+key, the CUB onesweep
+    radix sort (1 histogram + one pass per 8 key bits), box offsets and the
+    gather (DESIGN.md lists them)."""
+    return plan.launch_count(M)
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    name = args.workload
+    coeffs = workloads.coefficients(name)
+    runs = []
+    per_step = max(3.0, args.cpu_seconds / 4)
+    for i in range(args.warmup + args.steps):
+        r = cpu_port_run(name, coeffs, per_step)
+        if i >= args.warmup:
+            runs.append(r)
+    value = float(np.mean([r["value"] for r in runs]))
+    cores = runs[0]["cores"]
+    sample = (f"each step: the {name} plan (oracle port, numpy/scipy) then its gather fork-sharded over "
+              f"{cores} cores for {per_step:.0f} s (~{int(np.mean([r['points'] for r in runs]))} points); "
+              f"CPU {cpu_model()}")
+    out = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "points/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": float(np.mean([r["seconds"] for r in runs]) * 1e3),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic, seeded (SURVEY 8d recipe)",
+        "config": workload_config(name, world),
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 and args.impl == "ours":
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -121,6 +121,11 @@ int vfn_plan_set_gather(vfn_plan* plan, int variant);
  * whole device-side evaluate, measured with CUDA events on its stream. */
 int vfn_plan_last_timing(const vfn_plan* plan, float* gather_ms, float* total_ms);
 
+/* Utility (not a reference interface): measured sustained FP64 FMA rate of
+ * `device` in TFLOP/s over ~`seconds`, the roofline denominator bench.py
+ * reports against; *sm_clock_mhz gets the device's max SM clock.        */
+int vfn_bench_fp64_peak(int device, double seconds, double* tflops, double* sm_clock_mhz);
+
 #ifdef __cplusplus
 }
 #endif

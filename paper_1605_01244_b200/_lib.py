@@ -61,6 +61,10 @@ SIGNATURES = {
     "vfn_plan_geometry": (
         ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int * 3, ctypes.c_int * 3]
     ),
+    "vfn_bench_fp64_peak": (
+        ctypes.c_int,
+        [ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
+    ),
     "vfn_plan_last_timing": (
         ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
     ),

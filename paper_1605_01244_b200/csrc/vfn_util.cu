@@ -1,0 +1,62 @@
+// Roofline denominator: sustained FP64 FMA throughput of this device,
+// measured with an independent-chain DFMA kernel over all SMs (bench.py).
+#include "vfn_internal.cuh"
+
+namespace vfn {
+
+__global__ void k_dfma_peak(double* out, int iters, double s) {
+  double a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-3 + i;
+  const double c = 1e-9;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = fma(a[i], s, c);
+    }
+  }
+  double r = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r += a[i];
+  if (r == 1234.5678) out[0] = r;
+}
+
+}  // namespace vfn
+
+using namespace vfn;
+
+extern "C" int vfn_bench_fp64_peak(int device, double seconds, double* tflops, double* sm_clock_mhz) {
+  if (!tflops) return fail(VFN_ERR_INVALID, "null argument");
+  DeviceGuard guard(device);
+  int nsm = 0, clk = 0;
+  VFN_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+  VFN_CUDA(cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, device));
+  double* d = nullptr;
+  VFN_CUDA(cudaMalloc(&d, 64));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int threads = 256, blocks = nsm * 8, iters = 2000;
+  k_dfma_peak<<<blocks, threads>>>(d, iters, 0.999999);  // warm up
+  cudaDeviceSynchronize();
+  double flops_per_launch = 2.0 * 8 * 16 * (double)iters * blocks * threads;
+  int reps = 0;
+  float total_ms = 0.f;
+  cudaEventRecord(e0);
+  do {
+    k_dfma_peak<<<blocks, threads>>>(d, iters, 0.999999);
+    ++reps;
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&total_ms, e0, e1);
+  } while (total_ms < seconds * 1e3 && reps < 100000);
+  cudaError_t err = cudaGetLastError();
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  if (err != cudaSuccess) return fail(VFN_ERR_CUDA, cudaGetErrorString(err));
+  *tflops = flops_per_launch * reps / (total_ms * 1e-3) / 1e12;
+  if (sm_clock_mhz) *sm_clock_mhz = clk / 1e3;
+  return VFN_OK;
+}

@@ -301,13 +301,24 @@ class NufftPlan:
         _lib.check(_lib.load().vfn_plan_last_timing(self._handle, ctypes.byref(g), ctypes.byref(t)))
         return g.value, t.value
 
-    def evaluate(self, points, chunk: int = 4096):
+    def evaluate(self, points, chunk: int = 4096, *, out=None):
         """Series values at M points, in input order (nufft.py:244-272).
 
         ``chunk`` is accepted for signature compatibility; the device path
-        has no chunk loop and results do not depend on it."""
+        has no chunk loop and results do not depend on it.  ``out`` (optional)
+        is a caller-owned complex128 buffer of length M on the same side as
+        ``points`` (e.g. pinned host memory), written in place and returned."""
         pts, on_dev, M = _points_arg(points)
-        out = _empty_like_points(pts, on_dev, M)
+        if out is None:
+            out = _empty_like_points(pts, on_dev, M)
+        else:
+            ok = out.shape == (M,) and (
+                (on_dev and _is_cuda_tensor(out) and out.dtype == _torch().complex128 and out.is_contiguous())
+                or (not on_dev and isinstance(out, np.ndarray) and out.dtype == np.complex128
+                    and out.flags.c_contiguous)
+            )
+            if not ok:
+                raise ValueError("out must be a contiguous complex128 buffer of shape (M,) next to points")
         if M == 0:
             return out
         if on_dev and (pts.device.index or 0) != self.device:
@@ -327,6 +338,20 @@ class NufftPlan:
         tile = (ctypes.c_int * 3)()
         _lib.check(_lib.load().vfn_plan_geometry(self._handle, int(M), box, tile))
         return tuple(box), tuple(tile)
+
+    def launch_count(self, M: int) -> int:
+        """Kernels of this library one evaluate of M points launches: map+key,
+        the CUB onesweep radix sort (histogram, exclusive-sum, one pass per 8
+        key bits) and the gather (plus box offsets for the DMMA gather)."""
+        if M == 0:
+            return 0
+        box, tile = self.geometry(M)
+        ntiles = 1
+        for d in range(3):
+            ntiles *= -(-self._n[d] // tile[d])
+        nboxes = ntiles * (tile[0] // box[0]) * (tile[1] // box[1]) * (tile[2] // box[2])
+        bits = max(1, int(nboxes - 1).bit_length())
+        return 1 + 2 + -(-bits // 8) + 1
 
     def bin(self, points):
         """(keys, perm) of the device bin sort as numpy arrays."""
