@@ -1,6 +1,8 @@
 // Host-side numerics of a plan: Kaiser-Bessel parameter, window transform
 // table and the piecewise-polynomial window fit used by the gather kernels.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -73,7 +75,7 @@ static long double phi(long double v, int m, long double beta, long double i0b) 
 // Chebyshev interpolation of phi(delta - c) on delta in [-1/2, 1/2] for
 // c = j - m, converted to monomials in delta (Horner-evaluated on the GPU).
 // The degree is the smallest one whose max error on a dense check grid is
-// below 1e-15 (phi <= 1), capped at max_deg.
+// below 4e-15 (phi <= 1; a few ulp of Horner rounding), capped at max_deg.
 int fit_window_poly(int m, double beta, double* coef, int max_deg) {
   const long double i0b = i0l(beta);
   const int W = 2 * m + 1;
@@ -131,7 +133,8 @@ int fit_window_poly(int m, double beta, double* coef, int max_deg) {
     }
     best = all;
     chosen = deg;
-    if (worst < 1e-15L) break;
+    if (std::getenv("VFN_DEBUG_FIT")) fprintf(stderr, "fit m=%d deg=%d err=%.3Le\n", m, deg, worst);
+    if (worst < 4e-15L) break;
   }
   for (size_t i = 0; i < best.size(); ++i) coef[i] = (double)best[i];
   return chosen;
