@@ -153,6 +153,7 @@ int vfn_plan_create(vfn_plan** out, int device, const int64_t nmodes[3], const d
   const void* cdev = nullptr;
   int st = stage_in(staging, coeffs, cbytes, coeffs_on_device, &cdev, s);
   if (st == VFN_OK) st = build_grid(p, static_cast<const double*>(cdev), s);
+  if (st == VFN_OK) st = make_grid_tmap(p);
   staging.release();
   if (st != VFN_OK) {
     std::string msg = vfn_last_error();

@@ -349,6 +349,11 @@ int gather_boxes(vfn_plan* p, const double* pts, int64_t M, const BinGeom& g,
   A.WS = WS;
   cudaEventRecord(p->ev[1], s);  // gather timing starts here (prep excluded)
   int st = VFN_OK;
+  if (m6_applicable(p, g)) {
+    st = launch_m6(p, pts, perm, bstart, p->items.as<int4>(), ioff + g.ntiles, out, g, s);
+    if (st == VFN_OK) *used = true;
+    return st;
+  }
   switch (KC) {
     case 1: st = launch_dmma<1>(A, smem, s); break;
     case 2: st = launch_dmma<2>(A, smem, s); break;

@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <string>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cufft.h>
 
@@ -118,6 +119,8 @@ struct vfn_plan {
   int pad_tile[3] = {8, 8, 8};  // grid padded to multiples of this
   double2* grid = nullptr;
   int gather_variant = 0;
+  CUtensorMap tmap;        // TMA view of `grid` for the m = 6 gather
+  bool has_tmap = false;
   // evaluate scratch (grow-only)
   vfn::DevBuf pts, out, keys, keys_sorted, idx, perm, sort_tmp, box_start, items, misc;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -151,5 +154,10 @@ int rect_eval(int device, const int64_t nmodes[3], const double a[3], const doub
               int on_device, cudaStream_t s);
 
 BinGeom choose_geometry(const vfn_plan* p, int64_t M);
+int make_grid_tmap(vfn_plan* p);
+bool m6_applicable(const vfn_plan* p, const BinGeom& g);
+int launch_m6(vfn_plan* p, const double* pts, const int32_t* perm, const int32_t* box_start,
+              const int4* items, const int32_t* nitems, double2* out, const BinGeom& g,
+              cudaStream_t s);
 
 }  // namespace vfn
