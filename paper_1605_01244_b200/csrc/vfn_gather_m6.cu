@@ -102,12 +102,12 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
   const unsigned raw = (unsigned)__cvta_generic_to_shared(smem_raw);
   const unsigned tile_s = (raw + 1023u) & ~1023u;
   unsigned char* tile_g = smem_raw + (tile_s - raw);
-  double* sPoly = reinterpret_cast<double*>(tile_g + 2 * kHalf);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tile_g + 2 * kHalf);  // 1024-aligned
+  double* sPoly = reinterpret_cast<double*>(tile_g + 2 * kHalf + 16);
   const int npoly = W * (A.deg + 1);
   double* sW = sPoly + ((npoly + 1) & ~1);                     // [kWarps][8][kWS]
   int* sBox = reinterpret_cast<int*>(sW + kWarps * kUnitPts * kWS);  // [bpt + 1]
   int* sUnit = sBox + 33;                                          // [bpt + 1]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sUnit + 34);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tig = lane & 3;
