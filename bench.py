@@ -14,7 +14,7 @@ pad, 3D FFT) is built once per rank and reported separately.
 * ``e2e``     — the same through the public API with pinned HOST buffers, H2D of
                 the points and D2H of the results inside the timed region;
 * ``roofline``— the gather kernel's algorithmic FP64 rate (2[(2m+1)^3+(2m+1)^2
-                +(2m+1)] FMA per point) over its CUDA-event time, against the
+                +(2m+1)] real FMA = 9516 flop per point at m=6) over its CUDA-event time, against the
                 DFMA peak measured on this device by vfn_bench_fp64_peak;
 * ``cpu_baseline`` — the oracle port of the reference (oracle/nfft_oracle.py,
                 numpy, fork-sharded over all host cores) on a bounded sample.
@@ -45,9 +45,11 @@ METRIC = "3D NFFT trafo points/sec (fp64 complex)"
 SIGMA, CUTOFF = 2.0, 6
 
 
-def fma_per_point(m: int) -> int:
+def flop_per_point(m: int) -> int:
+    """Algorithmic work of the gather per point: (2m+1)^3 + (2m+1)^2 + (2m+1)
+    complex-by-real multiply-adds (nufft.py:269-271), 2 real FMA = 4 flop each."""
     w = 2 * m + 1
-    return w ** 3 + w ** 2 + w
+    return 4 * (w ** 3 + w ** 2 + w)
 
 
 def parse():
@@ -338,7 +340,7 @@ def run_ours(args):
     value = total_points / (step_ms * 1e-3)
     if rank != 0:
         return
-    fl = 2.0 * fma_per_point(CUTOFF)
+    fl = float(flop_per_point(CUTOFF))
     achieved = fl * M / (g_ms * 1e-3) / 1e12
     result = {
         "metric": METRIC,
@@ -370,7 +372,7 @@ def run_ours(args):
             "unit": "TFLOP/s",
             "frac": achieved / peak if peak else None,
             "traffic": None,
-            "algorithmic": f"{int(fl)} flop/point = 2*((2m+1)^3+(2m+1)^2+(2m+1)) FMA at m={CUTOFF}; "
+            "algorithmic": f"{int(fl)} flop/point = 2*((2m+1)^3+(2m+1)^2+(2m+1)) real FMA at m={CUTOFF}; "
             f"{M} points per launch",
             "peak_source": "measured DFMA peak on this device (vfn_bench_fp64_peak, 0.5 s); "
             "MEASURED_PEAKS.json has no FP64 figure",

@@ -260,7 +260,7 @@ int vfn_map_to_torus(int device, const double a[3], const double b[3], const dou
 // Shared front half of evaluate / bin: stage points, map+validate+key, sort.
 static int bin_points(vfn_plan* p, const double* points, int64_t M, int on_device,
                       const BinGeom& g, const double** pts_dev, int64_t** bad_dev,
-                      cudaStream_t s) {
+                      cudaStream_t s, bool want_u = false) {
   const void* pdev = nullptr;
   VFN_CHECK(stage_in(p->pts, points, sizeof(double) * 3 * M, on_device, &pdev, s));
   *pts_dev = static_cast<const double*>(pdev);
@@ -272,7 +272,12 @@ static int bin_points(vfn_plan* p, const double* points, int64_t M, int on_devic
   VFN_CHECK(p->keys_sorted.ensure(sizeof(uint32_t) * M));
   VFN_CHECK(p->idx.ensure(sizeof(int32_t) * M));
   VFN_CHECK(p->perm.ensure(sizeof(int32_t) * M));
-  VFN_CHECK(map_and_key(p, *pts_dev, M, g, p->keys.as<uint32_t>(), p->idx.as<int32_t>(), *bad_dev, s));
+  double* u = nullptr;
+  if (want_u) {
+    VFN_CHECK(p->uvals.ensure(sizeof(double) * 3 * M));
+    u = p->uvals.as<double>();
+  }
+  VFN_CHECK(map_and_key(p, *pts_dev, M, g, p->keys.as<uint32_t>(), p->idx.as<int32_t>(), u, *bad_dev, s));
   VFN_CHECK(sort_pairs(p, p->keys.as<uint32_t>(), p->keys_sorted.as<uint32_t>(),
                        p->idx.as<int32_t>(), p->perm.as<int32_t>(), M, key_bits_for(g.nboxes), s));
   return VFN_OK;
@@ -315,7 +320,8 @@ int vfn_plan_eval(vfn_plan* p, const double* points, int64_t M, double* out, int
   BinGeom g = choose_geometry(p, M);
   const double* pts_dev;
   int64_t* bad_dev;
-  VFN_CHECK(bin_points(p, points, M, on_device, g, &pts_dev, &bad_dev, s));
+  VFN_CHECK(bin_points(p, points, M, on_device, g, &pts_dev, &bad_dev, s,
+                       p->gather_variant != 1 && m6_applicable(p, g)));
   double2* out_dev = reinterpret_cast<double2*>(out);
   if (!on_device) {
     VFN_CHECK(p->out.ensure(sizeof(double2) * M));

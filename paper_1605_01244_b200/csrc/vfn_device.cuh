@@ -41,6 +41,25 @@ __device__ __forceinline__ int nearest_cell(double x, double a, double amb, doub
   return l >= n ? l - n : l;
 }
 
+// u = z * n with z = zeta < 0 ? zeta + 1 : zeta (nufft.py:249, :256)
+__device__ __forceinline__ double torus_u(double x, double a, double amb, double nd) {
+  double zeta = torus_coord(x, a, amb);
+  double z = zeta < 0.0 ? __dadd_rn(zeta, 1.0) : zeta;
+  return __dmul_rn(z, nd);
+}
+
+// l0 = floor(u + 1/2) (nufft.py:257): cell = l0 mod n, delta = u - l0.
+__device__ __forceinline__ int cell_from_u(double u, double nd, int n, double& delta) {
+  double l0 = floor(__dadd_rn(u, 0.5));
+  delta = __dsub_rn(u, l0);
+  if (!(l0 >= 0.0 && l0 <= nd)) {
+    delta = 0.0;
+    return 0;
+  }
+  int l = (int)l0;
+  return l >= n ? l - n : l;
+}
+
 __device__ __forceinline__ bool inside(double x, double a, double b) { return x >= a && x < b; }
 
 // Horner evaluation of window polynomial j at delta.

@@ -350,7 +350,7 @@ int gather_boxes(vfn_plan* p, const double* pts, int64_t M, const BinGeom& g,
   cudaEventRecord(p->ev[1], s);  // gather timing starts here (prep excluded)
   int st = VFN_OK;
   if (m6_applicable(p, g)) {
-    st = launch_m6(p, pts, perm, bstart, p->items.as<int4>(), ioff + g.ntiles, out, g, s);
+    st = launch_m6(p, p->uvals.as<double>(), perm, bstart, p->items.as<int4>(), ioff + g.ntiles, out, g, s);
     if (st == VFN_OK) *used = true;
     return st;
   }

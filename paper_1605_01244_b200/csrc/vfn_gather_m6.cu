@@ -31,10 +31,11 @@ constexpr int kTile = 4;             // tile = 4 x 4 x 4 cells
 constexpr int kT = kTile + 12;       // staged extent per axis (16)
 constexpr int kLine = 128;           // bytes per staged z-half row
 constexpr int kHalf = kT * kT * kLine;  // 32 KB per z-half
-constexpr int kWS = 17;              // per-point x-weight stride (odd)
+constexpr int kWtO = 4;              // zero pad before j = 0 in the weights table
+constexpr int kWtS = 25;             // weights-table row stride (odd: 4 + 16 + pad)
 
 struct Args {
-  const double* pts;
+  const double* u;  // u = z * n per point and axis, input order (from k_map_key)
   const int32_t* perm;
   const int32_t* box_start;
   const int4* items;
@@ -103,15 +104,24 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
   const unsigned tile_s = (raw + 1023u) & ~1023u;
   unsigned char* tile_g = smem_raw + (tile_s - raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(tile_g + 2 * kHalf);  // 1024-aligned
-  double* sPoly = reinterpret_cast<double*>(tile_g + 2 * kHalf + 16);
-  const int npoly = W * (A.deg + 1);
-  double* sW = sPoly + ((npoly + 1) & ~1);                     // [kWarps][8][kWS]
-  int* sBox = reinterpret_cast<int*>(sW + kWarps * kUnitPts * kWS);  // [bpt + 1]
-  int* sUnit = sBox + 33;                                          // [bpt + 1]
+  double* sWt = reinterpret_cast<double*>(tile_g + 2 * kHalf + 16);  // [kWarps][3][8][kWtS]
+  int* sBox = reinterpret_cast<int*>(sWt + kWarps * 3 * kUnitPts * kWtS);  // [bpt + 1]
+  int* sUnit = sBox + 33;                                                  // [bpt + 1]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tig = lane & 3;
-  for (int i = tid; i < npoly; i += blockDim.x) sPoly[i] = A.poly[i];
+  // window weights table: entry kWtO + j holds phi_j(delta) of point g on an
+  // axis, j = 0..12; the pads j in [-kWtO, 0) and [13, 16) stay zero
+  for (int i = tid; i < kWarps * 3 * kUnitPts * kWtS; i += blockDim.x) sWt[i] = 0.0;
+  // B fragments of the window-polynomial DMMA: C[d][j], d = 4 kc + tig, j = 8 nb + g
+  double cb[4][2];
+#pragma unroll
+  for (int kc = 0; kc < 4; ++kc)
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) {
+      const int d = 4 * kc + tig, j = 8 * nb + g;
+      cb[kc][nb] = (d <= A.deg && j < W) ? A.poly[j * (A.deg + 1) + d] : 0.0;
+    }
   if (tid == 0) {
     mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
@@ -119,16 +129,16 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
   __syncthreads();
 
   const BinGeom& G = A.g;
-  double* w0 = sW + warp * kUnitPts * kWS;
+  double* wt = sWt + warp * 3 * kUnitPts * kWtS;  // [3][8][kWtS]
   const int nitems = *A.nitems;
   unsigned phase = 0;
 
   for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
     const int4 item = A.items[it];
-    const int64_t tile = item.x;
-    const int t2 = (int)(tile % G.ntile[2]);
-    const int t1 = (int)((tile / G.ntile[2]) % G.ntile[1]);
-    const int t0 = (int)(tile / ((int64_t)G.ntile[2] * G.ntile[1]));
+    const int tile = item.x;
+    const int t2 = tile % G.ntile[2];
+    const int t1 = (tile / G.ntile[2]) % G.ntile[1];
+    const int t0 = tile / (G.ntile[2] * G.ntile[1]);
     const int ox = t0 * kTile, oy = t1 * kTile, oz = t2 * kTile;
     __syncthreads();  // everyone is done reading the previous tile
     if (tid == 0) {
@@ -138,7 +148,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
     }
     if (warp == 0) {
       const int bpt = G.boxes_per_tile;
-      const int32_t* bs = A.box_start + tile * bpt;
+      const int32_t* bs = A.box_start + (int64_t)tile * bpt;
       int cnt = 0, start = 0;
       if (lane < bpt) {
         start = bs[lane];
@@ -158,9 +168,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
       if (lane == bpt - 1) sBox[bpt] = start + cnt;
     }
     __syncthreads();
-    mbar_wait(bar, phase);
-    phase ^= 1u;
 
+    bool waited = false;
     for (int u = item.y + warp; u < item.z; u += kWarps) {
       int b = 0;
       while (sUnit[b + 1] <= u) ++b;
@@ -170,41 +179,56 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
       const int by = b % NB, bx = b / NB;
       const int X0 = bx * BXY, Y0 = by * BXY;
 
+      // point g of the unit: nearest cell and offset from u (nufft.py:256-257)
       const bool valid = g < cnt;
-      int cell[3] = {0, 0, 0};
-      double dl[3] = {0.0, 0.0, 0.0};
       int64_t prow = 0;
+      double uu[3] = {0.0, 0.0, 0.0};
       if (valid) {
-        prow = A.perm[p0 + g];
+        prow = __ldg(A.perm + p0 + g);
 #pragma unroll
-        for (int d = 0; d < 3; ++d)
-          cell[d] = nearest_cell(__ldg(A.pts + 3 * prow + d), A.tm.a[d], A.tm.amb[d], A.tm.nd[d],
-                                 A.tm.n[d], dl[d]);
+        for (int d = 0; d < 3; ++d) uu[d] = __ldg(A.u + 3 * prow + d);
       }
+      int cell[3];
+      double dl[3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) cell[d] = cell_from_u(uu[d], A.tm.nd[d], A.tm.n[d], dl[d]);
       const int ci = cell[0] - ox - X0;
       const int cj = cell[1] - oy - Y0;
       const int ck = cell[2] - oz;
+      // window weights of point g on all three axes by DMMA:
+      // W[p, j] = sum_d delta_p^d C[d, j]   (A = powers of delta, B = coefficients)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double x1 = dl[d], x2 = x1 * x1, x4 = x2 * x2;
+        double pw = tig == 0 ? 1.0 : (tig == 1 ? x1 : (tig == 2 ? x2 : x2 * x1));
+        double w00 = 0.0, w01 = 0.0, w10 = 0.0, w11 = 0.0;
+#pragma unroll
+        for (int kc = 0; kc < 4; ++kc) {
+          dmma(w00, w01, pw, cb[kc][0]);
+          dmma(w10, w11, pw, cb[kc][1]);
+          pw *= x4;
+        }
+        double* row = wt + (d * kUnitPts + g) * kWtS + kWtO;
+        row[2 * tig] = w00;
+        row[2 * tig + 1] = w01;
+        if (8 + 2 * tig < W) row[8 + 2 * tig] = w10;  // j = 13..15 stay zero
+        if (9 + 2 * tig < W) row[9 + 2 * tig] = w11;
+      }
+      __syncwarp();
+      const double* w0 = wt + (0 * kUnitPts + g) * kWtS + kWtO - ci;  // w0[x]: axis 1
+      const double* w1 = wt + (1 * kUnitPts + g) * kWtS + kWtO - cj;  // w1[y]: axis 2
+      const double* w2 = wt + (2 * kUnitPts + g) * kWtS + kWtO - ck;  // w2[k]: axis 3
       double a[4];
 #pragma unroll
-      for (int kc = 0; kc < 4; ++kc) {
-        const int j = 4 * kc + tig - ck;
-        a[kc] = (valid && j >= 0 && j < W) ? window_poly(sPoly, A.deg, j, dl[2]) : 0.0;
-      }
+      for (int kc = 0; kc < 4; ++kc) a[kc] = valid ? w2[4 * kc + tig] : 0.0;
       double wy[2][2];
 #pragma unroll
       for (int h = 0; h < 2; ++h)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int y = 8 * h + 2 * tig + e;
-          const int j = y - cj;
-          wy[h][e] = (valid && y < YB && j >= 0 && j < W) ? window_poly(sPoly, A.deg, j, dl[1]) : 0.0;
+          wy[h][e] = y < YB ? w1[y] : 0.0;
         }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int x = tig + 4 * i;
-        const int j = x - ci;
-        if (x < XB) w0[g * kWS + x] = (valid && j >= 0 && j < W) ? window_poly(sPoly, A.deg, j, dl[0]) : 0.0;
-      }
       // B-fragment row of this lane per half: y = 8h + g (clamped into the box)
       unsigned off[2][4];
 #pragma unroll
@@ -216,8 +240,10 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
           off[h][kc] = tile_s + (kc >> 1) * kHalf + (X0 * kT + y) * kLine +
                        16 * (((kc & 1) * 4 + tig) ^ sw);
       }
-      __syncwarp();
-      const double* wx = w0 + g * kWS;
+      if (!waited) {
+        mbar_wait(bar, phase);
+        waited = true;
+      }
       double acc_re = 0.0, acc_im = 0.0;
 #pragma unroll
       for (int x = 0; x < XB; ++x) {
@@ -236,7 +262,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
           sim = fma(wy[h][0], ci0, sim);
           sim = fma(wy[h][1], ci1, sim);
         }
-        const double w = wx[x];
+        const double w = w0[x];
         acc_re = fma(w, sre, acc_re);
         acc_im = fma(w, sim, acc_im);
       }
@@ -247,6 +273,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
       if (valid && tig == 0) A.out[prow] = make_double2(acc_re, acc_im);
       __syncwarp();
     }
+    if (!waited) mbar_wait(bar, phase);  // keep the phase bookkeeping uniform
+    phase ^= 1u;
   }
 }
 
@@ -282,9 +310,8 @@ int make_grid_tmap(vfn_plan* p) {
 
 size_t m6_smem_bytes(int deg) {
   size_t b = 1024 + 2 * m6::kHalf;
-  b += sizeof(double) * (((13 * (deg + 1)) + 1) & ~1);
-  b += sizeof(double) * m6::kWarps * m6::kUnitPts * m6::kWS;
-  b += sizeof(int) * (33 + 34) + 16;
+  b += 16 + sizeof(double) * m6::kWarps * 3 * m6::kUnitPts * m6::kWtS;
+  b += sizeof(int) * (33 + 34);
   return b;
 }
 
@@ -305,15 +332,15 @@ static int launch(vfn_plan* p, const m6::Args& A, cudaStream_t s) {
 }
 
 bool m6_applicable(const vfn_plan* p, const BinGeom& g) {
-  return p->m == 6 && p->has_tmap && g.tile[0] == 4 && g.tile[1] == 4 && g.tile[2] == 4 &&
+  return p->m == 6 && p->has_tmap && p->poly.deg <= 15 && g.tile[0] == 4 && g.tile[1] == 4 && g.tile[2] == 4 &&
          g.box[2] == 4 && g.box[0] == g.box[1] && (g.box[0] == 1 || g.box[0] == 2);
 }
 
-int launch_m6(vfn_plan* p, const double* pts, const int32_t* perm, const int32_t* box_start,
+int launch_m6(vfn_plan* p, const double* u, const int32_t* perm, const int32_t* box_start,
               const int4* items, const int32_t* nitems, double2* out, const BinGeom& g,
               cudaStream_t s) {
   m6::Args A;
-  A.pts = pts;
+  A.u = u;
   A.perm = perm;
   A.box_start = box_start;
   A.items = items;

@@ -122,7 +122,7 @@ struct vfn_plan {
   CUtensorMap tmap;        // TMA view of `grid` for the m = 6 gather
   bool has_tmap = false;
   // evaluate scratch (grow-only)
-  vfn::DevBuf pts, out, keys, keys_sorted, idx, perm, sort_tmp, box_start, items, misc;
+  vfn::DevBuf pts, out, uvals, keys, keys_sorted, idx, perm, sort_tmp, box_start, items, misc;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   float last_gather_ms = 0.f, last_total_ms = 0.f;
 };
@@ -140,7 +140,7 @@ int fit_window_poly(int m, double beta, double* coef, int max_deg);
 // ---------------------------------------------------------------- launchers
 int build_grid(vfn_plan* p, const double* coeffs_dev, cudaStream_t s);
 int map_and_key(vfn_plan* p, const double* pts_dev, int64_t M, const BinGeom& g, uint32_t* keys,
-                int32_t* iota, int64_t* bad_dev, cudaStream_t s);
+                int32_t* iota, double* u, int64_t* bad_dev, cudaStream_t s);
 int sort_pairs(vfn_plan* p, const uint32_t* keys_in, uint32_t* keys_out, const int32_t* vals_in,
                int32_t* vals_out, int64_t M, int key_bits, cudaStream_t s);
 int launch_torus(const TorusMap& tm, const double* pts, int64_t M, double* zeta, cudaStream_t s);
@@ -156,7 +156,7 @@ int rect_eval(int device, const int64_t nmodes[3], const double a[3], const doub
 BinGeom choose_geometry(const vfn_plan* p, int64_t M);
 int make_grid_tmap(vfn_plan* p);
 bool m6_applicable(const vfn_plan* p, const BinGeom& g);
-int launch_m6(vfn_plan* p, const double* pts, const int32_t* perm, const int32_t* box_start,
+int launch_m6(vfn_plan* p, const double* u, const int32_t* perm, const int32_t* box_start,
               const int4* items, const int32_t* nitems, double2* out, const BinGeom& g,
               cudaStream_t s);
 

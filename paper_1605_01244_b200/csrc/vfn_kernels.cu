@@ -14,9 +14,11 @@ namespace vfn {
 // ------------------------------------------------------------------ K0 + K1
 // One pass over the points: domain check (first bad row by atomicMin,
 // nufft.py:115-126), nearest cell per axis, and the bin key.
+// u (optional) receives the reference's u = z * n per coordinate
+// (nufft.py:256), from which the gather re-derives l0 and delta exactly.
 __global__ void k_map_key(const double* __restrict__ pts, int64_t M, TorusMap tm, BinGeom g,
                           uint32_t* __restrict__ keys, int32_t* __restrict__ iota,
-                          unsigned long long* __restrict__ bad) {
+                          double* __restrict__ u, unsigned long long* __restrict__ bad) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= M) return;
   int cell[3];
@@ -27,6 +29,7 @@ __global__ void k_map_key(const double* __restrict__ pts, int64_t M, TorusMap tm
     ok = ok && inside(x, tm.a[d], tm.b[d]);
     double delta;
     cell[d] = nearest_cell(x, tm.a[d], tm.amb[d], tm.nd[d], tm.n[d], delta);
+    if (u) u[3 * i + d] = torus_u(x, tm.a[d], tm.amb[d], tm.nd[d]);
   }
   if (!ok) {
     atomicMin(bad, (unsigned long long)i);
@@ -53,11 +56,11 @@ __global__ void k_torus(const double* __restrict__ pts, int64_t M, TorusMap tm,
 }
 
 int map_and_key(vfn_plan* p, const double* pts, int64_t M, const BinGeom& g, uint32_t* keys,
-                int32_t* iota, int64_t* bad_dev, cudaStream_t s) {
+                int32_t* iota, double* u, int64_t* bad_dev, cudaStream_t s) {
   if (M == 0) return VFN_OK;
   int threads = 256;
   int64_t blocks = (M + threads - 1) / threads;
-  k_map_key<<<(unsigned)blocks, threads, 0, s>>>(pts, M, p->map, g, keys, iota,
+  k_map_key<<<(unsigned)blocks, threads, 0, s>>>(pts, M, p->map, g, keys, iota, u,
                                                   reinterpret_cast<unsigned long long*>(bad_dev));
   VFN_CUDA(cudaGetLastError());
   return VFN_OK;
