@@ -192,9 +192,14 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
       double dl[3];
 #pragma unroll
       for (int d = 0; d < 3; ++d) cell[d] = cell_from_u(uu[d], A.tm.nd[d], A.tm.n[d], dl[d]);
-      const int ci = cell[0] - ox - X0;
-      const int cj = cell[1] - oy - Y0;
-      const int ck = cell[2] - oz;
+      // offsets inside the box; idle lanes (and out-of-domain points, whose
+      // key is 0) are pinned to 0 so every table index stays in bounds
+      const bool inbox = valid && cell[0] - ox - X0 >= 0 && cell[0] - ox - X0 < BXY &&
+                         cell[1] - oy - Y0 >= 0 && cell[1] - oy - Y0 < BXY &&
+                         cell[2] - oz >= 0 && cell[2] - oz < kTile;
+      const int ci = inbox ? cell[0] - ox - X0 : 0;
+      const int cj = inbox ? cell[1] - oy - Y0 : 0;
+      const int ck = inbox ? cell[2] - oz : 0;
       // window weights of point g on all three axes by DMMA:
       // W[p, j] = sum_d delta_p^d C[d, j]   (A = powers of delta, B = coefficients)
 #pragma unroll
@@ -220,7 +225,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
       const double* w2 = wt + (2 * kUnitPts + g) * kWtS + kWtO - ck;  // w2[k]: axis 3
       double a[4];
 #pragma unroll
-      for (int kc = 0; kc < 4; ++kc) a[kc] = valid ? w2[4 * kc + tig] : 0.0;
+      for (int kc = 0; kc < 4; ++kc) a[kc] = inbox ? w2[4 * kc + tig] : 0.0;
       double wy[2][2];
 #pragma unroll
       for (int h = 0; h < 2; ++h)
