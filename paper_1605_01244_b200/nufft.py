@@ -351,7 +351,11 @@ class NufftPlan:
             ntiles *= -(-self._n[d] // tile[d])
         nboxes = ntiles * (tile[0] // box[0]) * (tile[1] // box[1]) * (tile[2] // box[2])
         bits = max(1, int(nboxes - 1).bit_length())
-        return 1 + 2 + -(-bits // 8) + 1
+        # CUB onesweep (M above its single-tile threshold): histogram + exclusive
+        # sum + 2 kernels per 8-bit pass (profiles/r01/launches_c5_v4.md)
+        sort = 2 + 2 * -(-bits // 8)
+        prep = 1 + 2 + 1 + 2 + 1  # box counts, scan, tile units, scan, items
+        return 1 + sort + prep + 1
 
     def bin(self, points):
         """(keys, perm) of the device bin sort as numpy arrays."""
