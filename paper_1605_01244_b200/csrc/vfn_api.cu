@@ -67,18 +67,20 @@ BinGeom choose_geometry(const vfn_plan* p, int64_t M) {
   const double density = M / cells;
   const int K = ((2 * p->m + 1) + 3) / 4 * 4;  // DMMA k-extent
   const int bk = K - 2 * p->m;                  // box depth in cells (2 or 4)
-  int bxy = density >= 1.0 ? 1 : 2;
+  const int bxy = density >= 1.0 ? 1 : 2;
+  const bool m6 = p->m == 6 && p->has_tmap;     // vfn_gather_m6.cu: 4x4x8 tiles, depth-8 boxes
   g.box[0] = bxy;
   g.box[1] = bxy;
-  g.box[2] = bk;
+  g.box[2] = m6 ? 8 : bk;
   g.tile[0] = 4;
   g.tile[1] = 4;
-  g.tile[2] = bk;
+  g.tile[2] = m6 ? 8 : bk;
   for (int d = 0; d < 3; ++d) {
     g.ntile[d] = (int)((p->n[d] + g.tile[d] - 1) / g.tile[d]);
     g.nbox[d] = g.tile[d] / g.box[d];
   }
   g.boxes_per_tile = g.nbox[0] * g.nbox[1] * g.nbox[2];
+  g.cells_per_box = g.box[0] * g.box[1] * g.box[2];
   g.ntiles = (int64_t)g.ntile[0] * g.ntile[1] * g.ntile[2];
   g.nboxes = g.ntiles * g.boxes_per_tile;
   return g;
@@ -170,7 +172,7 @@ int vfn_plan_destroy(vfn_plan* p) {
   if (p->grid) cudaFree(p->grid);
   if (p->poly.dev) cudaFree(p->poly.dev);
   DevBuf* bufs[] = {&p->pts, &p->out, &p->keys, &p->keys_sorted, &p->idx, &p->perm,
-                    &p->sort_tmp, &p->box_start, &p->items, &p->misc};
+                    &p->sort_tmp, &p->box_start, &p->items, &p->units, &p->uscratch, &p->misc};
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < 4; ++i)
     if (p->ev[i]) cudaEventDestroy(p->ev[i]);
@@ -279,7 +281,7 @@ static int bin_points(vfn_plan* p, const double* points, int64_t M, int on_devic
   }
   VFN_CHECK(map_and_key(p, *pts_dev, M, g, p->keys.as<uint32_t>(), p->idx.as<int32_t>(), u, *bad_dev, s));
   VFN_CHECK(sort_pairs(p, p->keys.as<uint32_t>(), p->keys_sorted.as<uint32_t>(),
-                       p->idx.as<int32_t>(), p->perm.as<int32_t>(), M, key_bits_for(g.nboxes), s));
+                       p->idx.as<int32_t>(), p->perm.as<int32_t>(), M, key_bits_for(g.nboxes * g.cells_per_box), s));
   return VFN_OK;
 }
 

@@ -230,9 +230,10 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_gather_dmma(GatherArgs A) {
 
 // ------------------------------------------------------------------ work items
 
-__global__ void k_box_counts(const uint32_t* __restrict__ keys, int64_t M, int32_t* __restrict__ counts) {
+__global__ void k_box_counts(const uint32_t* __restrict__ keys, int64_t M, int cells_per_box,
+                             int32_t* __restrict__ counts) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < M) atomicAdd(&counts[keys[i]], 1);
+  if (i < M) atomicAdd(&counts[keys[i] / cells_per_box], 1);
 }
 
 __global__ void k_tile_units(const int32_t* __restrict__ box_start, int64_t ntiles, int bpt,
@@ -289,6 +290,7 @@ int gather_boxes(vfn_plan* p, const double* pts, int64_t M, const BinGeom& g,
                  const uint32_t* keys_sorted, const int32_t* perm, double2* out, cudaStream_t s,
                  bool* used) {
   *used = false;
+  const bool m6 = m6_applicable(p, g);
   const int K = 4 * ((2 * p->m + 1 + 3) / 4);
   const int KC = K / 4;
   const int X = g.tile[0] + 2 * p->m, Y = g.tile[1] + 2 * p->m, Z = g.tile[2] + 2 * p->m;
@@ -296,9 +298,11 @@ int gather_boxes(vfn_plan* p, const double* pts, int64_t M, const BinGeom& g,
   while (SZ % 8 != 4) ++SZ;  // odd multiple of 4 complex: conflict-free B fragments
   const int WS = (std::max(g.box[0], g.box[1]) + 2 * p->m + 1) | 1;
   const size_t smem = dmma_smem_bytes(X, Y, SZ, p->m, p->poly.deg, WS);
-  if (smem > 200 * 1024 || g.box[0] + 2 * p->m > kMaxRowW || g.box[1] + 2 * p->m > kMaxRowW ||
-      g.boxes_per_tile > kMaxBoxes || KC > 7 || M > INT32_MAX)
+  if (!m6 && (smem > 200 * 1024 || g.box[0] + 2 * p->m > kMaxRowW ||
+              g.box[1] + 2 * p->m > kMaxRowW || g.boxes_per_tile > kMaxBoxes || KC > 7 ||
+              g.box[2] != K - 2 * p->m))
     return VFN_OK;  // not applicable: caller uses the thread-per-point gather
+  if (M > INT32_MAX) return VFN_OK;
 
   // box offsets: counts -> exclusive scan (nboxes + 1 entries)
   const int64_t nb = g.nboxes;
@@ -308,7 +312,7 @@ int gather_boxes(vfn_plan* p, const double* pts, int64_t M, const BinGeom& g,
   int32_t* nitems = bstart + (nb + 1);
   int32_t* ioff = nitems + (g.ntiles + 1);
   VFN_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (nb + 1), s));
-  k_box_counts<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(keys_sorted, M, counts);
+  k_box_counts<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(keys_sorted, M, g.cells_per_box, counts);
   VFN_CUDA(cudaGetLastError());
   size_t tmp = 0;
   VFN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, counts, bstart, (int)(nb + 1), s));
@@ -316,6 +320,11 @@ int gather_boxes(vfn_plan* p, const double* pts, int64_t M, const BinGeom& g,
   VFN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp2, nitems, ioff, (int)(g.ntiles + 1), s));
   VFN_CHECK(p->sort_tmp.ensure(std::max(tmp, tmp2)));
   VFN_CUDA(cub::DeviceScan::ExclusiveSum(p->sort_tmp.ptr, tmp, counts, bstart, (int)(nb + 1), s));
+  if (m6) {
+    int st = launch_m6(p, p->uvals.as<double>(), perm, keys_sorted, bstart, out, g, M, s);
+    if (st == VFN_OK) *used = true;
+    return st;
+  }
   k_tile_units<<<(unsigned)((g.ntiles + 1 + 255) / 256), 256, 0, s>>>(bstart, g.ntiles,
                                                                       g.boxes_per_tile, nitems);
   VFN_CUDA(cudaGetLastError());
@@ -349,11 +358,6 @@ int gather_boxes(vfn_plan* p, const double* pts, int64_t M, const BinGeom& g,
   A.WS = WS;
   cudaEventRecord(p->ev[1], s);  // gather timing starts here (prep excluded)
   int st = VFN_OK;
-  if (m6_applicable(p, g)) {
-    st = launch_m6(p, p->uvals.as<double>(), perm, bstart, p->items.as<int4>(), ioff + g.ntiles, out, g, s);
-    if (st == VFN_OK) *used = true;
-    return st;
-  }
   switch (KC) {
     case 1: st = launch_dmma<1>(A, smem, s); break;
     case 2: st = launch_dmma<2>(A, smem, s); break;

@@ -1,23 +1,32 @@
-// K4 v3: the m = 6 (default cutoff, nufft.py:56) specialisation of the DMMA
-// box gather, fully unrolled over the 13 (or 14) x-rows of a box.
+// K4 for the default cutoff m = 6 (nufft.py:56): binned gather on the FP64
+// tensor cores (DMMA, mma.sync.m8n8k4.f64), TMA-staged, double-buffered.
 //
-// Tile (4 x 4 x 4 cells) staging is two TMA loads (cp.async.bulk.tensor.3d)
-// of the ghost-padded grid viewed as doubles: z-halves of 8 complex values
-// (128 B lines), 16 y-rows, 16 x-rows, 128B-swizzled, completing on an
-// mbarrier.  With the swizzle, a lane's B-fragment address inside a line is
-// ((4 (kc & 1) + tig) ^ (y & 7)) * 16 B — conflict-free LDS.128 for the 8
-// rows x 4 depths a DMMA pair reads — and every offset is a per-unit
-// constant plus a compile-time x stride, so the inner body is just
-// LDS.128 + 2 DMMA per k-chunk.
+// Geometry.  Tiles of 4 x 4 x 8 cells; their 16 x 16 x 20 complex block of
+// the ghost-padded grid (80 KB) is one TMA copy (cp.async.bulk.tensor.3d) of
+// the grid viewed as doubles.  z-lines are 20 complex = 320 B, so the 8 rows x
+// 4 depths a DMMA pair reads hit both bank halves evenly (conflict-free
+// LDS.128) without a swizzle.  Boxes are 1 x 1 x 8 (2 x 2 x 8 at low density)
+// columns of a tile; inside a box the points are sorted by depth (the bin key
+// numbers cells depth-major).
 //
-// Per unit (<= 8 points of one box): rows y are padded from YB = BXY + 12 to
-// 16 (two 8-row halves); padded rows read a valid clamped row with weight 0.
-//   for x in 0..XB-1, h in {0, 1}:
-//     C_re/im[p, y] = sum_kc A[p, 4kc..4kc+3] . G[x, y, 4kc..4kc+3].re/im     (DMMA, axis 3)
-//     s[p] += w_y[p, y] C[p, y]                                               (axis 2)
-//   acc[p] += w_x[p, x] s[p]                                                  (axis 1)
-// which is the reference's contraction order c -> b -> a (nufft.py:269-271).
+// Units.  k_units cuts every box into greedy depth runs of <= 8 points whose
+// depth span is <= 7 cells: span <= 3 runs use K = 16 depths (4 k-chunks),
+// longer ones K = 20 (5 k-chunks).  A unit's 8 points are the DMMA's M rows.
+//
+// Per unit, with rows r = (x, y) of the box's (bi+12) x (bj+12) footprint in
+// 8-row tiles:
+//   C_re/im[p, r] = sum_k W3[p, k] G[r, k].re/im        (DMMA; axis 3, nufft.py:269)
+//   acc[p] += W1[p, x(r)] W2[p, y(r)] C[p, r]           (axes 2 and 1, nufft.py:270-271)
+// and the 3 x 13 window weights of the unit's points are themselves one
+// DMMA each (A = powers of delta, B = the fitted polynomial coefficients).
+//
+// Pipeline.  One CTA of 12 warps per SM, persistent over work items (tile,
+// unit range).  Two tile buffers: item k's tile is loaded while item k-1 is
+// being computed; the last warp to finish an item (smem counter) issues the
+// TMA for item k+2 into the freed buffer, so warps never wait for each other.
 #include <cuda.h>
+
+#include <cub/device/device_scan.cuh>
 
 #include "vfn_device.cuh"
 
@@ -26,22 +35,26 @@ namespace vfn {
 namespace m6 {
 
 constexpr int kUnitPts = 8;
-constexpr int kWarps = 8;
-constexpr int kTile = 4;             // tile = 4 x 4 x 4 cells
-constexpr int kT = kTile + 12;       // staged extent per axis (16)
-constexpr int kLine = 128;           // bytes per staged z-half row
-constexpr int kHalf = kT * kT * kLine;  // 32 KB per z-half
-constexpr int kWtO = 4;              // zero pad before j = 0 in the weights table
-constexpr int kWtS = 25;             // weights-table row stride (odd: 4 + 16 + pad)
+constexpr int kWarps = 12;
+constexpr int kTZ = 8;                    // tile depth in cells (x, y: 4)
+constexpr int kSXY = 16;                  // staged x, y extent (4 + 12)
+constexpr int kSZ = 20;                   // staged z extent (8 + 12)
+constexpr int kLine = kSZ * 16;           // bytes per staged (x, y) line
+constexpr int kTileBytes = kSXY * kSXY * kLine;  // 80 KB
+constexpr int kItemUnits = 48;            // units per work item
+// per-warp window-weight tables (doubles); entry off + j holds phi_j(delta)
+constexpr int kAO = 8, kAS = 29;          // axis 3 (A fragments): j in [-8, 21)
+constexpr int kXO = 1, kXS = 17;          // axes 1, 2: j in [-1, 16)
+constexpr int kWarpW = kUnitPts * (kAS + 2 * kXS);
 
 struct Args {
-  const double* u;  // u = z * n per point and axis, input order (from k_map_key)
-  const int32_t* perm;
-  const int32_t* box_start;
-  const int4* items;
-  const int32_t* nitems;
+  const double* u;        // u = z * n per point and axis, input order (k_map_key)
+  const int32_t* perm;    // sorted position -> input row
+  const int4* units;      // (start, cnt | k20 << 4 | kz << 8, box, 0)
+  const int4* items;      // (tile, unit_begin, unit_end, 0)
+  const int32_t* nitems;  // device scalar
   double2* out;
-  const double* poly;
+  const double* poly;     // window polynomial table (13 x (deg+1))
   int deg;
   TorusMap tm;
   BinGeom g;
@@ -53,36 +66,33 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(s), "r"(count));
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
 }
 
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(s), "r"(bytes));
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
       "WAIT_%=:\n"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
       "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(s),
-      "r"(parity));
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
 }
 
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
-                                            uint64_t* bar) {
-  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+__device__ __forceinline__ void tma_load_3d(unsigned dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, unsigned bar) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(d),
-      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(b)
+      " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
 }
 
@@ -92,201 +102,254 @@ __device__ __forceinline__ double2 lds128(unsigned addr) {
   return v;
 }
 
+// Load item `it`'s tile into the buffer at `dst` (completes on `bar`).
+__device__ __forceinline__ void issue_tile(const CUtensorMap* map, const Args& A, int it,
+                                           unsigned dst, unsigned bar) {
+  if (it >= *A.nitems) return;
+  const int tile = A.items[it].x;
+  const BinGeom& G = A.g;
+  const int t2 = tile % G.ntile[2];
+  const int t1 = (tile / G.ntile[2]) % G.ntile[1];
+  const int t0 = tile / (G.ntile[2] * G.ntile[1]);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // prior generic reads of dst
+  mbar_expect_tx(bar, kTileBytes);
+  tma_load_3d(dst, map, 2 * t2 * kTZ, t1 * 4, t0 * 4, bar);
+}
+
+// One unit: <= 8 points of one box sharing the box's rows.
+template <int BXY, int KC>
+__device__ __forceinline__ void gather_unit(const Args& A, const double (&cb)[4][2], double* wt,
+                                            unsigned tile_s, int tile, int ox, int oy, int oz,
+                                            int4 desc, int lane) {
+  constexpr int XB = BXY + 12, YB = BXY + 12;  // box footprint rows per axis
+  constexpr int R = XB * YB;
+  constexpr int NT = (R + 7) / 8;
+  constexpr int NB = 4 / BXY;                  // boxes per tile along x and y
+  const int g = lane >> 2, tig = lane & 3;
+  const int start = desc.x, cnt = desc.y & 15, kz = desc.y >> 8;
+  const int bt = desc.z - tile * (NB * NB);
+  const int X0 = (bt / NB) * BXY, Y0 = (bt % NB) * BXY;
+
+  const bool valid = g < cnt;
+  int64_t prow = 0;
+  double uu[3] = {0.0, 0.0, 0.0};
+  if (valid) {
+    prow = __ldg(A.perm + start + g);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) uu[d] = __ldg(A.u + 3 * prow + d);
+  }
+  int cell[3];
+  double dl[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) cell[d] = cell_from_u(uu[d], A.tm.nd[d], A.tm.n[d], dl[d]);
+  // offsets inside the box; idle lanes and out-of-domain points (key 0) are
+  // pinned to 0 so every table index stays in bounds
+  const int ci0 = cell[0] - ox - X0, cj0 = cell[1] - oy - Y0, ck0 = cell[2] - oz;
+  const bool inbox = valid && ci0 >= 0 && ci0 < BXY && cj0 >= 0 && cj0 < BXY && ck0 >= 0 && ck0 < kTZ;
+  const int ci = inbox ? ci0 : 0, cj = inbox ? cj0 : 0, ck = inbox ? ck0 : 0;
+
+  // window weights W[p, j] = sum_d delta_p^d C[d, j] on the three axes (DMMA)
+  double* wA = wt;                              // [8][kAS]  axis 3
+  double* wX = wt + kUnitPts * kAS;             // [8][kXS]  axis 1
+  double* wY = wX + kUnitPts * kXS;             // [8][kXS]  axis 2
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double x1 = dl[d], x2 = x1 * x1, x4 = x2 * x2;
+    double pw = tig == 0 ? 1.0 : (tig == 1 ? x1 : (tig == 2 ? x2 : x2 * x1));
+    double w00 = 0.0, w01 = 0.0, w10 = 0.0, w11 = 0.0;
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) {
+      dmma(w00, w01, pw, cb[kc][0]);
+      dmma(w10, w11, pw, cb[kc][1]);
+      pw *= x4;
+    }
+    double* row = d == 2 ? wA + g * kAS + kAO : (d == 0 ? wX : wY) + g * kXS + kXO;
+    row[2 * tig] = w00;      // j = 2 tig, 2 tig + 1, 8 + 2 tig, 9 + 2 tig;
+    row[2 * tig + 1] = w01;  // j >= 13 come out exactly 0 (zero coefficients)
+    row[8 + 2 * tig] = w10;
+    row[9 + 2 * tig] = w11;
+  }
+  __syncwarp();
+  // A fragments: axis-3 weights of point g at staged depth kz + 4 kc + tig
+  double a[KC];
+  const double* wa = wA + g * kAS + kAO + kz + tig - ck;
+#pragma unroll
+  for (int kc = 0; kc < KC; ++kc) a[kc] = inbox ? wa[4 * kc] : 0.0;
+  const double* wx = wX + g * kXS + kXO - ci;  // wx[x], x in [0, XB)
+  const double* wy = wY + g * kXS + kXO - cj;  // wy[y], y in [0, YB)
+
+  // B rows: lane row r = 8t + g; C rows: r1 = 8t + 2 tig and r1 + 1
+  int bx = 0, by = g;        // g < 8 <= YB
+  int x1 = 0, y1 = 2 * tig;  // 2 tig + 1 < 8 <= YB
+  const unsigned zoff = (unsigned)(kz + tig) * 16u;
+  const unsigned base = tile_s + zoff;
+  double acc_re = 0.0, acc_im = 0.0;
+#pragma unroll 2
+  for (int t = 0; t < NT; ++t) {
+    const int rb = 8 * t + g;
+    const unsigned line = rb < R ? (unsigned)((X0 + bx) * kSXY + (Y0 + by)) : 0u;
+    const unsigned addr = base + line * kLine;
+    double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
+#pragma unroll
+    for (int kc = 0; kc < KC; ++kc) {
+      const double2 v = lds128(addr + kc * 64);
+      dmma(cr0, cr1, a[kc], v.x);
+      dmma(ci0, ci1, a[kc], v.y);
+    }
+    const int r1 = 8 * t + 2 * tig;
+    int x2 = x1, y2 = y1 + 1;
+    if (y2 == YB) { y2 = 0; ++x2; }
+    const double wa1 = r1 < R ? wx[x1] * wy[y1] : 0.0;
+    const double wa2 = r1 + 1 < R ? wx[x2] * wy[y2] : 0.0;
+    acc_re = fma(wa1, cr0, acc_re);
+    acc_im = fma(wa1, ci0, acc_im);
+    acc_re = fma(wa2, cr1, acc_re);
+    acc_im = fma(wa2, ci1, acc_im);
+    by += 8;
+    if (by >= YB) { by -= YB; ++bx; }
+    y1 += 8;
+    if (y1 >= YB) { y1 -= YB; ++x1; }
+  }
+  acc_re += __shfl_xor_sync(0xffffffffu, acc_re, 1);
+  acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 1);
+  acc_re += __shfl_xor_sync(0xffffffffu, acc_re, 2);
+  acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 2);
+  if (valid && tig == 0) A.out[prow] = make_double2(acc_re, acc_im);
+  __syncwarp();  // the weight tables are rewritten by the next unit
+}
+
 template <int BXY>
-__global__ void __launch_bounds__(kWarps * 32, 2)
+__global__ void __launch_bounds__(kWarps * 32, 1)
     k_gather_m6(const __grid_constant__ CUtensorMap tmap, const Args A) {
-  constexpr int XB = BXY + 12;  // box rows per axis
-  constexpr int YB = BXY + 12;
-  constexpr int W = 13;
   extern __shared__ unsigned char smem_raw[];
-  // 1024-byte aligned tile for the 128B swizzle pattern
   const unsigned raw = (unsigned)__cvta_generic_to_shared(smem_raw);
-  const unsigned tile_s = (raw + 1023u) & ~1023u;
-  unsigned char* tile_g = smem_raw + (tile_s - raw);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(tile_g + 2 * kHalf);  // 1024-aligned
-  double* sWt = reinterpret_cast<double*>(tile_g + 2 * kHalf + 16);  // [kWarps][3][8][kWtS]
-  int* sBox = reinterpret_cast<int*>(sWt + kWarps * 3 * kUnitPts * kWtS);  // [bpt + 1]
-  int* sUnit = sBox + 33;                                                  // [bpt + 1]
+  const unsigned tiles_s = (raw + 1023u) & ~1023u;          // 2 x kTileBytes
+  const unsigned bar_s = tiles_s + 2 * kTileBytes;          // full[2]
+  unsigned char* ctl = smem_raw + (bar_s - raw);
+  int* done = reinterpret_cast<int*>(ctl + 16);              // done[2]
+  double* wts = reinterpret_cast<double*>(ctl + 32);         // [kWarps][kWarpW]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tig = lane & 3;
-  // window weights table: entry kWtO + j holds phi_j(delta) of point g on an
-  // axis, j = 0..12; the pads j in [-kWtO, 0) and [13, 16) stay zero
-  for (int i = tid; i < kWarps * 3 * kUnitPts * kWtS; i += blockDim.x) sWt[i] = 0.0;
-  // B fragments of the window-polynomial DMMA: C[d][j], d = 4 kc + tig, j = 8 nb + g
-  double cb[4][2];
+  for (int i = tid; i < kWarps * kWarpW; i += blockDim.x) wts[i] = 0.0;  // zero pads
+  double cb[4][2];  // B fragments of the weights DMMA: C[d = 4 kc + tig][j = 8 nb + g]
 #pragma unroll
   for (int kc = 0; kc < 4; ++kc)
 #pragma unroll
     for (int nb = 0; nb < 2; ++nb) {
       const int d = 4 * kc + tig, j = 8 * nb + g;
-      cb[kc][nb] = (d <= A.deg && j < W) ? A.poly[j * (A.deg + 1) + d] : 0.0;
+      cb[kc][nb] = (d <= A.deg && j < 13) ? A.poly[j * (A.deg + 1) + d] : 0.0;
     }
   if (tid == 0) {
-    mbar_init(bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    mbar_init(bar_s, 1);
+    mbar_init(bar_s + 8, 1);
+    done[0] = 0;
+    done[1] = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    issue_tile(&tmap, A, blockIdx.x, tiles_s, bar_s);
+    issue_tile(&tmap, A, blockIdx.x + gridDim.x, tiles_s + kTileBytes, bar_s + 8);
   }
   __syncthreads();
 
-  const BinGeom& G = A.g;
-  double* wt = sWt + warp * 3 * kUnitPts * kWtS;  // [3][8][kWtS]
+  double* wt = wts + warp * kWarpW;
   const int nitems = *A.nitems;
-  unsigned phase = 0;
-
-  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+  const BinGeom& G = A.g;
+  for (int k = 0;; ++k) {
+    const int it = blockIdx.x + k * gridDim.x;
+    if (it >= nitems) break;
+    const int b = k & 1;
     const int4 item = A.items[it];
     const int tile = item.x;
     const int t2 = tile % G.ntile[2];
     const int t1 = (tile / G.ntile[2]) % G.ntile[1];
     const int t0 = tile / (G.ntile[2] * G.ntile[1]);
-    const int ox = t0 * kTile, oy = t1 * kTile, oz = t2 * kTile;
-    __syncthreads();  // everyone is done reading the previous tile
-    if (tid == 0) {
-      mbar_expect_tx(bar, 2 * kHalf);
-      tma_load_3d(tile_g, &tmap, 2 * oz, oy, ox, bar);
-      tma_load_3d(tile_g + kHalf, &tmap, 2 * oz + 16, oy, ox, bar);
+    const unsigned tile_s = tiles_s + b * kTileBytes;
+    mbar_wait(bar_s + 8 * b, (k >> 1) & 1);
+    for (int ui = item.y + warp; ui < item.z; ui += kWarps) {
+      const int4 desc = __ldg(A.units + ui);
+      if ((desc.y >> 4) & 1)
+        gather_unit<BXY, 5>(A, cb, wt, tile_s, tile, t0 * 4, t1 * 4, t2 * kTZ, desc, lane);
+      else
+        gather_unit<BXY, 4>(A, cb, wt, tile_s, tile, t0 * 4, t1 * 4, t2 * kTZ, desc, lane);
     }
-    if (warp == 0) {
-      const int bpt = G.boxes_per_tile;
-      const int32_t* bs = A.box_start + (int64_t)tile * bpt;
-      int cnt = 0, start = 0;
-      if (lane < bpt) {
-        start = bs[lane];
-        cnt = bs[lane + 1] - start;
+    __syncwarp();
+    if (lane == 0) {
+      if (atomicAdd(&done[b], 1) == kWarps - 1) {  // last warp out refills the buffer
+        done[b] = 0;
+        issue_tile(&tmap, A, it + 2 * gridDim.x, tile_s, bar_s + 8 * b);
       }
-      int incl = (cnt + kUnitPts - 1) / kUnitPts;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      if (lane < bpt) {
-        sBox[lane] = start;
-        sUnit[lane + 1] = incl;
-      }
-      if (lane == 0) sUnit[0] = 0;
-      if (lane == bpt - 1) sBox[bpt] = start + cnt;
     }
-    __syncthreads();
-
-    bool waited = false;
-    for (int u = item.y + warp; u < item.z; u += kWarps) {
-      int b = 0;
-      while (sUnit[b + 1] <= u) ++b;
-      const int p0 = sBox[b] + (u - sUnit[b]) * kUnitPts;
-      const int cnt = min(kUnitPts, sBox[b + 1] - p0);
-      constexpr int NB = kTile / BXY;  // boxes per tile along x and y (z: 1)
-      const int by = b % NB, bx = b / NB;
-      const int X0 = bx * BXY, Y0 = by * BXY;
-
-      // point g of the unit: nearest cell and offset from u (nufft.py:256-257)
-      const bool valid = g < cnt;
-      int64_t prow = 0;
-      double uu[3] = {0.0, 0.0, 0.0};
-      if (valid) {
-        prow = __ldg(A.perm + p0 + g);
-#pragma unroll
-        for (int d = 0; d < 3; ++d) uu[d] = __ldg(A.u + 3 * prow + d);
-      }
-      int cell[3];
-      double dl[3];
-#pragma unroll
-      for (int d = 0; d < 3; ++d) cell[d] = cell_from_u(uu[d], A.tm.nd[d], A.tm.n[d], dl[d]);
-      // offsets inside the box; idle lanes (and out-of-domain points, whose
-      // key is 0) are pinned to 0 so every table index stays in bounds
-      const bool inbox = valid && cell[0] - ox - X0 >= 0 && cell[0] - ox - X0 < BXY &&
-                         cell[1] - oy - Y0 >= 0 && cell[1] - oy - Y0 < BXY &&
-                         cell[2] - oz >= 0 && cell[2] - oz < kTile;
-      const int ci = inbox ? cell[0] - ox - X0 : 0;
-      const int cj = inbox ? cell[1] - oy - Y0 : 0;
-      const int ck = inbox ? cell[2] - oz : 0;
-      // window weights of point g on all three axes by DMMA:
-      // W[p, j] = sum_d delta_p^d C[d, j]   (A = powers of delta, B = coefficients)
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const double x1 = dl[d], x2 = x1 * x1, x4 = x2 * x2;
-        double pw = tig == 0 ? 1.0 : (tig == 1 ? x1 : (tig == 2 ? x2 : x2 * x1));
-        double w00 = 0.0, w01 = 0.0, w10 = 0.0, w11 = 0.0;
-#pragma unroll
-        for (int kc = 0; kc < 4; ++kc) {
-          dmma(w00, w01, pw, cb[kc][0]);
-          dmma(w10, w11, pw, cb[kc][1]);
-          pw *= x4;
-        }
-        double* row = wt + (d * kUnitPts + g) * kWtS + kWtO;
-        row[2 * tig] = w00;
-        row[2 * tig + 1] = w01;
-        if (8 + 2 * tig < W) row[8 + 2 * tig] = w10;  // j = 13..15 stay zero
-        if (9 + 2 * tig < W) row[9 + 2 * tig] = w11;
-      }
-      __syncwarp();
-      const double* w0 = wt + (0 * kUnitPts + g) * kWtS + kWtO - ci;  // w0[x]: axis 1
-      const double* w1 = wt + (1 * kUnitPts + g) * kWtS + kWtO - cj;  // w1[y]: axis 2
-      const double* w2 = wt + (2 * kUnitPts + g) * kWtS + kWtO - ck;  // w2[k]: axis 3
-      double a[4];
-#pragma unroll
-      for (int kc = 0; kc < 4; ++kc) a[kc] = inbox ? w2[4 * kc + tig] : 0.0;
-      double wy[2][2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int y = 8 * h + 2 * tig + e;
-          wy[h][e] = y < YB ? w1[y] : 0.0;
-        }
-      // B-fragment row of this lane per half: y = 8h + g (clamped into the box)
-      unsigned off[2][4];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int y = Y0 + min(8 * h + g, YB - 1);
-        const int sw = y & 7;
-#pragma unroll
-        for (int kc = 0; kc < 4; ++kc)
-          off[h][kc] = tile_s + (kc >> 1) * kHalf + (X0 * kT + y) * kLine +
-                       16 * (((kc & 1) * 4 + tig) ^ sw);
-      }
-      if (!waited) {
-        mbar_wait(bar, phase);
-        waited = true;
-      }
-      double acc_re = 0.0, acc_im = 0.0;
-#pragma unroll
-      for (int x = 0; x < XB; ++x) {
-        double sre = 0.0, sim = 0.0;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
-#pragma unroll
-          for (int kc = 0; kc < 4; ++kc) {
-            const double2 v = lds128(off[h][kc] + x * kT * kLine);
-            dmma(cr0, cr1, a[kc], v.x);
-            dmma(ci0, ci1, a[kc], v.y);
-          }
-          sre = fma(wy[h][0], cr0, sre);
-          sre = fma(wy[h][1], cr1, sre);
-          sim = fma(wy[h][0], ci0, sim);
-          sim = fma(wy[h][1], ci1, sim);
-        }
-        const double w = w0[x];
-        acc_re = fma(w, sre, acc_re);
-        acc_im = fma(w, sim, acc_im);
-      }
-      acc_re += __shfl_xor_sync(0xffffffffu, acc_re, 1);
-      acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 1);
-      acc_re += __shfl_xor_sync(0xffffffffu, acc_re, 2);
-      acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 2);
-      if (valid && tig == 0) A.out[prow] = make_double2(acc_re, acc_im);
-      __syncwarp();
-    }
-    if (!waited) mbar_wait(bar, phase);  // keep the phase bookkeeping uniform
-    phase ^= 1u;
   }
 }
 
 }  // namespace m6
 
+// ------------------------------------------------------------------ units
+
+// Greedy depth runs of one box's points (sorted by depth): <= 8 points and
+// depth span <= 7 cells; K20 when the span exceeds 3.
+__device__ __forceinline__ int box_depth(uint32_t key, int cpb, int bij) {
+  return (int)(key % (uint32_t)cpb) / bij;
+}
+
+template <bool WRITE>
+__global__ void k_units(const uint32_t* __restrict__ keys, const int32_t* __restrict__ box_start,
+                        int64_t nboxes, int cpb, int bij, const int32_t* __restrict__ uoff,
+                        int32_t* __restrict__ ucount, int4* __restrict__ units) {
+  int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b > nboxes) return;
+  if (b == nboxes) {
+    if (!WRITE) ucount[b] = 0;
+    return;
+  }
+  const int be = box_start[b + 1];
+  int s = box_start[b];
+  int n = 0;
+  int4* dst = WRITE ? units + uoff[b] : nullptr;
+  while (s < be) {
+    const int k0 = box_depth(keys[s], cpb, bij);
+    int e = s + 1, klast = k0;
+    while (e < be && e - s < m6::kUnitPts) {
+      const int k = box_depth(keys[e], cpb, bij);
+      if (k - k0 > 7) break;
+      klast = k;
+      ++e;
+    }
+    if (WRITE) {
+      const int k20 = klast - k0 > 3 ? 1 : 0;
+      const int kz = k20 ? 0 : min(k0, 4);
+      dst[n] = make_int4(s, (e - s) | (k20 << 4) | (kz << 8), (int)b, 0);
+    }
+    ++n;
+    s = e;
+  }
+  if (!WRITE) ucount[b] = n;
+}
+
+__global__ void k_m6_tile_items(const int32_t* __restrict__ uoff, int64_t ntiles, int bpt,
+                                int32_t* __restrict__ nitems) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > ntiles) return;
+  if (t == ntiles) {
+    nitems[t] = 0;
+    return;
+  }
+  const int units = uoff[(t + 1) * bpt] - uoff[t * bpt];
+  nitems[t] = (units + m6::kItemUnits - 1) / m6::kItemUnits;
+}
+
+__global__ void k_m6_items(const int32_t* __restrict__ uoff, const int32_t* __restrict__ ioff,
+                           int64_t ntiles, int bpt, int4* __restrict__ items) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  const int first = ioff[t], n = ioff[t + 1] - first;
+  const int u0 = uoff[t * bpt], u1 = uoff[(t + 1) * bpt];
+  for (int j = 0; j < n; ++j)
+    items[first + j] = make_int4((int)t, u0 + j * m6::kItemUnits, min(u1, u0 + (j + 1) * m6::kItemUnits), 0);
+}
+
 // Tensor map over the ghost-padded grid as doubles: (2 P2, P1, P0), box
-// (16 doubles, 16, 16), 128B swizzle.
+// (40 doubles, 16, 16), no swizzle.
 int make_grid_tmap(vfn_plan* p) {
   p->has_tmap = false;
   if (p->m != 6) return VFN_OK;
@@ -302,59 +365,87 @@ int make_grid_tmap(vfn_plan* p) {
                           CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
   cuuint64_t dims[3] = {(cuuint64_t)(2 * p->P[2]), (cuuint64_t)p->P[1], (cuuint64_t)p->P[0]};
   cuuint64_t strides[2] = {(cuuint64_t)(2 * p->P[2] * 8), (cuuint64_t)(2 * p->P[2] * 8 * p->P[1])};
-  cuuint32_t box[3] = {16, (cuuint32_t)m6::kT, (cuuint32_t)m6::kT};
+  cuuint32_t box[3] = {2 * m6::kSZ, (cuuint32_t)m6::kSXY, (cuuint32_t)m6::kSXY};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = reinterpret_cast<Fn>(fn)(&p->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, p->grid, dims,
                                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(VFN_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   p->has_tmap = true;
   return VFN_OK;
 }
 
-size_t m6_smem_bytes(int deg) {
-  size_t b = 1024 + 2 * m6::kHalf;
-  b += 16 + sizeof(double) * m6::kWarps * 3 * m6::kUnitPts * m6::kWtS;
-  b += sizeof(int) * (33 + 34);
-  return b;
+static size_t m6_smem_bytes() {
+  return 1024 + 2 * m6::kTileBytes + 32 + sizeof(double) * m6::kWarps * m6::kWarpW;
+}
+
+bool m6_applicable(const vfn_plan* p, const BinGeom& g) {
+  return p->m == 6 && p->has_tmap && p->poly.deg <= 15 && g.tile[0] == 4 && g.tile[1] == 4 &&
+         g.tile[2] == m6::kTZ && g.box[2] == m6::kTZ && g.box[0] == g.box[1] &&
+         (g.box[0] == 1 || g.box[0] == 2);
 }
 
 template <int BXY>
 static int launch(vfn_plan* p, const m6::Args& A, cudaStream_t s) {
-  const size_t smem = m6_smem_bytes(p->poly.deg);
+  const size_t smem = m6_smem_bytes();
   VFN_CUDA(cudaFuncSetAttribute(m6::k_gather_m6<BXY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
-  int dev = 0, nsm = 148, per_sm = 0;
+  int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  VFN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, m6::k_gather_m6<BXY>,
-                                                         m6::kWarps * 32, smem));
-  if (per_sm < 1) return fail(VFN_ERR_INVALID, "m=6 gather does not fit on an SM");
-  m6::k_gather_m6<BXY><<<nsm * per_sm, m6::kWarps * 32, smem, s>>>(p->tmap, A);
+  m6::k_gather_m6<BXY><<<nsm, m6::kWarps * 32, smem, s>>>(p->tmap, A);
   VFN_CUDA(cudaGetLastError());
   return VFN_OK;
 }
 
-bool m6_applicable(const vfn_plan* p, const BinGeom& g) {
-  return p->m == 6 && p->has_tmap && p->poly.deg <= 15 && g.tile[0] == 4 && g.tile[1] == 4 && g.tile[2] == 4 &&
-         g.box[2] == 4 && g.box[0] == g.box[1] && (g.box[0] == 1 || g.box[0] == 2);
-}
-
-int launch_m6(vfn_plan* p, const double* u, const int32_t* perm, const int32_t* box_start,
-              const int4* items, const int32_t* nitems, double2* out, const BinGeom& g,
+// Build units and items from the box offsets, then run the m = 6 gather.
+int launch_m6(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t* keys_sorted,
+              const int32_t* box_start, double2* out, const BinGeom& g, int64_t M,
               cudaStream_t s) {
+  const int64_t nb = g.nboxes;
+  const int bij = g.box[0] * g.box[1];
+  // scratch: ucount/uoff (nb + 1 each), nitems/ioff (ntiles + 1 each)
+  VFN_CHECK(p->uscratch.ensure(sizeof(int32_t) * (2 * (nb + 1) + 2 * (g.ntiles + 1))));
+  int32_t* ucount = p->uscratch.as<int32_t>();
+  int32_t* uoff = ucount + (nb + 1);
+  int32_t* nitems = uoff + (nb + 1);
+  int32_t* ioff = nitems + (g.ntiles + 1);
+  const unsigned bb = (unsigned)((nb + 1 + 255) / 256);
+  k_units<false><<<bb, 256, 0, s>>>(keys_sorted, box_start, nb, g.cells_per_box, bij, nullptr,
+                                    ucount, nullptr);
+  VFN_CUDA(cudaGetLastError());
+  size_t t1 = 0, t2 = 0;
+  VFN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t1, ucount, uoff, (int)(nb + 1), s));
+  VFN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, nitems, ioff, (int)(g.ntiles + 1), s));
+  VFN_CHECK(p->sort_tmp.ensure(std::max(t1, t2)));
+  VFN_CUDA(cub::DeviceScan::ExclusiveSum(p->sort_tmp.ptr, t1, ucount, uoff, (int)(nb + 1), s));
+  // units <= M (each holds >= 1 point)
+  VFN_CHECK(p->units.ensure(sizeof(int4) * (M + 1)));
+  k_units<true><<<bb, 256, 0, s>>>(keys_sorted, box_start, nb, g.cells_per_box, bij, uoff, nullptr,
+                                   p->units.as<int4>());
+  VFN_CUDA(cudaGetLastError());
+  const unsigned tb = (unsigned)((g.ntiles + 1 + 255) / 256);
+  k_m6_tile_items<<<tb, 256, 0, s>>>(uoff, g.ntiles, g.boxes_per_tile, nitems);
+  VFN_CUDA(cudaGetLastError());
+  VFN_CUDA(cub::DeviceScan::ExclusiveSum(p->sort_tmp.ptr, t2, nitems, ioff, (int)(g.ntiles + 1), s));
+  const int64_t max_items = std::min<int64_t>(g.ntiles, M) + M / m6::kItemUnits + 1;
+  VFN_CHECK(p->items.ensure(sizeof(int4) * max_items));
+  k_m6_items<<<tb, 256, 0, s>>>(uoff, ioff, g.ntiles, g.boxes_per_tile, p->items.as<int4>());
+  VFN_CUDA(cudaGetLastError());
+
   m6::Args A;
   A.u = u;
   A.perm = perm;
-  A.box_start = box_start;
-  A.items = items;
-  A.nitems = nitems;
+  A.units = p->units.as<int4>();
+  A.items = p->items.as<int4>();
+  A.nitems = ioff + g.ntiles;
   A.out = out;
   A.poly = p->poly.dev;
   A.deg = p->poly.deg;
   A.tm = p->map;
   A.g = g;
+  cudaEventRecord(p->ev[1], s);  // gather timing starts here (binning prep excluded)
   return g.box[0] == 1 ? launch<1>(p, A, s) : launch<2>(p, A, s);
 }
 

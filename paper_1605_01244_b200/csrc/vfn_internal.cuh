@@ -89,6 +89,7 @@ struct BinGeom {
   int ntile[3];   // tiles per axis = ceil(n / tile)
   int nbox[3];    // boxes per tile per axis
   int boxes_per_tile;
+  int cells_per_box;  // key = (tile * boxes_per_tile + box) * cells_per_box + cell
   int64_t ntiles;
   int64_t nboxes;  // ntiles * boxes_per_tile
 };
@@ -122,7 +123,7 @@ struct vfn_plan {
   CUtensorMap tmap;        // TMA view of `grid` for the m = 6 gather
   bool has_tmap = false;
   // evaluate scratch (grow-only)
-  vfn::DevBuf pts, out, uvals, keys, keys_sorted, idx, perm, sort_tmp, box_start, items, misc;
+  vfn::DevBuf pts, out, uvals, keys, keys_sorted, idx, perm, sort_tmp, box_start, items, units, uscratch, misc;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   float last_gather_ms = 0.f, last_total_ms = 0.f;
 };
@@ -156,8 +157,8 @@ int rect_eval(int device, const int64_t nmodes[3], const double a[3], const doub
 BinGeom choose_geometry(const vfn_plan* p, int64_t M);
 int make_grid_tmap(vfn_plan* p);
 bool m6_applicable(const vfn_plan* p, const BinGeom& g);
-int launch_m6(vfn_plan* p, const double* u, const int32_t* perm, const int32_t* box_start,
-              const int4* items, const int32_t* nitems, double2* out, const BinGeom& g,
+int launch_m6(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t* keys_sorted,
+              const int32_t* box_start, double2* out, const BinGeom& g, int64_t M,
               cudaStream_t s);
 
 }  // namespace vfn

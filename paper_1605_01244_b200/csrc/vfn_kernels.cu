@@ -35,15 +35,21 @@ __global__ void k_map_key(const double* __restrict__ pts, int64_t M, TorusMap tm
     atomicMin(bad, (unsigned long long)i);
     cell[0] = cell[1] = cell[2] = 0;  // any in-range key; the call fails anyway
   }
-  int t[3], in[3];
+  // key = (tile * boxes_per_tile + box) * cells_per_box + cell-in-box, tiles
+  // and boxes row-major, cells in a box depth-major (k, i, j) so that a box's
+  // points come out sorted by depth (the gather's units are depth runs)
+  int t[3], in[3], c[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     t[d] = cell[d] / g.tile[d];
-    in[d] = (cell[d] - t[d] * g.tile[d]) / g.box[d];
+    const int r = cell[d] - t[d] * g.tile[d];
+    in[d] = r / g.box[d];
+    c[d] = r - in[d] * g.box[d];
   }
   int64_t tile_id = ((int64_t)t[0] * g.ntile[1] + t[1]) * g.ntile[2] + t[2];
   int box_id = (in[0] * g.nbox[1] + in[1]) * g.nbox[2] + in[2];
-  keys[i] = (uint32_t)(tile_id * g.boxes_per_tile + box_id);
+  int cell_id = (c[2] * g.box[0] + c[0]) * g.box[1] + c[1];
+  keys[i] = (uint32_t)((tile_id * g.boxes_per_tile + box_id) * g.cells_per_box + cell_id);
   if (iota) iota[i] = (int32_t)i;
 }
 
