@@ -9,9 +9,9 @@
 // columns of a tile; inside a box the points are sorted by depth (the bin key
 // numbers cells depth-major).
 //
-// Units.  k_units cuts every box into greedy depth runs of <= 8 points whose
-// depth span is <= 7 cells: span <= 3 runs use K = 16 depths (4 k-chunks),
-// longer ones K = 20 (5 k-chunks).  A unit's 8 points are the DMMA's M rows.
+// Units.  A box's points sorted by depth are cut into chunks of 8 (the
+// DMMA's M rows); a chunk spans <= 7 depths of the 8-deep box, and uses K = 16
+// depths (4 k-chunks) when it spans <= 3 cells, K = 20 (5 k-chunks) otherwise.
 //
 // Per unit, with rows r = (x, y) of the box's (bi+12) x (bj+12) footprint in
 // 8-row tiles:
@@ -286,44 +286,38 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 
 // ------------------------------------------------------------------ units
 
-// Greedy depth runs of one box's points (sorted by depth): <= 8 points and
-// depth span <= 7 cells; K20 when the span exceeds 3.
+// A box's points are sorted by depth and the box is 8 cells deep, so any 8
+// consecutive points span <= 7 depths: units are the box's chunks of 8,
+// using K = 16 depths when the chunk spans <= 3 cells and K = 20 otherwise.
 __device__ __forceinline__ int box_depth(uint32_t key, int cpb, int bij) {
   return (int)(key % (uint32_t)cpb) / bij;
 }
 
-template <bool WRITE>
-__global__ void k_units(const uint32_t* __restrict__ keys, const int32_t* __restrict__ box_start,
-                        int64_t nboxes, int cpb, int bij, const int32_t* __restrict__ uoff,
-                        int32_t* __restrict__ ucount, int4* __restrict__ units) {
+__global__ void k_unit_counts(const int32_t* __restrict__ box_start, int64_t nboxes,
+                              int32_t* __restrict__ ucount) {
   int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b > nboxes) return;
-  if (b == nboxes) {
-    if (!WRITE) ucount[b] = 0;
-    return;
+  ucount[b] = b == nboxes ? 0 : (box_start[b + 1] - box_start[b] + m6::kUnitPts - 1) / m6::kUnitPts;
+}
+
+// one warp per box; lanes write the box's chunks
+__global__ void k_write_units(const uint32_t* __restrict__ keys, const int32_t* __restrict__ box_start,
+                              int64_t nboxes, int cpb, int bij, const int32_t* __restrict__ uoff,
+                              int4* __restrict__ units) {
+  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (b >= nboxes) return;
+  const int bs = box_start[b], be = box_start[b + 1];
+  const int n = (be - bs + m6::kUnitPts - 1) / m6::kUnitPts;
+  int4* dst = units + uoff[b];
+  for (int c = lane; c < n; c += 32) {
+    const int s = bs + c * m6::kUnitPts;
+    const int e = min(be, s + m6::kUnitPts);
+    const int k0 = box_depth(keys[s], cpb, bij), k1 = box_depth(keys[e - 1], cpb, bij);
+    const int k20 = k1 - k0 > 3 ? 1 : 0;
+    const int kz = k20 ? 0 : min(k0, 4);
+    dst[c] = make_int4(s, (e - s) | (k20 << 4) | (kz << 8), (int)b, 0);
   }
-  const int be = box_start[b + 1];
-  int s = box_start[b];
-  int n = 0;
-  int4* dst = WRITE ? units + uoff[b] : nullptr;
-  while (s < be) {
-    const int k0 = box_depth(keys[s], cpb, bij);
-    int e = s + 1, klast = k0;
-    while (e < be && e - s < m6::kUnitPts) {
-      const int k = box_depth(keys[e], cpb, bij);
-      if (k - k0 > 7) break;
-      klast = k;
-      ++e;
-    }
-    if (WRITE) {
-      const int k20 = klast - k0 > 3 ? 1 : 0;
-      const int kz = k20 ? 0 : min(k0, 4);
-      dst[n] = make_int4(s, (e - s) | (k20 << 4) | (kz << 8), (int)b, 0);
-    }
-    ++n;
-    s = e;
-  }
-  if (!WRITE) ucount[b] = n;
 }
 
 __global__ void k_m6_tile_items(const int32_t* __restrict__ uoff, int64_t ntiles, int bpt,
@@ -412,8 +406,7 @@ int launch_m6(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t*
   int32_t* nitems = uoff + (nb + 1);
   int32_t* ioff = nitems + (g.ntiles + 1);
   const unsigned bb = (unsigned)((nb + 1 + 255) / 256);
-  k_units<false><<<bb, 256, 0, s>>>(keys_sorted, box_start, nb, g.cells_per_box, bij, nullptr,
-                                    ucount, nullptr);
+  k_unit_counts<<<bb, 256, 0, s>>>(box_start, nb, ucount);
   VFN_CUDA(cudaGetLastError());
   size_t t1 = 0, t2 = 0;
   VFN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t1, ucount, uoff, (int)(nb + 1), s));
@@ -422,8 +415,9 @@ int launch_m6(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t*
   VFN_CUDA(cub::DeviceScan::ExclusiveSum(p->sort_tmp.ptr, t1, ucount, uoff, (int)(nb + 1), s));
   // units <= M (each holds >= 1 point)
   VFN_CHECK(p->units.ensure(sizeof(int4) * (M + 1)));
-  k_units<true><<<bb, 256, 0, s>>>(keys_sorted, box_start, nb, g.cells_per_box, bij, uoff, nullptr,
-                                   p->units.as<int4>());
+  k_write_units<<<(unsigned)((nb * 32 + 255) / 256), 256, 0, s>>>(keys_sorted, box_start, nb,
+                                                                  g.cells_per_box, bij, uoff,
+                                                                  p->units.as<int4>());
   VFN_CUDA(cudaGetLastError());
   const unsigned tb = (unsigned)((g.ntiles + 1 + 255) / 256);
   k_m6_tile_items<<<tb, 256, 0, s>>>(uoff, g.ntiles, g.boxes_per_tile, nitems);
