@@ -20,7 +20,7 @@
 // and the 3 x 13 window weights of the unit's points are themselves one
 // DMMA each (A = powers of delta, B = the fitted polynomial coefficients).
 //
-// Pipeline.  One CTA of 12 warps per SM, persistent over work items (tile,
+// Pipeline.  One CTA of 16 warps per SM, persistent over work items (tile,
 // unit range).  Two tile buffers: item k's tile is loaded while item k-1 is
 // being computed; the last warp to finish an item (smem counter) issues the
 // TMA for item k+2 into the freed buffer, so warps never wait for each other.
@@ -35,7 +35,7 @@ namespace vfn {
 namespace m6 {
 
 constexpr int kUnitPts = 8;
-constexpr int kWarps = 12;
+constexpr int kWarps = 16;
 constexpr int kTZ = 8;                    // tile depth in cells (x, y: 4)
 constexpr int kSXY = 16;                  // staged x, y extent (4 + 12)
 constexpr int kSZ = 20;                   // staged z extent (8 + 12)
@@ -117,10 +117,30 @@ __device__ __forceinline__ void issue_tile(const CUtensorMap* map, const Args& A
 }
 
 // One unit: <= 8 points of one box sharing the box's rows.
+// The unit's points (lane quad g owns point g): sorted-position -> input row
+// and its u values.  Issued one unit ahead so the latency hides behind the
+// previous unit's DMMAs.
+struct UnitPoints {
+  int64_t prow;
+  double uu[3];
+};
+
+__device__ __forceinline__ UnitPoints load_unit_points(const Args& A, int4 desc, int g) {
+  UnitPoints up;
+  up.prow = 0;
+  up.uu[0] = up.uu[1] = up.uu[2] = 0.0;
+  if (g < (desc.y & 15)) {
+    up.prow = __ldg(A.perm + desc.x + g);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) up.uu[d] = __ldg(A.u + 3 * up.prow + d);
+  }
+  return up;
+}
+
 template <int BXY, int KC>
 __device__ __forceinline__ void gather_unit(const Args& A, const double (&cb)[4][2], double* wt,
                                             unsigned tile_s, int tile, int ox, int oy, int oz,
-                                            int4 desc, int lane) {
+                                            int4 desc, const UnitPoints& up, int lane) {
   constexpr int XB = BXY + 12, YB = BXY + 12;  // box footprint rows per axis
   constexpr int R = XB * YB;
   constexpr int NT = (R + 7) / 8;
@@ -130,18 +150,13 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double (&cb)[4]
   const int bt = desc.z - tile * (NB * NB);
   const int X0 = (bt / NB) * BXY, Y0 = (bt % NB) * BXY;
 
+  (void)start;
   const bool valid = g < cnt;
-  int64_t prow = 0;
-  double uu[3] = {0.0, 0.0, 0.0};
-  if (valid) {
-    prow = __ldg(A.perm + start + g);
-#pragma unroll
-    for (int d = 0; d < 3; ++d) uu[d] = __ldg(A.u + 3 * prow + d);
-  }
+  const int64_t prow = up.prow;
   int cell[3];
   double dl[3];
 #pragma unroll
-  for (int d = 0; d < 3; ++d) cell[d] = cell_from_u(uu[d], A.tm.nd[d], A.tm.n[d], dl[d]);
+  for (int d = 0; d < 3; ++d) cell[d] = cell_from_u(up.uu[d], A.tm.nd[d], A.tm.n[d], dl[d]);
   // offsets inside the box; idle lanes and out-of-domain points (key 0) are
   // pinned to 0 so every table index stays in bounds
   const int ci0 = cell[0] - ox - X0, cj0 = cell[1] - oy - Y0, ck0 = cell[2] - oz;
@@ -264,13 +279,29 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     const int t1 = (tile / G.ntile[2]) % G.ntile[1];
     const int t0 = tile / (G.ntile[2] * G.ntile[1]);
     const unsigned tile_s = tiles_s + b * kTileBytes;
+    int ui = item.y + warp;
+    int4 desc = make_int4(0, 0, 0, 0);
+    UnitPoints up;
+    if (ui < item.z) {
+      desc = __ldg(A.units + ui);
+      up = load_unit_points(A, desc, g);
+    }
     mbar_wait(bar_s + 8 * b, (k >> 1) & 1);
-    for (int ui = item.y + warp; ui < item.z; ui += kWarps) {
-      const int4 desc = __ldg(A.units + ui);
+    while (ui < item.z) {
+      const int nx = ui + kWarps;
+      int4 desc_n = make_int4(0, 0, 0, 0);
+      UnitPoints up_n;
+      if (nx < item.z) {
+        desc_n = __ldg(A.units + nx);
+        up_n = load_unit_points(A, desc_n, g);
+      }
       if ((desc.y >> 4) & 1)
-        gather_unit<BXY, 5>(A, cb, wt, tile_s, tile, t0 * 4, t1 * 4, t2 * kTZ, desc, lane);
+        gather_unit<BXY, 5>(A, cb, wt, tile_s, tile, t0 * 4, t1 * 4, t2 * kTZ, desc, up, lane);
       else
-        gather_unit<BXY, 4>(A, cb, wt, tile_s, tile, t0 * 4, t1 * 4, t2 * kTZ, desc, lane);
+        gather_unit<BXY, 4>(A, cb, wt, tile_s, tile, t0 * 4, t1 * 4, t2 * kTZ, desc, up, lane);
+      ui = nx;
+      desc = desc_n;
+      up = up_n;
     }
     __syncwarp();
     if (lane == 0) {
