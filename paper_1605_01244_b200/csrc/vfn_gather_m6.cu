@@ -242,6 +242,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   const unsigned bar_s = tiles_s + 2 * kTileBytes;          // full[2]
   unsigned char* ctl = smem_raw + (bar_s - raw);
   int* done = reinterpret_cast<int*>(ctl + 16);              // done[2]
+  int* ctr = done + 2;                                       // next unit of the item in buffer b
   double* wts = reinterpret_cast<double*>(ctl + 32);         // [kWarps][kWarpW]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -258,8 +259,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   if (tid == 0) {
     mbar_init(bar_s, 1);
     mbar_init(bar_s + 8, 1);
-    done[0] = 0;
-    done[1] = 0;
+    done[0] = done[1] = 0;
+    ctr[0] = ctr[1] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     issue_tile(&tmap, A, blockIdx.x, tiles_s, bar_s);
     issue_tile(&tmap, A, blockIdx.x + gridDim.x, tiles_s + kTileBytes, bar_s + 8);
@@ -279,20 +280,29 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     const int t1 = (tile / G.ntile[2]) % G.ntile[1];
     const int t0 = tile / (G.ntile[2] * G.ntile[1]);
     const unsigned tile_s = tiles_s + b * kTileBytes;
-    int ui = item.y + warp;
+    // units are handed out dynamically (smem counter per buffer); each warp
+    // reserves its next unit and prefetches its points before computing the
+    // current one
+    const int nunits = item.z - item.y;
+    auto grab = [&]() {
+      int v = 0;
+      if (lane == 0) v = atomicAdd(&ctr[b], 1);
+      return __shfl_sync(0xffffffffu, v, 0);
+    };
+    int ui = grab();
     int4 desc = make_int4(0, 0, 0, 0);
     UnitPoints up;
-    if (ui < item.z) {
-      desc = __ldg(A.units + ui);
+    if (ui < nunits) {
+      desc = __ldg(A.units + item.y + ui);
       up = load_unit_points(A, desc, g);
     }
     mbar_wait(bar_s + 8 * b, (k >> 1) & 1);
-    while (ui < item.z) {
-      const int nx = ui + kWarps;
+    while (ui < nunits) {
+      const int nx = grab();
       int4 desc_n = make_int4(0, 0, 0, 0);
       UnitPoints up_n;
-      if (nx < item.z) {
-        desc_n = __ldg(A.units + nx);
+      if (nx < nunits) {
+        desc_n = __ldg(A.units + item.y + nx);
         up_n = load_unit_points(A, desc_n, g);
       }
       if ((desc.y >> 4) & 1)
@@ -307,6 +317,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     if (lane == 0) {
       if (atomicAdd(&done[b], 1) == kWarps - 1) {  // last warp out refills the buffer
         done[b] = 0;
+        ctr[b] = 0;
         issue_tile(&tmap, A, it + 2 * gridDim.x, tile_s, bar_s + 8 * b);
       }
     }
@@ -402,7 +413,7 @@ int make_grid_tmap(vfn_plan* p) {
 }
 
 static size_t m6_smem_bytes() {
-  return 1024 + 2 * m6::kTileBytes + 32 + sizeof(double) * m6::kWarps * m6::kWarpW;
+  return 1024 + 2 * m6::kTileBytes + 32 + sizeof(double) * m6::kWarps * m6::kWarpW;  // ctl: bars, done, ctr
 }
 
 bool m6_applicable(const vfn_plan* p, const BinGeom& g) {
