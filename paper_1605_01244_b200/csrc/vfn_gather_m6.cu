@@ -116,6 +116,19 @@ __device__ __forceinline__ void issue_tile(const CUtensorMap* map, const Args& A
   tma_load_3d(dst, map, 2 * t2 * kTZ, t1 * 4, t0 * 4, bar);
 }
 
+// One 8-row DMMA tile: C_re/im[p, n] for the lane's B row at `addr`.
+template <int KC>
+__device__ __forceinline__ void tile_mma(unsigned addr, const double (&a)[KC], double& cr0,
+                                         double& cr1, double& ci0, double& ci1) {
+  cr0 = cr1 = ci0 = ci1 = 0.0;
+#pragma unroll
+  for (int kc = 0; kc < KC; ++kc) {
+    const double2 v = lds128(addr + kc * 64);
+    dmma(cr0, cr1, a[kc], v.x);
+    dmma(ci0, ci1, a[kc], v.y);
+  }
+}
+
 // One unit: <= 8 points of one box sharing the box's rows.
 // The unit's points (lane quad g owns point g): sorted-position -> input row
 // and its u values.  Issued one unit ahead so the latency hides behind the
@@ -142,8 +155,6 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double (&cb)[4]
                                             unsigned tile_s, int tile, int ox, int oy, int oz,
                                             int4 desc, const UnitPoints& up, int lane) {
   constexpr int XB = BXY + 12, YB = BXY + 12;  // box footprint rows per axis
-  constexpr int R = XB * YB;
-  constexpr int NT = (R + 7) / 8;
   constexpr int NB = 4 / BXY;                  // boxes per tile along x and y
   const int g = lane >> 2, tig = lane & 3;
   const int start = desc.x, cnt = desc.y & 15, kz = desc.y >> 8;
@@ -190,40 +201,66 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double (&cb)[4]
   const double* wa = wA + g * kAS + kAO + kz + tig - ck;
 #pragma unroll
   for (int kc = 0; kc < KC; ++kc) a[kc] = inbox ? wa[4 * kc] : 0.0;
-  const double* wx = wX + g * kXS + kXO - ci;  // wx[x], x in [0, XB)
-  const double* wy = wY + g * kXS + kXO - cj;  // wy[y], y in [0, YB)
+  const double* wx = wX + g * kXS + kXO - ci;  // wx[x], x in [0, XB]; zero off the stencil
+  const double* wy = wY + g * kXS + kXO - cj;  // wy[y], y in [0, YB]
 
-  // B rows: lane row r = 8t + g; C rows: r1 = 8t + 2 tig and r1 + 1
-  int bx = 0, by = g;        // g < 8 <= YB
-  int x1 = 0, y1 = 2 * tig;  // 2 tig + 1 < 8 <= YB
-  const unsigned zoff = (unsigned)(kz + tig) * 16u;
-  const unsigned base = tile_s + zoff;
+  // Static row schedule over the box's XB x YB rows, 8 rows per DMMA tile,
+  // chosen so that every lane's B row and C rows are compile-time functions
+  // of (tile, lane) — no cursors, no bounds checks in the hot loop:
+  //   A: one tile per x, rows y = 0..7          (B: y = g;  C: y = 2tig + e)
+  //   B: one tile per x pair, rows y = 8..11    (B: x = 2p + g/4, y = 8 + g%4)
+  //   C: the rows y >= 12                       (BXY=1: x = 8q + n; BXY=2: x = 4q + n/2)
+  // Rows past the box read a clamped valid row and get weight 0.
+  const unsigned base = tile_s + (unsigned)((kz + tig) * 16 + (X0 * kSXY + Y0) * kLine);
+  constexpr unsigned kX = kSXY * kLine;  // x stride
   double acc_re = 0.0, acc_im = 0.0;
-#pragma unroll 2
-  for (int t = 0; t < NT; ++t) {
-    const int rb = 8 * t + g;
-    const unsigned line = rb < R ? (unsigned)((X0 + bx) * kSXY + (Y0 + by)) : 0u;
-    const unsigned addr = base + line * kLine;
-    double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
+  {
+    const double wy0 = wy[2 * tig], wy1 = wy[2 * tig + 1];
+    const unsigned ba = base + g * kLine;
 #pragma unroll
-    for (int kc = 0; kc < KC; ++kc) {
-      const double2 v = lds128(addr + kc * 64);
-      dmma(cr0, cr1, a[kc], v.x);
-      dmma(ci0, ci1, a[kc], v.y);
+    for (int x = 0; x < XB; ++x) {
+      double cr0, cr1, ci0, ci1;
+      tile_mma<KC>(ba + x * kX, a, cr0, cr1, ci0, ci1);
+      const double w = wx[x];
+      acc_re = fma(w, fma(wy0, cr0, wy1 * cr1), acc_re);
+      acc_im = fma(w, fma(wy0, ci0, wy1 * ci1), acc_im);
     }
-    const int r1 = 8 * t + 2 * tig;
-    int x2 = x1, y2 = y1 + 1;
-    if (y2 == YB) { y2 = 0; ++x2; }
-    const double wa1 = r1 < R ? wx[x1] * wy[y1] : 0.0;
-    const double wa2 = r1 + 1 < R ? wx[x2] * wy[y2] : 0.0;
-    acc_re = fma(wa1, cr0, acc_re);
-    acc_im = fma(wa1, ci0, acc_im);
-    acc_re = fma(wa2, cr1, acc_re);
-    acc_im = fma(wa2, ci1, acc_im);
-    by += 8;
-    if (by >= YB) { by -= YB; ++bx; }
-    y1 += 8;
-    if (y1 >= YB) { y1 -= YB; ++x1; }
+  }
+  {
+    const double wy0 = wy[8 + 2 * (tig & 1)], wy1 = wy[9 + 2 * (tig & 1)];
+    const int xb = g >> 2, xc = tig >> 1;
+    const unsigned bb = base + (8 + (g & 3)) * kLine;
+#pragma unroll
+    for (int p = 0; p < (XB + 1) / 2; ++p) {
+      double cr0, cr1, ci0, ci1;
+      tile_mma<KC>(bb + min(2 * p + xb, XB - 1) * kX, a, cr0, cr1, ci0, ci1);
+      const double w = wx[2 * p + xc];
+      acc_re = fma(w, fma(wy0, cr0, wy1 * cr1), acc_re);
+      acc_im = fma(w, fma(wy0, ci0, wy1 * ci1), acc_im);
+    }
+  }
+  if (BXY == 1) {  // rows (x, 12), x = 0..12: two tiles
+    const double wy0 = wy[12];
+    const unsigned bc = base + 12 * kLine;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      double cr0, cr1, ci0, ci1;
+      tile_mma<KC>(bc + min(8 * q + g, XB - 1) * kX, a, cr0, cr1, ci0, ci1);
+      const double w0 = wx[8 * q + 2 * tig] * wy0, w1 = wx[8 * q + 2 * tig + 1] * wy0;
+      acc_re = fma(w0, cr0, fma(w1, cr1, acc_re));
+      acc_im = fma(w0, ci0, fma(w1, ci1, acc_im));
+    }
+  } else {  // rows (x, 12..13), x = 0..13: four tiles
+    const double wy0 = wy[12], wy1 = wy[13];
+    const unsigned bc = base + (12 + (g & 1)) * kLine;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double cr0, cr1, ci0, ci1;
+      tile_mma<KC>(bc + min(4 * q + (g >> 1), XB - 1) * kX, a, cr0, cr1, ci0, ci1);
+      const double w = wx[4 * q + tig];
+      acc_re = fma(w, fma(wy0, cr0, wy1 * cr1), acc_re);
+      acc_im = fma(w, fma(wy0, ci0, wy1 * ci1), acc_im);
+    }
   }
   acc_re += __shfl_xor_sync(0xffffffffu, acc_re, 1);
   acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 1);

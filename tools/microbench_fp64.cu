@@ -155,6 +155,26 @@ __global__ void dmma_lds(double* out, int rows) {
   if (s == 12345.678) out[0] = s;
 }
 
+
+// DMMA latency: one warp per SM, NCH independent dependent-chains
+template <int NCH>
+__global__ void dmma_lat(double* out, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+  double c[NCH][2];
+#pragma unroll
+  for (int i = 0; i < NCH; ++i) { c[i][0] = i; c[i][1] = -i; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < NCH; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+  }
+  double r = 0;
+#pragma unroll
+  for (int i = 0; i < NCH; ++i) r += c[i][0] + c[i][1];
+  if (r == 12345.678) out[0] = r;
+}
+
 template <typename K>
 float time_kernel(K kern, dim3 grid, dim3 block, size_t smem, int reps) {
   cudaEvent_t a, b;
@@ -222,5 +242,14 @@ int main() {
     printf("{\"test\": \"dmma_lds\", \"ldw\": %d, \"ms\": %.4f, \"tflops\": %.3f}\n", LDW, ms, flops / ms / 1e9); \
   }
   RUN_DL(1) RUN_DL(2)
+
+#define RUN_LAT(NCH, WARPS)                                                                   \
+  {                                                                                           \
+    int iters = 20000; dim3 g(nsm), blk(32 * WARPS);                                          \
+    float ms = time_kernel([&](dim3 g, dim3 b, size_t s) { dmma_lat<NCH><<<g, b, s>>>(d, iters); }, g, blk, 0, 3); \
+    double per = ms * 1e-3 * clk_khz * 1e3 / iters;                                           \
+    printf("{\"test\": \"dmma_lat\", \"chains\": %d, \"warps_per_sm\": %d, \"cycles_per_iter\": %.2f, \"cycles_per_dmma_per_warp\": %.2f}\n", NCH, WARPS, per, per / NCH); \
+  }
+  RUN_LAT(1, 1) RUN_LAT(2, 1) RUN_LAT(4, 1) RUN_LAT(8, 1) RUN_LAT(1, 4) RUN_LAT(2, 4) RUN_LAT(4, 4) RUN_LAT(1, 16) RUN_LAT(2, 16)
   return 0;
 }
