@@ -230,10 +230,25 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_gather_dmma(GatherArgs A) {
 
 // ------------------------------------------------------------------ work items
 
+// Per-box point counts from the SORTED keys: equal boxes are runs, so each
+// warp adds one atomic per run it sees (clustered inputs put millions of
+// points in a handful of boxes; per-point atomics would serialise on them).
 __global__ void k_box_counts(const uint32_t* __restrict__ keys, int64_t M, int cells_per_box,
                              int32_t* __restrict__ counts) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < M) atomicAdd(&counts[keys[i] / cells_per_box], 1);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool live = i < M;
+  const uint32_t box = live ? keys[i] / (uint32_t)cells_per_box : 0xffffffffu;
+  const uint32_t prev = __shfl_up_sync(0xffffffffu, box, 1);
+  const bool head = live && (lane == 0 || prev != box);
+  const unsigned heads = __ballot_sync(0xffffffffu, head);
+  const unsigned lives = __ballot_sync(0xffffffffu, live);
+  if (head) {
+    // run = this lane up to the next head (or the last live lane)
+    const unsigned later = heads & ~((2u << lane) - 1u);
+    const int end = later ? __ffs(later) - 1 : 32 - __clz(lives);
+    atomicAdd(&counts[box], end - lane);
+  }
 }
 
 __global__ void k_tile_units(const int32_t* __restrict__ box_start, int64_t ntiles, int bpt,

@@ -379,24 +379,24 @@ __global__ void k_unit_counts(const int32_t* __restrict__ box_start, int64_t nbo
   ucount[b] = b == nboxes ? 0 : (box_start[b + 1] - box_start[b] + m6::kUnitPts - 1) / m6::kUnitPts;
 }
 
-// one warp per box; lanes write the box's chunks
-__global__ void k_write_units(const uint32_t* __restrict__ keys, const int32_t* __restrict__ box_start,
-                              int64_t nboxes, int cpb, int bij, const int32_t* __restrict__ uoff,
-                              int4* __restrict__ units) {
-  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (b >= nboxes) return;
-  const int bs = box_start[b], be = box_start[b + 1];
-  const int n = (be - bs + m6::kUnitPts - 1) / m6::kUnitPts;
-  int4* dst = units + uoff[b];
-  for (int c = lane; c < n; c += 32) {
-    const int s = bs + c * m6::kUnitPts;
-    const int e = min(be, s + m6::kUnitPts);
-    const int k0 = box_depth(keys[s], cpb, bij), k1 = box_depth(keys[e - 1], cpb, bij);
-    const int k20 = k1 - k0 > 3 ? 1 : 0;
-    const int kz = k20 ? 0 : min(k0, 4);
-    dst[c] = make_int4(s, (e - s) | (k20 << 4) | (kz << 8), (int)b, 0);
-  }
+// One thread per sorted point; the point that opens a chunk of 8 in its box
+// writes the unit (fully parallel, also for boxes holding millions of points).
+__global__ void k_write_units(const uint32_t* __restrict__ keys, int64_t M,
+                              const int32_t* __restrict__ box_start, int cpb, int bij,
+                              const int32_t* __restrict__ uoff, int4* __restrict__ units) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  const uint32_t key = keys[i];
+  const int64_t b = key / (uint32_t)cpb;
+  const int bs = box_start[b];
+  const int r = (int)i - bs;
+  if (r % m6::kUnitPts) return;
+  const int be = box_start[b + 1];
+  const int e = min(be, (int)i + m6::kUnitPts);
+  const int k0 = box_depth(key, cpb, bij), k1 = box_depth(keys[e - 1], cpb, bij);
+  const int k20 = k1 - k0 > 3 ? 1 : 0;
+  const int kz = k20 ? 0 : min(k0, 4);
+  units[uoff[b] + r / m6::kUnitPts] = make_int4((int)i, (e - (int)i) | (k20 << 4) | (kz << 8), (int)b, 0);
 }
 
 __global__ void k_m6_tile_items(const int32_t* __restrict__ uoff, int64_t ntiles, int bpt,
@@ -494,9 +494,9 @@ int launch_m6(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t*
   VFN_CUDA(cub::DeviceScan::ExclusiveSum(p->sort_tmp.ptr, t1, ucount, uoff, (int)(nb + 1), s));
   // units <= M (each holds >= 1 point)
   VFN_CHECK(p->units.ensure(sizeof(int4) * (M + 1)));
-  k_write_units<<<(unsigned)((nb * 32 + 255) / 256), 256, 0, s>>>(keys_sorted, box_start, nb,
-                                                                  g.cells_per_box, bij, uoff,
-                                                                  p->units.as<int4>());
+  k_write_units<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(keys_sorted, M, box_start,
+                                                            g.cells_per_box, bij, uoff,
+                                                            p->units.as<int4>());
   VFN_CUDA(cudaGetLastError());
   const unsigned tb = (unsigned)((g.ntiles + 1 + 255) / 256);
   k_m6_tile_items<<<tb, 256, 0, s>>>(uoff, g.ntiles, g.boxes_per_tile, nitems);
