@@ -326,6 +326,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       if (lane == 0) v = atomicAdd(&ctr[b], 1);
       return __shfl_sync(0xffffffffu, v, 0);
     };
+    // the buffer's counter is reset by the warp that issued this tile's TMA,
+    // before the copy completes: grab only after the wait
+    mbar_wait(bar_s + 8 * b, (k >> 1) & 1);
     int ui = grab();
     int4 desc = make_int4(0, 0, 0, 0);
     UnitPoints up;
@@ -333,7 +336,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       desc = __ldg(A.units + item.y + ui);
       up = load_unit_points(A, desc, g);
     }
-    mbar_wait(bar_s + 8 * b, (k >> 1) & 1);
     while (ui < nunits) {
       const int nx = grab();
       int4 desc_n = make_int4(0, 0, 0, 0);
