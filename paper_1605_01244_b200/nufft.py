@@ -340,21 +340,25 @@ class NufftPlan:
         return tuple(box), tuple(tile)
 
     def launch_count(self, M: int) -> int:
-        """Kernels of this library one evaluate of M points launches: map+key,
-        the CUB onesweep radix sort (histogram, exclusive-sum, one pass per 8
-        key bits) and the gather (plus box offsets for the DMMA gather)."""
+        """Kernels of this library one evaluate of M points launches (for M above
+        CUB's single-tile sort threshold): map+key, the onesweep radix sort
+        (histogram, exclusive sum, 2 kernels per 8 key bits), box counts and
+        their scan, the unit/work-item builders and the gather
+        (profiles/r01/launches_c5_v8.md lists them)."""
         if M == 0:
             return 0
         box, tile = self.geometry(M)
         ntiles = 1
         for d in range(3):
             ntiles *= -(-self._n[d] // tile[d])
-        nboxes = ntiles * (tile[0] // box[0]) * (tile[1] // box[1]) * (tile[2] // box[2])
-        bits = max(1, int(nboxes - 1).bit_length())
-        # CUB onesweep (M above its single-tile threshold): histogram + exclusive
-        # sum + 2 kernels per 8-bit pass (profiles/r01/launches_c5_v4.md)
+        nkeys = ntiles * (tile[0] // box[0]) * (tile[1] // box[1]) * (tile[2] // box[2])
+        nkeys *= box[0] * box[1] * box[2]
+        bits = max(1, int(nkeys - 1).bit_length())
         sort = 2 + 2 * -(-bits // 8)
-        prep = 1 + 2 + 1 + 2 + 1  # box counts, scan, tile units, scan, items
+        if self.params.cutoff == 6 and tile[2] == 8:
+            prep = 1 + 2 + (1 + 2 + 1) + (1 + 2 + 1)  # box counts+scan, units+scan+write, items
+        else:
+            prep = 1 + 2 + 1 + 2 + 1                  # box counts+scan, tile units+scan, items
         return 1 + sort + prep + 1
 
     def bin(self, points):
