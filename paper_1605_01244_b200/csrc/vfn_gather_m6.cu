@@ -26,6 +26,8 @@
 // TMA for item k+2 into the freed buffer, so warps never wait for each other.
 #include <cuda.h>
 
+#include <climits>
+
 #include <cub/device/device_scan.cuh>
 
 #include "vfn_device.cuh"
@@ -279,8 +281,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   const unsigned bar_s = tiles_s + 2 * kTileBytes;          // full[2]
   unsigned char* ctl = smem_raw + (bar_s - raw);
   int* done = reinterpret_cast<int*>(ctl + 16);              // done[2]
-  int* ctr = done + 2;                                       // next unit of the item in buffer b
-  double* wts = reinterpret_cast<double*>(ctl + 32);         // [kWarps][kWarpW]
+  int* ctr = done + 2;                                       // ctr[4]: next unit of item k, slot k & 3
+  double* wts = reinterpret_cast<double*>(ctl + 48);         // [kWarps][kWarpW]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tig = lane & 3;
@@ -297,7 +299,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     mbar_init(bar_s, 1);
     mbar_init(bar_s + 8, 1);
     done[0] = done[1] = 0;
-    ctr[0] = ctr[1] = 0;
+    ctr[0] = ctr[1] = ctr[2] = ctr[3] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     issue_tile(&tmap, A, blockIdx.x, tiles_s, bar_s);
     issue_tile(&tmap, A, blockIdx.x + gridDim.x, tiles_s + kTileBytes, bar_s + 8);
@@ -307,42 +309,53 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   double* wt = wts + warp * kWarpW;
   const int nitems = *A.nitems;
   const BinGeom& G = A.g;
-  for (int k = 0;; ++k) {
-    const int it = blockIdx.x + k * gridDim.x;
-    if (it >= nitems) break;
+  // Units are handed out dynamically from per-item smem counters (4 slots,
+  // item k uses slot k & 3; the last warp out of item k resets it).  Each warp
+  // reserves its next unit — from the current item or, when that is
+  // exhausted, from the next one — and prefetches its points before computing
+  // the current unit.
+  auto grab = [&](int slot) {
+    int v = 0;
+    if (lane == 0) v = atomicAdd(&ctr[slot], 1);
+    return __shfl_sync(0xffffffffu, v, 0);
+  };
+  int k = 0;
+  int it = blockIdx.x;
+  int4 item = it < nitems ? A.items[it] : make_int4(0, 0, 0, 0);
+  int ui = it < nitems ? grab(0) : INT_MAX;
+  int4 desc = make_int4(0, 0, 0, 0);
+  UnitPoints up;
+  if (ui < item.z - item.y) {
+    desc = __ldg(A.units + item.y + ui);
+    up = load_unit_points(A, desc, g);
+  }
+  while (it < nitems) {
     const int b = k & 1;
-    const int4 item = A.items[it];
     const int tile = item.x;
     const int t2 = tile % G.ntile[2];
     const int t1 = (tile / G.ntile[2]) % G.ntile[1];
     const int t0 = tile / (G.ntile[2] * G.ntile[1]);
     const unsigned tile_s = tiles_s + b * kTileBytes;
-    // units are handed out dynamically (smem counter per buffer); each warp
-    // reserves its next unit and prefetches its points before computing the
-    // current one
     const int nunits = item.z - item.y;
-    auto grab = [&]() {
-      int v = 0;
-      if (lane == 0) v = atomicAdd(&ctr[b], 1);
-      return __shfl_sync(0xffffffffu, v, 0);
-    };
-    // the buffer's counter is reset by the warp that issued this tile's TMA,
-    // before the copy completes: grab only after the wait
+    const int it_n = it + gridDim.x;
+    const int4 item_n = it_n < nitems ? A.items[it_n] : make_int4(0, 0, 0, 0);
+    const int nunits_n = item_n.z - item_n.y;
     mbar_wait(bar_s + 8 * b, (k >> 1) & 1);
-    int ui = grab();
-    int4 desc = make_int4(0, 0, 0, 0);
-    UnitPoints up;
-    if (ui < nunits) {
-      desc = __ldg(A.units + item.y + ui);
-      up = load_unit_points(A, desc, g);
-    }
+    bool carried = false;
     while (ui < nunits) {
-      const int nx = grab();
+      int nx = grab(k & 3);
+      const bool same = nx < nunits;
       int4 desc_n = make_int4(0, 0, 0, 0);
       UnitPoints up_n;
-      if (nx < nunits) {
+      if (same) {
         desc_n = __ldg(A.units + item.y + nx);
         up_n = load_unit_points(A, desc_n, g);
+      } else {
+        nx = it_n < nitems ? grab((k + 1) & 3) : INT_MAX;
+        if (nx < nunits_n) {
+          desc_n = __ldg(A.units + item_n.y + nx);
+          up_n = load_unit_points(A, desc_n, g);
+        }
       }
       if ((desc.y >> 4) & 1)
         gather_unit<BXY, 5>(A, cb, wt, tile_s, tile, t0 * 4, t1 * 4, t2 * kTZ, desc, up, lane);
@@ -351,15 +364,30 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       ui = nx;
       desc = desc_n;
       up = up_n;
+      if (!same) {
+        carried = true;
+        break;
+      }
+    }
+    if (!carried) {  // no unit of this item left for this warp: reserve from the next
+      ui = it_n < nitems ? grab((k + 1) & 3) : INT_MAX;
+      if (ui < nunits_n) {
+        desc = __ldg(A.units + item_n.y + ui);
+        up = load_unit_points(A, desc, g);
+      }
     }
     __syncwarp();
     if (lane == 0) {
       if (atomicAdd(&done[b], 1) == kWarps - 1) {  // last warp out refills the buffer
         done[b] = 0;
-        ctr[b] = 0;
+        ctr[k & 3] = 0;
+        __threadfence_block();
         issue_tile(&tmap, A, it + 2 * gridDim.x, tile_s, bar_s + 8 * b);
       }
     }
+    ++k;
+    it = it_n;
+    item = item_n;
   }
 }
 
@@ -452,7 +480,7 @@ int make_grid_tmap(vfn_plan* p) {
 }
 
 static size_t m6_smem_bytes() {
-  return 1024 + 2 * m6::kTileBytes + 32 + sizeof(double) * m6::kWarps * m6::kWarpW;  // ctl: bars, done, ctr
+  return 1024 + 2 * m6::kTileBytes + 48 + sizeof(double) * m6::kWarps * m6::kWarpW;  // ctl: bars, done, ctr
 }
 
 bool m6_applicable(const vfn_plan* p, const BinGeom& g) {
