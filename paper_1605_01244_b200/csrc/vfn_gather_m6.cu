@@ -215,21 +215,28 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double (&cb)[4]
   // Rows past the box read a clamped valid row and get weight 0.
   const unsigned base = tile_s + (unsigned)((kz + tig) * 16 + (X0 * kSXY + Y0) * kLine);
   constexpr unsigned kX = kSXY * kLine;  // x stride
+  // Per part, the lane's C rows have fixed y, so the x-weights are applied
+  // per tile (2 FMA per row pair) and the y-weights once at the end.
   double acc_re = 0.0, acc_im = 0.0;
   {
-    const double wy0 = wy[2 * tig], wy1 = wy[2 * tig + 1];
+    double t0r = 0.0, t1r = 0.0, t0i = 0.0, t1i = 0.0;
     const unsigned ba = base + g * kLine;
 #pragma unroll
     for (int x = 0; x < XB; ++x) {
       double cr0, cr1, ci0, ci1;
       tile_mma<KC>(ba + x * kX, a, cr0, cr1, ci0, ci1);
       const double w = wx[x];
-      acc_re = fma(w, fma(wy0, cr0, wy1 * cr1), acc_re);
-      acc_im = fma(w, fma(wy0, ci0, wy1 * ci1), acc_im);
+      t0r = fma(w, cr0, t0r);
+      t1r = fma(w, cr1, t1r);
+      t0i = fma(w, ci0, t0i);
+      t1i = fma(w, ci1, t1i);
     }
+    const double wy0 = wy[2 * tig], wy1 = wy[2 * tig + 1];
+    acc_re = fma(wy0, t0r, wy1 * t1r);
+    acc_im = fma(wy0, t0i, wy1 * t1i);
   }
   {
-    const double wy0 = wy[8 + 2 * (tig & 1)], wy1 = wy[9 + 2 * (tig & 1)];
+    double t0r = 0.0, t1r = 0.0, t0i = 0.0, t1i = 0.0;
     const int xb = g >> 2, xc = tig >> 1;
     const unsigned bb = base + (8 + (g & 3)) * kLine;
 #pragma unroll
@@ -237,32 +244,45 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double (&cb)[4]
       double cr0, cr1, ci0, ci1;
       tile_mma<KC>(bb + min(2 * p + xb, XB - 1) * kX, a, cr0, cr1, ci0, ci1);
       const double w = wx[2 * p + xc];
-      acc_re = fma(w, fma(wy0, cr0, wy1 * cr1), acc_re);
-      acc_im = fma(w, fma(wy0, ci0, wy1 * ci1), acc_im);
+      t0r = fma(w, cr0, t0r);
+      t1r = fma(w, cr1, t1r);
+      t0i = fma(w, ci0, t0i);
+      t1i = fma(w, ci1, t1i);
     }
+    const double wy0 = wy[8 + 2 * (tig & 1)], wy1 = wy[9 + 2 * (tig & 1)];
+    acc_re = fma(wy0, t0r, fma(wy1, t1r, acc_re));
+    acc_im = fma(wy0, t0i, fma(wy1, t1i, acc_im));
   }
   if (BXY == 1) {  // rows (x, 12), x = 0..12: two tiles
-    const double wy0 = wy[12];
+    double tr = 0.0, ti = 0.0;
     const unsigned bc = base + 12 * kLine;
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       double cr0, cr1, ci0, ci1;
       tile_mma<KC>(bc + min(8 * q + g, XB - 1) * kX, a, cr0, cr1, ci0, ci1);
-      const double w0 = wx[8 * q + 2 * tig] * wy0, w1 = wx[8 * q + 2 * tig + 1] * wy0;
-      acc_re = fma(w0, cr0, fma(w1, cr1, acc_re));
-      acc_im = fma(w0, ci0, fma(w1, ci1, acc_im));
+      const double w0 = wx[8 * q + 2 * tig], w1 = wx[8 * q + 2 * tig + 1];
+      tr = fma(w0, cr0, fma(w1, cr1, tr));
+      ti = fma(w0, ci0, fma(w1, ci1, ti));
     }
+    const double wy0 = wy[12];
+    acc_re = fma(wy0, tr, acc_re);
+    acc_im = fma(wy0, ti, acc_im);
   } else {  // rows (x, 12..13), x = 0..13: four tiles
-    const double wy0 = wy[12], wy1 = wy[13];
+    double t0r = 0.0, t1r = 0.0, t0i = 0.0, t1i = 0.0;
     const unsigned bc = base + (12 + (g & 1)) * kLine;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       double cr0, cr1, ci0, ci1;
       tile_mma<KC>(bc + min(4 * q + (g >> 1), XB - 1) * kX, a, cr0, cr1, ci0, ci1);
       const double w = wx[4 * q + tig];
-      acc_re = fma(w, fma(wy0, cr0, wy1 * cr1), acc_re);
-      acc_im = fma(w, fma(wy0, ci0, wy1 * ci1), acc_im);
+      t0r = fma(w, cr0, t0r);
+      t1r = fma(w, cr1, t1r);
+      t0i = fma(w, ci0, t0i);
+      t1i = fma(w, ci1, t1i);
     }
+    const double wy0 = wy[12], wy1 = wy[13];
+    acc_re = fma(wy0, t0r, fma(wy1, t1r, acc_re));
+    acc_im = fma(wy0, t0i, fma(wy1, t1i, acc_im));
   }
   acc_re += __shfl_xor_sync(0xffffffffu, acc_re, 1);
   acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 1);

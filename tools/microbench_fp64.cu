@@ -175,6 +175,46 @@ __global__ void dmma_lat(double* out, int iters) {
   if (r == 12345.678) out[0] = r;
 }
 
+
+// Do DMMA and DFMA share the FP64 datapath?  Warps with (warp % 2 == 0) run
+// DMMA chains, the others DFMA chains; MODE 0 = both, 1 = DMMA warps only, 2 = DFMA only
+template <int MODE>
+__global__ void mixed_fp64(double* out, int iters) {
+  const int warp = threadIdx.x >> 5;
+  const bool is_mma = (warp & 1) == 0;
+  double r = 0;
+  if (is_mma && MODE != 2) {
+    double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+    double c[4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { c[i][0] = i; c[i][1] = -i; }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) r += c[i][0] + c[i][1];
+  } else if (!is_mma && MODE != 1) {
+    double a[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-3 + i;
+    // 16 DMMA-equivalents of work per iteration = 16*256/32 = 128 FMA per lane
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = fma(a[i], 0.999999, 1e-9);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r += a[i];
+  }
+  if (r == 12345.678) out[0] = r;
+}
+
 template <typename K>
 float time_kernel(K kern, dim3 grid, dim3 block, size_t smem, int reps) {
   cudaEvent_t a, b;
@@ -251,5 +291,15 @@ int main() {
     printf("{\"test\": \"dmma_lat\", \"chains\": %d, \"warps_per_sm\": %d, \"cycles_per_iter\": %.2f, \"cycles_per_dmma_per_warp\": %.2f}\n", NCH, WARPS, per, per / NCH); \
   }
   RUN_LAT(1, 1) RUN_LAT(2, 1) RUN_LAT(4, 1) RUN_LAT(8, 1) RUN_LAT(1, 4) RUN_LAT(2, 4) RUN_LAT(4, 4) RUN_LAT(1, 16) RUN_LAT(2, 16)
+
+#define RUN_MIX(MODE)                                                                         \
+  {                                                                                           \
+    int iters = 4000; dim3 g(nsm), blk(512);                                                  \
+    float ms = time_kernel([&](dim3 g, dim3 b, size_t s) { mixed_fp64<MODE><<<g, b, s>>>(d, iters); }, g, blk, 0, 3); \
+    double fl_mma = (MODE != 2) ? 2.0 * 256 * 16 * (double)iters * g.x * 8 : 0;               \
+    double fl_fma = (MODE != 1) ? 2.0 * 128 * 32 * (double)iters * g.x * 8 : 0;               \
+    printf("{\"test\": \"mixed_fp64\", \"mode\": %d, \"ms\": %.3f, \"tflops_total\": %.2f}\n", MODE, ms, (fl_mma + fl_fma) / ms / 1e9); \
+  }
+  RUN_MIX(0) RUN_MIX(1) RUN_MIX(2)
   return 0;
 }
