@@ -109,9 +109,16 @@ int vfn_direct_eval(int device, const int64_t nmodes[3], const double a[3], cons
                     const double* coeffs, const double* points, int64_t M, double* out,
                     int on_device, int64_t* first_bad_row, void* stream);
 
-/* Gather geometry vfn_plan_eval / vfn_plan_bin use for M points: the box
- * and staging-tile sizes in cells that define the bin key. */
+/* Gather geometry of the last vfn_plan_eval / vfn_plan_bin call (else the
+ * point-independent rule for M points): the box and staging-tile sizes in
+ * cells that define the bin key.                        */
 int vfn_plan_geometry(const vfn_plan* plan, int64_t M, int box_out[3], int tile_out[3]);
+
+/* Gather box width in cells (0 = automatic, 1 or 2).  Values are bitwise
+ * reproducible for a fixed box width; the automatic choice depends on the
+ * point set (its local density), so set it explicitly when bitwise
+ * equality across different batches or GPU counts matters.            */
+int vfn_plan_set_box(vfn_plan* plan, int bxy);
 
 /* Kernel selection for vfn_plan_eval (benchmarks / A-B tests):
  * 0 = automatic, 1 = simple thread-per-point gather, 2 = DMMA box gather. */

@@ -58,6 +58,7 @@ SIGNATURES = {
          ctypes.c_int, ctypes.POINTER(ctypes.c_int64), _vp],
     ),
     "vfn_plan_set_gather": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "vfn_plan_set_box": (ctypes.c_int, [_vp, ctypes.c_int]),
     "vfn_plan_geometry": (
         ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int * 3, ctypes.c_int * 3]
     ),

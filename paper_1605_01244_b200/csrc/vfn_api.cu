@@ -1,10 +1,13 @@
 // extern "C" entry points of libvfnfft (see include/vfnfft.h).
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
-#include "vfn_internal.cuh"
+#include <cub/device/device_radix_sort.cuh>
+
+#include "vfn_device.cuh"
 
 namespace vfn {
 const char* last_error_cstr();
@@ -60,14 +63,16 @@ int key_bits_for(int64_t nkeys) {
 
 namespace vfn {
 
-// Gather geometry: box/tile sizes by point density (K4).
-BinGeom choose_geometry(const vfn_plan* p, int64_t M) {
+// Gather geometry (K4): tiles of 4 x 4 x depth cells; boxes are
+// bxy x bxy columns of a tile.  1 x 1 columns waste the fewest rows but need
+// dense columns to fill 8-point units; 2 x 2 boxes fill better at low local
+// density.  bxy: the plan's setting (vfn_plan_set_box), else — for large
+// evaluates — from the local density measured on a sample of the points,
+// else from the global density.
+BinGeom make_geometry(const vfn_plan* p, int bxy) {
   BinGeom g;
-  const double cells = (double)p->n[0] * (double)p->n[1] * (double)p->n[2];
-  const double density = M / cells;
   const int K = ((2 * p->m + 1) + 3) / 4 * 4;  // DMMA k-extent
   const int bk = K - 2 * p->m;                  // box depth in cells (2 or 4)
-  const int bxy = density >= 1.0 ? 1 : 2;
   const bool m6 = p->m == 6 && p->has_tmap;     // vfn_gather_m6.cu: 4x4x8 tiles, depth-8 boxes
   g.box[0] = bxy;
   g.box[1] = bxy;
@@ -84,6 +89,69 @@ BinGeom choose_geometry(const vfn_plan* p, int64_t M) {
   g.ntiles = (int64_t)g.ntile[0] * g.ntile[1] * g.ntile[2];
   g.nboxes = g.ntiles * g.boxes_per_tile;
   return g;
+}
+
+__global__ void k_sample_columns(const double* __restrict__ pts, int64_t M, int S, TorusMap tm,
+                                 uint32_t* __restrict__ cols) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= S) return;
+  const int64_t i = (int64_t)j * (M / S);
+  int c[3];
+  for (int d = 0; d < 3; ++d) {
+    double delta;
+    c[d] = nearest_cell(pts[3 * i + d], tm.a[d], tm.amb[d], tm.nd[d], tm.n[d], delta);
+  }
+  cols[j] = (uint32_t)(((int64_t)c[0] * tm.n[1] + c[1]) * ((tm.n[2] + 7) / 8) + c[2] / 8);
+}
+
+// Expected number of OTHER points in a random point's 1 x 1 x 8 column,
+// estimated from the colliding pairs of a strided sample of S points.
+static int local_density(vfn_plan* p, const double* pts, int64_t M, cudaStream_t s, double* rho) {
+  const int S = 16384;
+  DevBuf buf;
+  VFN_CHECK(buf.ensure(sizeof(uint32_t) * 2 * S));
+  uint32_t* a = buf.as<uint32_t>();
+  uint32_t* b = a + S;
+  k_sample_columns<<<(S + 255) / 256, 256, 0, s>>>(pts, M, S, p->map, a);
+  VFN_CUDA(cudaGetLastError());
+  size_t tmp = 0;
+  VFN_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, a, b, S, 0, 32, s));
+  VFN_CHECK(p->sort_tmp.ensure(tmp));
+  VFN_CUDA(cub::DeviceRadixSort::SortKeys(p->sort_tmp.ptr, tmp, a, b, S, 0, 32, s));
+  std::vector<uint32_t> h(S);
+  VFN_CUDA(cudaMemcpyAsync(h.data(), b, sizeof(uint32_t) * S, cudaMemcpyDeviceToHost, s));
+  VFN_CUDA(cudaStreamSynchronize(s));
+  double pairs = 0;
+  for (int i = 0, j; i < S; i = j) {
+    for (j = i + 1; j < S && h[j] == h[i]; ++j) {
+    }
+    const double L = j - i;
+    pairs += L * (L - 1) / 2;
+  }
+  *rho = 2.0 * pairs * (double)(M - 1) / ((double)S * (S - 1));
+  buf.release();
+  return VFN_OK;
+}
+
+int choose_geometry(vfn_plan* p, int64_t M, const double* pts_dev, cudaStream_t s, BinGeom* g) {
+  int bxy = p->box_mode;
+  if (bxy == 0) {
+    const char* fb = std::getenv("VFN_BOX_XY");  // experiment override
+    if (fb) bxy = std::atoi(fb) == 1 ? 1 : 2;
+  }
+  if (bxy == 0) {
+    const double cells = (double)p->n[0] * (double)p->n[1] * (double)p->n[2];
+    bxy = M >= cells ? 1 : 2;
+    if (pts_dev && p->m == 6 && p->has_tmap && M >= (int64_t)1 << 20) {
+      double rho = 0.0;
+      VFN_CHECK(local_density(p, pts_dev, M, s, &rho));
+      bxy = rho >= 32.0 ? 1 : 2;
+    }
+  }
+  *g = make_geometry(p, bxy);
+  p->last_geom = *g;
+  p->has_last_geom = true;
+  return VFN_OK;
 }
 
 }  // namespace vfn
@@ -190,11 +258,20 @@ int vfn_plan_info(const vfn_plan* p, int64_t n_out[3], double* beta_out) {
 
 int vfn_plan_geometry(const vfn_plan* p, int64_t M, int box_out[3], int tile_out[3]) {
   if (!p || !box_out || !tile_out) return fail(VFN_ERR_INVALID, "null argument");
-  BinGeom g = choose_geometry(p, M);
+  // the geometry of the last evaluate/bin call, else the point-free rule for M
+  const double cells = (double)p->n[0] * (double)p->n[1] * (double)p->n[2];
+  BinGeom g = p->has_last_geom ? p->last_geom
+                               : make_geometry(p, p->box_mode ? p->box_mode : (M >= cells ? 1 : 2));
   for (int d = 0; d < 3; ++d) {
     box_out[d] = g.box[d];
     tile_out[d] = g.tile[d];
   }
+  return VFN_OK;
+}
+
+int vfn_plan_set_box(vfn_plan* p, int bxy) {
+  if (!p || bxy < 0 || bxy > 2) return fail(VFN_ERR_INVALID, "box must be 0 (auto), 1 or 2");
+  p->box_mode = bxy;
   return VFN_OK;
 }
 
@@ -261,11 +338,14 @@ int vfn_map_to_torus(int device, const double a[3], const double b[3], const dou
 
 // Shared front half of evaluate / bin: stage points, map+validate+key, sort.
 static int bin_points(vfn_plan* p, const double* points, int64_t M, int on_device,
-                      const BinGeom& g, const double** pts_dev, int64_t** bad_dev,
-                      cudaStream_t s, bool want_u = false) {
+                      BinGeom* gout, const double** pts_dev, int64_t** bad_dev,
+                      cudaStream_t s) {
   const void* pdev = nullptr;
   VFN_CHECK(stage_in(p->pts, points, sizeof(double) * 3 * M, on_device, &pdev, s));
   *pts_dev = static_cast<const double*>(pdev);
+  VFN_CHECK(choose_geometry(p, M, *pts_dev, s, gout));
+  const BinGeom& g = *gout;
+  const bool want_u = p->gather_variant != 1 && m6_applicable(p, g);
   VFN_CHECK(p->misc.ensure(64));
   *bad_dev = p->misc.as<int64_t>();
   const int64_t sentinel = INT64_MAX;
@@ -293,10 +373,10 @@ int vfn_plan_bin(vfn_plan* p, const double* points, int64_t M, uint32_t* keys, i
   if (M == 0) return VFN_OK;
   DeviceGuard guard(p->device);
   cudaStream_t s = as_stream(stream);
-  BinGeom g = choose_geometry(p, M);
+  BinGeom g;
   const double* pts_dev;
   int64_t* bad_dev;
-  VFN_CHECK(bin_points(p, points, M, on_device, g, &pts_dev, &bad_dev, s));
+  VFN_CHECK(bin_points(p, points, M, on_device, &g, &pts_dev, &bad_dev, s));
   cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   VFN_CUDA(cudaMemcpyAsync(keys, p->keys.ptr, sizeof(uint32_t) * M, k, s));
   VFN_CUDA(cudaMemcpyAsync(perm, p->perm.ptr, sizeof(int32_t) * M, k, s));
@@ -319,11 +399,10 @@ int vfn_plan_eval(vfn_plan* p, const double* points, int64_t M, double* out, int
   DeviceGuard guard(p->device);
   cudaStream_t s = as_stream(stream);
   VFN_CUDA(cudaEventRecord(p->ev[0], s));
-  BinGeom g = choose_geometry(p, M);
+  BinGeom g;
   const double* pts_dev;
   int64_t* bad_dev;
-  VFN_CHECK(bin_points(p, points, M, on_device, g, &pts_dev, &bad_dev, s,
-                       p->gather_variant != 1 && m6_applicable(p, g)));
+  VFN_CHECK(bin_points(p, points, M, on_device, &g, &pts_dev, &bad_dev, s));
   double2* out_dev = reinterpret_cast<double2*>(out);
   if (!on_device) {
     VFN_CHECK(p->out.ensure(sizeof(double2) * M));

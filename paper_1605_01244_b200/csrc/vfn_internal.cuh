@@ -120,12 +120,15 @@ struct vfn_plan {
   int pad_tile[3] = {8, 8, 8};  // grid padded to multiples of this
   double2* grid = nullptr;
   int gather_variant = 0;
+  int box_mode = 0;          // 0 auto, 1 or 2: gather box width in cells (vfn_plan_set_box)
   CUtensorMap tmap;        // TMA view of `grid` for the m = 6 gather
   bool has_tmap = false;
   // evaluate scratch (grow-only)
   vfn::DevBuf pts, out, uvals, keys, keys_sorted, idx, perm, sort_tmp, box_start, items, units, uscratch, misc;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   float last_gather_ms = 0.f, last_total_ms = 0.f;
+  vfn::BinGeom last_geom;
+  bool has_last_geom = false;
 };
 
 namespace vfn {
@@ -154,7 +157,8 @@ int rect_eval(int device, const int64_t nmodes[3], const double a[3], const doub
               const double* coeffs, const double* y[3], const int64_t Mv[3], double* out,
               int on_device, cudaStream_t s);
 
-BinGeom choose_geometry(const vfn_plan* p, int64_t M);
+BinGeom make_geometry(const vfn_plan* p, int bxy);
+int choose_geometry(vfn_plan* p, int64_t M, const double* pts_dev, cudaStream_t s, BinGeom* g);
 int make_grid_tmap(vfn_plan* p);
 bool m6_applicable(const vfn_plan* p, const BinGeom& g);
 int launch_m6(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t* keys_sorted,

@@ -295,6 +295,11 @@ class NufftPlan:
         """0 = automatic, 1 = thread-per-point gather, 2 = DMMA box gather."""
         _lib.check(_lib.load().vfn_plan_set_gather(self._handle, int(variant)))
 
+    def set_box(self, bxy: int) -> None:
+        """Gather box width: 0 = automatic (by the points' local density), 1 or 2.
+        Fix it when results must be bitwise identical across batches/GPU counts."""
+        _lib.check(_lib.load().vfn_plan_set_box(self._handle, int(bxy)))
+
     def last_timing(self) -> tuple[float, float]:
         """(gather_ms, device_total_ms) of the last evaluate, CUDA-event timed."""
         g, t = ctypes.c_float(), ctypes.c_float()
@@ -333,7 +338,8 @@ class NufftPlan:
         return out
 
     def geometry(self, M: int) -> tuple[tuple, tuple]:
-        """(box, tile) cell sizes of the bin key used for M points."""
+        """(box, tile) cell sizes of the bin key of the last evaluate/bin call
+        (else the point-independent choice for M points)."""
         box = (ctypes.c_int * 3)()
         tile = (ctypes.c_int * 3)()
         _lib.check(_lib.load().vfn_plan_geometry(self._handle, int(M), box, tile))
