@@ -145,9 +145,10 @@ __device__ __forceinline__ UnitPoints load_unit_points(const Args& A, int4 desc,
   up.prow = 0;
   up.uu[0] = up.uu[1] = up.uu[2] = 0.0;
   if (g < (desc.y & 15)) {
-    up.prow = __ldg(A.perm + desc.x + g);
+    // streamed once: evict-first, so the grid's tiles keep the L2
+    up.prow = __ldcs(A.perm + desc.x + g);
 #pragma unroll
-    for (int d = 0; d < 3; ++d) up.uu[d] = __ldg(A.u + 3 * up.prow + d);
+    for (int d = 0; d < 3; ++d) up.uu[d] = __ldcs(A.u + 3 * up.prow + d);
   }
   return up;
 }
@@ -288,7 +289,7 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double (&cb)[4]
   acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 1);
   acc_re += __shfl_xor_sync(0xffffffffu, acc_re, 2);
   acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 2);
-  if (valid && tig == 0) A.out[prow] = make_double2(acc_re, acc_im);
+  if (valid && tig == 0) __stcs(A.out + prow, make_double2(acc_re, acc_im));
   __syncwarp();  // the weight tables are rewritten by the next unit
 }
 
