@@ -371,7 +371,7 @@ def run_ours(args):
             "peak": peak,
             "unit": "TFLOP/s",
             "frac": achieved / peak if peak else None,
-            "traffic": None,
+            "traffic": profiled_traffic(name),
             "algorithmic": f"{int(fl)} flop/point = 2*((2m+1)^3+(2m+1)^2+(2m+1)) real FMA at m={CUTOFF}; "
             f"{M} points per launch",
             "peak_source": "measured DFMA peak on this device (vfn_bench_fp64_peak, 0.5 s); "
@@ -383,6 +383,12 @@ def run_ours(args):
         "gpu_launches": None,
         "clocks": clk,
     }
+    tr = result["roofline"]["traffic"]
+    if tr is not None:
+        ng = 1
+        for v in plan._n:
+            ng *= v
+        tr["algorithmic_bytes_per_launch"] = 40 * M + 16 * ng
     result["gpu_launches"] = launches_per_step(plan, M) * args.steps
     if cpu is not None:
         sp = cpu["sample_points"]
@@ -401,6 +407,18 @@ def run_ours(args):
         }
         result["parity_vs_cpu"] = {"points": int(len(ref)), "rel_l2": err_l2, "rel_linf": err_inf}
     print(json.dumps(result), flush=True)
+
+
+def profiled_traffic(name: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the gather kernel from the
+    committed ncu --set full capture for this workload (profiles/), or None."""
+    path = os.path.join(REPO, "profiles", "r01", "traffic.json")
+    try:
+        t = json.load(open(path))[name]
+    except (OSError, KeyError, ValueError):
+        return None
+    return {"bytes_per_launch": t["dram_bytes_read"] + t["dram_bytes_write"], "source": t["source"],
+            "algorithmic_bytes_per_launch": None}
 
 
 def launches_per_step(plan, M: int) -> int:
