@@ -371,7 +371,7 @@ def run_ours(args):
             "peak": peak,
             "unit": "TFLOP/s",
             "frac": achieved / peak if peak else None,
-            "traffic": profiled_traffic(name),
+            "traffic": None,
             "algorithmic": f"{int(fl)} flop/point = 2*((2m+1)^3+(2m+1)^2+(2m+1)) real FMA at m={CUTOFF}; "
             f"{M} points per launch",
             "peak_source": "measured DFMA peak on this device (vfn_bench_fp64_peak, 0.5 s); "
@@ -383,12 +383,14 @@ def run_ours(args):
         "gpu_launches": None,
         "clocks": clk,
     }
-    tr = result["roofline"]["traffic"]
-    if tr is not None:
-        ng = 1
-        for v in plan._n:
-            ng *= v
-        tr["algorithmic_bytes_per_launch"] = 40 * M + 16 * ng
+    tr = profiled_traffic(name)
+    ng = 1
+    for v in plan._n:
+        ng *= v
+    result["roofline"]["algorithmic_bytes"] = 40 * M + 16 * ng  # points in/out + grid once
+    if tr is not None and world == 1:
+        result["roofline"]["traffic"] = tr[0]
+        result["roofline"]["traffic_source"] = tr[1]
     result["gpu_launches"] = launches_per_step(plan, M) * args.steps
     if cpu is not None:
         sp = cpu["sample_points"]
@@ -417,8 +419,7 @@ def profiled_traffic(name: str):
         t = json.load(open(path))[name]
     except (OSError, KeyError, ValueError):
         return None
-    return {"bytes_per_launch": t["dram_bytes_read"] + t["dram_bytes_write"], "source": t["source"],
-            "algorithmic_bytes_per_launch": None}
+    return t["dram_bytes_read"] + t["dram_bytes_write"], t["source"]
 
 
 def launches_per_step(plan, M: int) -> int:
