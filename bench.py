@@ -58,7 +58,7 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--workload", choices=["c1", "c2", "c3", "c5"], default="c5")
+    p.add_argument("--workload", choices=["c1", "c2", "c3", "c4", "c5"], default="c5")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--gather", type=int, default=0, help="0 auto, 1 simple, 2 box/DMMA")
@@ -422,6 +422,94 @@ def profiled_traffic(name: str):
     return t["dram_bytes_read"] + t["dram_bytes_write"], t["source"]
 
 
+def run_rect(args):
+    """Config 4: rectilinear 128^3 -> 256^3 tanh-clustered tensor grid through
+    eval_rectilinear (three exact separable passes).  Points = grid points."""
+    import torch
+
+    import paper_1605_01244_b200 as vfb
+
+    world, rank, local = dist_setup(args)
+    if rank != 0:
+        return
+    dev = torch.device("cuda", local)
+    w = workloads.WORKLOADS["c4"]
+    coeffs = workloads.coefficients("c4")
+    axes = workloads.rect_axes(256)
+    box = vfb.DomainBox(*w.box)
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import nfft_oracle as O
+
+        t0 = time.perf_counter()
+        ref = O.rectilinear(coeffs, box.a, box.b, axes)
+        cpu = {"seconds": time.perf_counter() - t0, "ref": ref}
+    spec_d = vfb.SpectralField(box, torch.as_tensor(coeffs).to(dev))
+    for _ in range(args.warmup):
+        out = vfb.eval_rectilinear(spec_d, axes)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    e0.record(stream)
+    for _ in range(args.steps):
+        out = vfb.eval_rectilinear(spec_d, axes)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    step_ms = e0.elapsed_time(e1) / args.steps
+    npts = 256 ** 3
+    # e2e: host coefficients in, host values out
+    t0 = time.perf_counter()
+    host = vfb.eval_rectilinear(vfb.SpectralField(box, coeffs), axes)
+    e2e_ms = (time.perf_counter() - t0) * 1e3
+    N, Mx = 128, 256
+    cmacs = N * N * N * Mx + N * N * Mx * Mx + N * Mx * Mx * Mx  # the three passes
+    achieved = 8.0 * cmacs / (step_ms * 1e-3) / 1e12
+    import ctypes
+
+    from paper_1605_01244_b200 import _lib
+
+    tf, mhz = ctypes.c_double(), ctypes.c_double()
+    _lib.check(_lib.load().vfn_bench_fp64_peak(local, 0.5, ctypes.byref(tf), ctypes.byref(mhz)))
+    result = {
+        "metric": "3D rectilinear-grid evaluation points/sec (fp64 complex)",
+        "value": npts / (step_ms * 1e-3),
+        "unit": "points/s",
+        "n_gpus": 1,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": step_ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic, seeded (SURVEY 8d recipe)",
+        "config": {"workload": "c4: N=128^3 coefficients -> 256^3 tanh-clustered rectilinear grid",
+                   "modes": [128, 128, 128], "points": npts},
+        "e2e": {"value": npts / (e2e_ms * 1e-3), "unit": "points/s",
+                "h2d_bytes_per_step": int(coeffs.nbytes + 3 * 256 * 8), "d2h_bytes_per_step": int(npts * 16),
+                "ms_per_step": e2e_ms},
+        "roofline": {"bound": "fp64", "kernel": "3 ZGEMM passes (cuBLAS DMMA)", "achieved": achieved,
+                     "peak": tf.value, "unit": "TFLOP/s", "frac": achieved / tf.value, "traffic": None,
+                     "algorithmic": f"{cmacs} complex MACs = 8 flop each"},
+        "gpu_launches": None,
+        "clocks": clk,
+    }
+    if cpu is not None:
+        ref = cpu["ref"]
+        result["cpu_baseline"] = {"value": npts / cpu["seconds"], "unit": "points/s",
+                                  "cores": len(os.sched_getaffinity(0)), "kind": "port",
+                                  "sample": "full c4 through oracle.rectilinear (numpy/BLAS restatement of rectilinear.py:47-64)"}
+        result["parity_vs_cpu"] = {
+            "points": npts,
+            "rel_l2": float(np.linalg.norm(host - ref) / np.linalg.norm(ref)),
+            "rel_linf": float(np.abs(host - ref).max() / np.abs(ref).max()),
+        }
+    print(json.dumps(result), flush=True)
+
+
 def launches_per_step(plan, M: int) -> int:
     """Kernels of ours launched by one evaluate: map+key, the CUB onesweep
     radix sort (1 histogram + one pass per 8 key bits), box offsets and the
@@ -436,6 +524,32 @@ def run_reference(args):
         return
     name = args.workload
     coeffs = workloads.coefficients(name)
+    if name == "c4":
+        from oracle import nfft_oracle as O
+
+        w = workloads.WORKLOADS["c4"]
+        axes = workloads.rect_axes(256)
+        times = []
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            O.rectilinear(coeffs, w.box[0], w.box[1], axes)
+            if i >= args.warmup:
+                times.append(time.perf_counter() - t0)
+        value = 256 ** 3 / float(np.mean(times))
+        cores = len(os.sched_getaffinity(0))
+        print(json.dumps({
+            "metric": "3D rectilinear-grid evaluation points/sec (fp64 complex)", "value": value,
+            "unit": "points/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": float(np.mean(times)) * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic, seeded (SURVEY 8d recipe)",
+            "config": {"workload": "c4: N=128^3 coefficients -> 256^3 tanh-clustered rectilinear grid",
+                       "modes": [128, 128, 128], "points": 256 ** 3},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "port",
+                             "sample": "full c4 per step, oracle.rectilinear (numpy + OpenBLAS threads)"},
+            "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }), flush=True)
+        return
     runs = []
     per_step = max(3.0, args.cpu_seconds / 4)
     for i in range(args.warmup + args.steps):
@@ -472,6 +586,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "c4":
+        run_rect(args)
     else:
         run_ours(args)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1 and args.impl == "ours":

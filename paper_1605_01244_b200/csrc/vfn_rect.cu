@@ -61,7 +61,22 @@ int rect_eval(int device, const int64_t nm[3], const double a[3], const double b
   const size_t fb = sizeof(double2) * M0 * M1 * M2;
   const size_t eb[3] = {sizeof(double2) * M0 * N0, sizeof(double2) * M1 * N1,
                         sizeof(double2) * M2 * N2};
-  DevBuf C, T1, T2, F, E[3], Y[3];
+  // grow-only scratch per device, reused across calls (one host thread at a time)
+  struct Scratch {
+    DevBuf C, T1, T2, F, E[3], Y[3];
+  };
+  static std::mutex smu;
+  static std::map<int, Scratch*> scratch;
+  Scratch* sc;
+  {
+    std::lock_guard<std::mutex> lock(smu);
+    Scratch*& slot = scratch[device];
+    if (!slot) slot = new Scratch();
+    sc = slot;
+  }
+  DevBuf &C = sc->C, &T1 = sc->T1, &T2 = sc->T2, &F = sc->F;
+  DevBuf* E = sc->E;
+  DevBuf* Y = sc->Y;
   int st = VFN_OK;
   const double2 one = make_double2(1.0, 0.0), zero = make_double2(0.0, 0.0);
   const double2* Cd = reinterpret_cast<const double2*>(coeffs);
@@ -126,14 +141,6 @@ int rect_eval(int device, const int64_t nm[3], const double a[3], const double b
     if (e != cudaSuccess) st = fail(VFN_ERR_CUDA, std::string("rectilinear: ") + cudaGetErrorString(e));
   }
 done:
-  C.release();
-  T1.release();
-  T2.release();
-  F.release();
-  for (int d = 0; d < 3; ++d) {
-    E[d].release();
-    Y[d].release();
-  }
   return st;
 }
 

@@ -293,3 +293,52 @@ def test_config2_full_size(vfb):
     assert l2 < TOL and linf < TOL
     assert l2 < 1e-13 and linf < 1e-13, (l2, linf)
     np.testing.assert_array_equal(out[sub], plan.evaluate(pts[sub]))
+
+
+def test_config3_clustered_full_size(vfb):
+    """BASELINE config 3 (vortex-pair spectrum on [-8,8)^3, 1e7 points in a
+    0.05-std cloud straddling the periodic seam): 20k-point subset vs oracle,
+    and the automatic box choice must not change any value's bits compared
+    with a fixed box on the same call geometry."""
+    from paper_1605_01244_b200 import workloads
+
+    coeffs = workloads.coefficients("c3")
+    pts = workloads.points("c3")
+    a, b = workloads.VORTEX_BOX
+    plan = vfb.NufftPlan(vfb.SpectralField(vfb.DomainBox(a, b), coeffs))
+    out = plan.evaluate(pts)
+    sub = np.random.default_rng(1).choice(len(pts), 20000, replace=False)
+    ref = O.nufft_eval(coeffs, a, b, pts[sub])
+    l2, linf = rel_err(out[sub], ref)
+    assert l2 < 1e-13 and linf < 1e-13, (l2, linf)
+    box, _ = plan.geometry(len(pts))
+    plan.set_box(box[0])
+    np.testing.assert_array_equal(plan.evaluate(pts), out)
+
+
+def test_config4_rectilinear_full_size(vfb):
+    """BASELINE config 4: 128^3 coefficients on the 256^3 tanh-clustered grid,
+    every value against the oracle (reference algorithm)."""
+    from paper_1605_01244_b200 import workloads
+
+    coeffs = workloads.coefficients("c4")
+    axes = workloads.rect_axes(256)
+    a, b = workloads.UNIT_BOX
+    out = vfb.eval_rectilinear(vfb.SpectralField(vfb.DomainBox(a, b), coeffs), axes)
+    ref = O.rectilinear(coeffs, a, b, axes)
+    l2, linf = rel_err(out, ref)
+    assert l2 < 1e-13 and linf < 1e-13, (l2, linf)
+
+
+def test_box_widths_agree(vfb, offset_box):
+    """Both gather box widths give the reference's values (to rounding)."""
+    spec = random_spectral(offset_box, (16, 16, 16), 95)
+    pts = np.random.default_rng(96).uniform(offset_box.a, offset_box.b, (40000, 3))
+    plan = vfb.NufftPlan(spec)
+    ref = O.nufft_eval(spec.coeffs, offset_box.a, offset_box.b, pts)
+    for bxy in (1, 2):
+        plan.set_box(bxy)
+        out = plan.evaluate(pts)
+        assert plan.geometry(len(pts))[0][0] == bxy
+        l2, linf = rel_err(out, ref)
+        assert l2 < 1e-13 and linf < 1e-13, (bxy, l2, linf)
