@@ -302,7 +302,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   const unsigned bar_s = tiles_s + 2 * kTileBytes;          // full[2]
   unsigned char* ctl = smem_raw + (bar_s - raw);
   int* done = reinterpret_cast<int*>(ctl + 16);              // done[2]
-  int* ctr = done + 2;                                       // ctr[4]: next unit of item k, slot k & 3
+  int* ctr = done + 2;                                       // next CTA unit to hand out
+  int* loaded = done + 4;                                    // loaded[2]: item ordinal per buffer
   double* wts = reinterpret_cast<double*>(ctl + 48);         // [kWarps][kWarpW]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -320,7 +321,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     mbar_init(bar_s, 1);
     mbar_init(bar_s + 8, 1);
     done[0] = done[1] = 0;
-    ctr[0] = ctr[1] = ctr[2] = ctr[3] = 0;
+    ctr[0] = 0;
+    loaded[0] = 0;
+    loaded[1] = 1;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     issue_tile(&tmap, A, blockIdx.x, tiles_s, bar_s);
     issue_tile(&tmap, A, blockIdx.x + gridDim.x, tiles_s + kTileBytes, bar_s + 8);
@@ -330,85 +333,84 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   double* wt = wts + warp * kWarpW;
   const int nitems = *A.nitems;
   const BinGeom& G = A.g;
-  // Units are handed out dynamically from per-item smem counters (4 slots,
-  // item k uses slot k & 3; the last warp out of item k resets it).  Each warp
-  // reserves its next unit — from the current item or, when that is
-  // exhausted, from the next one — and prefetches its points before computing
-  // the current unit.
-  auto grab = [&](int slot) {
+  // Units are handed out from one monotonic CTA counter over the
+  // concatenated units of this CTA's items (item k = items[blockIdx.x +
+  // k * gridDim.x]); each warp walks the item list forward to locate the unit
+  // it grabbed, reserves its next unit and prefetches its points before
+  // computing the current one.  A tile buffer is refilled (item k+2) by the
+  // warp that completes the last unit of item k.
+  struct Cur {
+    int k;      // item ordinal within this CTA (-1: none)
+    int4 item;  // (tile, unit_begin, unit_end)
+    int base;   // CTA unit index of the item's first unit
+  };
+  Cur walk;
+  walk.k = 0;
+  walk.item = blockIdx.x < nitems ? A.items[blockIdx.x] : make_int4(0, 0, 0, 0);
+  walk.base = 0;
+  // locate CTA unit u by walking forward (u is monotonic per warp)
+  auto locate = [&](int u, int4& desc, int& kk, int4& it4) -> bool {
+    while (true) {
+      const int it = blockIdx.x + walk.k * gridDim.x;
+      if (it >= nitems) return false;
+      const int n = walk.item.z - walk.item.y;
+      if (u < walk.base + n) {
+        kk = walk.k;
+        it4 = walk.item;
+        desc = __ldg(A.units + walk.item.y + (u - walk.base));
+        return true;
+      }
+      walk.base += n;
+      ++walk.k;
+      const int itn = blockIdx.x + walk.k * gridDim.x;
+      walk.item = itn < nitems ? A.items[itn] : make_int4(0, 0, 0, 0);
+    }
+  };
+  auto grab = [&]() {
     int v = 0;
-    if (lane == 0) v = atomicAdd(&ctr[slot], 1);
+    if (lane == 0) v = atomicAdd(ctr, 1);
     return __shfl_sync(0xffffffffu, v, 0);
   };
-  int k = 0;
-  int it = blockIdx.x;
-  int4 item = it < nitems ? A.items[it] : make_int4(0, 0, 0, 0);
-  int ui = it < nitems ? grab(0) : INT_MAX;
-  int4 desc = make_int4(0, 0, 0, 0);
+  int4 desc, item;
+  int kk = 0;
   UnitPoints up;
-  if (ui < item.z - item.y) {
-    desc = __ldg(A.units + item.y + ui);
-    up = load_unit_points(A, desc, g);
-  }
-  while (it < nitems) {
-    const int b = k & 1;
+  bool have = locate(grab(), desc, kk, item);
+  if (have) up = load_unit_points(A, desc, g);
+  while (have) {
+    int4 desc_n, item_n;
+    int kk_n = 0;
+    UnitPoints up_n;
+    const bool have_n = locate(grab(), desc_n, kk_n, item_n);
+    if (have_n) up_n = load_unit_points(A, desc_n, g);
+    const int b = kk & 1;
     const int tile = item.x;
     const int t2 = tile % G.ntile[2];
     const int t1 = (tile / G.ntile[2]) % G.ntile[1];
     const int t0 = tile / (G.ntile[2] * G.ntile[1]);
     const unsigned tile_s = tiles_s + b * kTileBytes;
-    const int nunits = item.z - item.y;
-    const int it_n = it + gridDim.x;
-    const int4 item_n = it_n < nitems ? A.items[it_n] : make_int4(0, 0, 0, 0);
-    const int nunits_n = item_n.z - item_n.y;
-    mbar_wait(bar_s + 8 * b, (k >> 1) & 1);
-    bool carried = false;
-    while (ui < nunits) {
-      int nx = grab(k & 3);
-      const bool same = nx < nunits;
-      int4 desc_n = make_int4(0, 0, 0, 0);
-      UnitPoints up_n;
-      if (same) {
-        desc_n = __ldg(A.units + item.y + nx);
-        up_n = load_unit_points(A, desc_n, g);
-      } else {
-        nx = it_n < nitems ? grab((k + 1) & 3) : INT_MAX;
-        if (nx < nunits_n) {
-          desc_n = __ldg(A.units + item_n.y + nx);
-          up_n = load_unit_points(A, desc_n, g);
+    // a warp may hold units of items far ahead (small items): the buffer's
+    // mbarrier parity only distinguishes consecutive loads, so first wait
+    // until the buffer's load for item kk has been issued
+    while (*reinterpret_cast<volatile int*>(&loaded[b]) != kk) __nanosleep(64);
+    mbar_wait(bar_s + 8 * b, (kk >> 1) & 1);
+    if ((desc.y >> 4) & 1)
+      gather_unit<BXY, 5>(A, cb, wt, tile_s, tile, t0 * 4, t1 * 4, t2 * kTZ, desc, up, lane);
+    else
+      gather_unit<BXY, 4>(A, cb, wt, tile_s, tile, t0 * 4, t1 * 4, t2 * kTZ, desc, up, lane);
+    if (lane == 0) {
+      if (atomicAdd(&done[b], 1) == item.z - item.y - 1) {  // last unit of item kk
+        done[b] = 0;
+        if (blockIdx.x + (kk + 2) * gridDim.x < nitems) {
+          *reinterpret_cast<volatile int*>(&loaded[b]) = kk + 2;
+          issue_tile(&tmap, A, blockIdx.x + (kk + 2) * gridDim.x, tile_s, bar_s + 8 * b);
         }
       }
-      if ((desc.y >> 4) & 1)
-        gather_unit<BXY, 5>(A, cb, wt, tile_s, tile, t0 * 4, t1 * 4, t2 * kTZ, desc, up, lane);
-      else
-        gather_unit<BXY, 4>(A, cb, wt, tile_s, tile, t0 * 4, t1 * 4, t2 * kTZ, desc, up, lane);
-      ui = nx;
-      desc = desc_n;
-      up = up_n;
-      if (!same) {
-        carried = true;
-        break;
-      }
     }
-    if (!carried) {  // no unit of this item left for this warp: reserve from the next
-      ui = it_n < nitems ? grab((k + 1) & 3) : INT_MAX;
-      if (ui < nunits_n) {
-        desc = __ldg(A.units + item_n.y + ui);
-        up = load_unit_points(A, desc, g);
-      }
-    }
-    __syncwarp();
-    if (lane == 0) {
-      if (atomicAdd(&done[b], 1) == kWarps - 1) {  // last warp out refills the buffer
-        done[b] = 0;
-        ctr[k & 3] = 0;
-        __threadfence_block();
-        issue_tile(&tmap, A, it + 2 * gridDim.x, tile_s, bar_s + 8 * b);
-      }
-    }
-    ++k;
-    it = it_n;
+    have = have_n;
+    desc = desc_n;
     item = item_n;
+    kk = kk_n;
+    up = up_n;
   }
 }
 
