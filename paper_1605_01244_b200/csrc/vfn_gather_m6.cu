@@ -317,6 +317,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       const int d = 4 * kc + tig, j = 8 * nb + g;
       cb[kc][nb] = (d <= A.deg && j < 13) ? A.poly[j * (A.deg + 1) + d] : 0.0;
     }
+  // this CTA's items: a contiguous block of the tile-ordered item list, so
+  // consecutive tiles of a column (12 of 20 staged planes shared) hit L2
+  const int nitems = *A.nitems;
+  const int per_cta = (nitems + gridDim.x - 1) / gridDim.x;
+  const int first_item = blockIdx.x * per_cta;
+  const int last_item = min(nitems, first_item + per_cta);
+  auto item_of = [&](int k) { return first_item + k < last_item ? first_item + k : INT_MAX; };
   if (tid == 0) {
     mbar_init(bar_s, 1);
     mbar_init(bar_s + 8, 1);
@@ -325,13 +332,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     loaded[0] = 0;
     loaded[1] = 1;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    issue_tile(&tmap, A, blockIdx.x, tiles_s, bar_s);
-    issue_tile(&tmap, A, blockIdx.x + gridDim.x, tiles_s + kTileBytes, bar_s + 8);
+    issue_tile(&tmap, A, item_of(0), tiles_s, bar_s);
+    issue_tile(&tmap, A, item_of(1), tiles_s + kTileBytes, bar_s + 8);
   }
   __syncthreads();
 
   double* wt = wts + warp * kWarpW;
-  const int nitems = *A.nitems;
   const BinGeom& G = A.g;
   // Units are handed out from one monotonic CTA counter over the
   // concatenated units of this CTA's items (item k = items[blockIdx.x +
@@ -346,12 +352,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   };
   Cur walk;
   walk.k = 0;
-  walk.item = blockIdx.x < nitems ? A.items[blockIdx.x] : make_int4(0, 0, 0, 0);
+  walk.item = item_of(0) < nitems ? A.items[item_of(0)] : make_int4(0, 0, 0, 0);
   walk.base = 0;
   // locate CTA unit u by walking forward (u is monotonic per warp)
   auto locate = [&](int u, int4& desc, int& kk, int4& it4) -> bool {
     while (true) {
-      const int it = blockIdx.x + walk.k * gridDim.x;
+      const int it = item_of(walk.k);
       if (it >= nitems) return false;
       const int n = walk.item.z - walk.item.y;
       if (u < walk.base + n) {
@@ -362,7 +368,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       }
       walk.base += n;
       ++walk.k;
-      const int itn = blockIdx.x + walk.k * gridDim.x;
+      const int itn = item_of(walk.k);
       walk.item = itn < nitems ? A.items[itn] : make_int4(0, 0, 0, 0);
     }
   };
@@ -400,9 +406,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     if (lane == 0) {
       if (atomicAdd(&done[b], 1) == item.z - item.y - 1) {  // last unit of item kk
         done[b] = 0;
-        if (blockIdx.x + (kk + 2) * gridDim.x < nitems) {
+        if (item_of(kk + 2) < nitems) {
           *reinterpret_cast<volatile int*>(&loaded[b]) = kk + 2;
-          issue_tile(&tmap, A, blockIdx.x + (kk + 2) * gridDim.x, tile_s, bar_s + 8 * b);
+          issue_tile(&tmap, A, item_of(kk + 2), tile_s, bar_s + 8 * b);
         }
       }
     }
