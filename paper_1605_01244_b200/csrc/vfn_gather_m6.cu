@@ -317,13 +317,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       const int d = 4 * kc + tig, j = 8 * nb + g;
       cb[kc][nb] = (d <= A.deg && j < 13) ? A.poly[j * (A.deg + 1) + d] : 0.0;
     }
-  // this CTA's items: a contiguous block of the tile-ordered item list, so
-  // consecutive tiles of a column (12 of 20 staged planes shared) hit L2
+  // this CTA's k-th item: strided over the tile-ordered item list, so the
+  // 148 CTAs work on neighbouring tiles at any moment and share the tiles'
+  // halos through L2 (contiguous blocks per CTA measured 38% more DRAM reads)
   const int nitems = *A.nitems;
-  const int per_cta = (nitems + gridDim.x - 1) / gridDim.x;
-  const int first_item = blockIdx.x * per_cta;
-  const int last_item = min(nitems, first_item + per_cta);
-  auto item_of = [&](int k) { return first_item + k < last_item ? first_item + k : INT_MAX; };
+  auto item_of = [&](int k) {
+    const long long it = (long long)blockIdx.x + (long long)k * gridDim.x;
+    return it < nitems ? (int)it : INT_MAX;
+  };
   if (tid == 0) {
     mbar_init(bar_s, 1);
     mbar_init(bar_s + 8, 1);
