@@ -217,29 +217,11 @@ def rectilinear(coeffs: np.ndarray, a, b, coords) -> np.ndarray:
 # N1 (new, no reference counterpart): the bin-sort key.
 # A point's nearest oversampled cell c_d = l0_d mod n_d (nufft.py:248-257) is
 # grouped into gather boxes of (bi, bj, bk) cells; boxes are numbered
-# row-major inside tiles of (ti, tj, tk) cells, tiles in Morton order over the
-# grid (row-major, the convention of tube.py:50-51, when Morton padding would
-# more than double the tile count), and cells depth-major inside a box.  The permutation is a stable
+# row-major inside tiles of (ti, tj, tk) cells, tiles row-major over the grid
+# (the row-major convention of tube.py:50-51), and cells depth-major inside a
+# box.  The permutation is a stable
 # sort on that key (precedent: the stable argsort of tube.py:125).
 # ---------------------------------------------------------------------------
-
-
-def tile_numbers(t: np.ndarray, ntile) -> np.ndarray:
-    """Tile number of tile coordinates t (rows of (t0, t1, t2)): Morton order
-    (bits interleaved, axis 2 fastest) when padding every axis to a power of
-    two at most doubles the tile count, row-major otherwise."""
-    ntile = np.asarray(ntile)
-    bits = [int(np.ceil(np.log2(v))) if v > 1 else 0 for v in ntile]
-    if 2 ** sum(bits) > 2 * int(np.prod(ntile)):
-        return (t[:, 0] * ntile[1] + t[:, 1]) * ntile[2] + t[:, 2]
-    out = np.zeros(t.shape[0], dtype=np.int64)
-    pos = 0
-    for bit in range(21):
-        for d in (2, 1, 0):
-            if bit < bits[d]:
-                out |= ((t[:, d].astype(np.int64) >> bit) & 1) << pos
-                pos += 1
-    return out
 
 
 def bin_keys(points, a, b, n, box=(1, 1, 4), tile=(4, 4, 4)) -> np.ndarray:
@@ -255,7 +237,7 @@ def bin_keys(points, a, b, n, box=(1, 1, 4), tile=(4, 4, 4)) -> np.ndarray:
     inner = rem // box
     c = rem % box
     nbox = tile // box
-    tile_id = tile_numbers(t, ntile)
+    tile_id = (t[:, 0] * ntile[1] + t[:, 1]) * ntile[2] + t[:, 2]
     box_id = (inner[:, 0] * nbox[1] + inner[:, 1]) * nbox[2] + inner[:, 2]
     cell_id = (c[:, 2] * box[0] + c[:, 0]) * box[1] + c[:, 1]
     key = (tile_id * int(np.prod(nbox)) + box_id) * int(np.prod(box)) + cell_id

@@ -87,18 +87,6 @@ BinGeom make_geometry(const vfn_plan* p, int bxy) {
   g.boxes_per_tile = g.nbox[0] * g.nbox[1] * g.nbox[2];
   g.cells_per_box = g.box[0] * g.box[1] * g.box[2];
   g.ntiles = (int64_t)g.ntile[0] * g.ntile[1] * g.ntile[2];
-  // Morton tile order when padding each axis to a power of two costs <= 2x
-  int64_t pow2 = 1;
-  for (int d = 0; d < 3; ++d) {
-    g.tbits[d] = 0;
-    while ((1 << g.tbits[d]) < g.ntile[d]) ++g.tbits[d];
-    pow2 <<= g.tbits[d];
-  }
-  if (pow2 <= 2 * g.ntiles) {
-    g.ntiles = pow2;  // tile numbers range over the padded Morton space
-  } else {
-    g.tbits[0] = g.tbits[1] = g.tbits[2] = 0;
-  }
   g.nboxes = g.ntiles * g.boxes_per_tile;
   return g;
 }

@@ -91,8 +91,9 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_gather_dmma(GatherArgs A) {
   for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
     const int4 item = A.items[it];
     const int64_t tile = item.x;
-    int t0, t1, t2;
-    tile_decode(G, tile, t0, t1, t2);
+    const int t2 = (int)(tile % G.ntile[2]);
+    const int t1 = (int)((tile / G.ntile[2]) % G.ntile[1]);
+    const int t0 = (int)(tile / ((int64_t)G.ntile[2] * G.ntile[1]));
     const int64_t ox = (int64_t)t0 * G.tile[0], oy = (int64_t)t1 * G.tile[1],
                   oz = (int64_t)t2 * G.tile[2];
     __syncthreads();  // previous item's readers are done with sG / sBox

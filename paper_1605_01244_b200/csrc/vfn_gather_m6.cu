@@ -110,8 +110,9 @@ __device__ __forceinline__ void issue_tile(const CUtensorMap* map, const Args& A
   if (it >= *A.nitems) return;
   const int tile = A.items[it].x;
   const BinGeom& G = A.g;
-  int t0, t1, t2;
-  tile_decode(G, tile, t0, t1, t2);
+  const int t2 = tile % G.ntile[2];
+  const int t1 = (tile / G.ntile[2]) % G.ntile[1];
+  const int t0 = tile / (G.ntile[2] * G.ntile[1]);
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // prior generic reads of dst
   mbar_expect_tx(bar, kTileBytes);
   tma_load_3d(dst, map, 2 * t2 * kTZ, t1 * 4, t0 * 4, bar);
@@ -390,8 +391,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     if (have_n) up_n = load_unit_points(A, desc_n, g);
     const int b = kk & 1;
     const int tile = item.x;
-    int t0, t1, t2;
-    tile_decode(G, tile, t0, t1, t2);
+    const int t2 = tile % G.ntile[2];
+    const int t1 = (tile / G.ntile[2]) % G.ntile[1];
+    const int t0 = tile / (G.ntile[2] * G.ntile[1]);
     const unsigned tile_s = tiles_s + b * kTileBytes;
     // a warp may hold units of items far ahead (small items): the buffer's
     // mbarrier parity only distinguishes consecutive loads, so first wait

@@ -88,45 +88,11 @@ struct BinGeom {
   int tile[3];    // staging-tile size in cells (multiple of box)
   int ntile[3];   // tiles per axis = ceil(n / tile)
   int nbox[3];    // boxes per tile per axis
-  int tbits[3];       // Morton tile order: bits per axis (all 0: row-major)
   int boxes_per_tile;
   int cells_per_box;  // key = (tile * boxes_per_tile + box) * cells_per_box + cell
   int64_t ntiles;
   int64_t nboxes;  // ntiles * boxes_per_tile
 };
-
-// Tile number of tile (t0, t1, t2): a Morton (bit-interleaved, axis 2
-// fastest) index when tbits is set, so consecutive tiles are compact 3D
-// blocks and neighbouring CTAs share halos in L2; row-major otherwise.
-__host__ __device__ __forceinline__ int64_t tile_encode(const BinGeom& g, int t0, int t1, int t2) {
-  if (g.tbits[0] + g.tbits[1] + g.tbits[2] == 0)
-    return ((int64_t)t0 * g.ntile[1] + t1) * g.ntile[2] + t2;
-  const int t[3] = {t0, t1, t2};
-  int64_t id = 0;
-  int pos = 0;
-  for (int b = 0; b < 21; ++b)
-    for (int d = 2; d >= 0; --d)
-      if (b < g.tbits[d]) id |= (int64_t)((t[d] >> b) & 1) << pos++;
-  return id;
-}
-
-__host__ __device__ __forceinline__ void tile_decode(const BinGeom& g, int64_t id, int& t0, int& t1,
-                                                     int& t2) {
-  if (g.tbits[0] + g.tbits[1] + g.tbits[2] == 0) {
-    t2 = (int)(id % g.ntile[2]);
-    t1 = (int)((id / g.ntile[2]) % g.ntile[1]);
-    t0 = (int)(id / ((int64_t)g.ntile[2] * g.ntile[1]));
-    return;
-  }
-  int t[3] = {0, 0, 0};
-  int pos = 0;
-  for (int b = 0; b < 21; ++b)
-    for (int d = 2; d >= 0; --d)
-      if (b < g.tbits[d]) t[d] |= (int)((id >> pos++) & 1) << b;
-  t0 = t[0];
-  t1 = t[1];
-  t2 = t[2];
-}
 
 // Window polynomial table: w_j(delta) = sum_d coef[j*(deg+1) + d] delta^d,
 // j = 0..2m (offset c = j - m), approximating phi(delta - c) (nufft.py:159-164).

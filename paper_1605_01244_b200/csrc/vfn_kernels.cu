@@ -46,7 +46,7 @@ __global__ void k_map_key(const double* __restrict__ pts, int64_t M, TorusMap tm
     in[d] = r / g.box[d];
     c[d] = r - in[d] * g.box[d];
   }
-  int64_t tile_id = tile_encode(g, t[0], t[1], t[2]);
+  int64_t tile_id = ((int64_t)t[0] * g.ntile[1] + t[1]) * g.ntile[2] + t[2];
   int box_id = (in[0] * g.nbox[1] + in[1]) * g.nbox[2] + in[2];
   int cell_id = (c[2] * g.box[0] + c[0]) * g.box[1] + c[1];
   keys[i] = (uint32_t)((tile_id * g.boxes_per_tile + box_id) * g.cells_per_box + cell_id);
