@@ -19,6 +19,9 @@
  *                        permutation
  *   vfn_plan_grid     <- NufftPlan._grid           nufft.py:242 (inspection)
  *   vfn_direct_eval   <- eval_direct               nufft.py:129-149 (exact NDFT)
+ *   vfn_decompose     <- snapshot_spectral         gpe.py:110-113 (mirror_extend gpe.py:90-101
+ *                        + decompose fourier.py:183-188)
+ *   vfn_tube_eval     <- tube_eval                 tube.py:58-127 (one reused plan)
  *
  * Conventions
  *   - complex numbers are interleaved (re, im) doubles, numpy complex128;
@@ -127,6 +130,28 @@ int vfn_plan_set_gather(vfn_plan* plan, int variant);
 /* Device time (ms) of the last vfn_plan_eval's gather kernel and of the
  * whole device-side evaluate, measured with CUDA events on its stream. */
 int vfn_plan_last_timing(const vfn_plan* plan, float* gather_ms, float* total_ms);
+
+/* snapshot -> centred coefficients on the computational box: samples
+ * (N1,N2,N3) complex128 on [a, b); along mirrored axes the samples are
+ * extended by their reflection and the box doubles; coeffs_out holds
+ * (N_d * (1 + mirror_d)) complex128 values (gpe.py:90-113).              */
+int vfn_decompose(int device, const double* values, const int64_t shape[3], const double a[3],
+                  const double b[3], const int mirror[3], double* coeffs_out, int on_device,
+                  void* stream);
+
+/* Adaptive low-density point extraction (tube.py:58-127): seeds are the
+ * samples with |v|^2 <= thresholds[0]; each later threshold selects the
+ * parents of the next 3x-refined 27-point stencils, evaluated through one
+ * plan (sigma, m).  Result (host-copied by vfn_tube_copy): count points
+ * (count*3 doubles), densities, levels, sorted by lattice key.  *no_seeds
+ * is set when no sample passes the first threshold (the reference warns). */
+typedef struct vfn_tube vfn_tube;
+int vfn_tube_eval(vfn_tube** out, int device, const double* values, const int64_t shape[3],
+                  const double a[3], const double b[3], const int mirror[3],
+                  const double* thresholds, int nthr, int has_filter, double final_filter,
+                  double sigma, int m, int64_t* count, int* no_seeds, void* stream);
+int vfn_tube_copy(const vfn_tube* tube, double* points, double* density, int64_t* level);
+int vfn_tube_destroy(vfn_tube* tube);
 
 /* Utility (not a reference interface): measured sustained FP64 FMA rate of
  * `device` in TFLOP/s over ~`seconds`, the roofline denominator bench.py

@@ -247,3 +247,72 @@ def bin_keys(points, a, b, n, box=(1, 1, 4), tile=(4, 4, 4)) -> np.ndarray:
 def bin_permutation(points, a, b, n, box=(1, 1, 4), tile=(4, 4, 4)) -> np.ndarray:
     """Stable argsort of bin_keys: sorted position -> input row."""
     return np.argsort(bin_keys(points, a, b, n, box, tile), kind="stable")
+
+
+# ---------------------------------------------------------------------------
+# SURVEY 8f next rows: the step before the path (snapshot -> coefficients) and
+# the in-package caller that reuses a plan (tube refinement).
+# ---------------------------------------------------------------------------
+
+
+def mirror_extend(values: np.ndarray, a, b, mirror):
+    """Append the index-reversed samples along mirrored axes; the box doubles
+    there (gpe.py:81-101).  Returns (values, a, b_ext)."""
+    b_ext = list(np.asarray(b, dtype=float))
+    a = np.asarray(a, dtype=float)
+    for d in range(3):
+        if mirror[d]:
+            values = np.concatenate([values, np.flip(values, axis=d)], axis=d)
+            b_ext[d] = a[d] + 2.0 * (b_ext[d] - a[d])
+    return values, a, np.asarray(b_ext)
+
+
+def decompose(values: np.ndarray, a, b) -> np.ndarray:
+    """Centred coefficients fftshift(fftn(v)) * prod(sqrt(w)/N) (fourier.py:183-188)."""
+    n = np.array(values.shape)
+    widths = np.asarray(b, dtype=float) - np.asarray(a, dtype=float)
+    scale = float(np.prod(np.sqrt(widths) / n))
+    return np.fft.fftshift(scipy.fft.fftn(values, workers=-1)) * scale
+
+
+def tube_eval(values, a, b, mirror, thresholds, final_filter=None, sigma=2.0, m=6):
+    """Adaptive low-density point extraction with one reused plan
+    (tube.py:58-127).  Returns (points, density, level) sorted by lattice key."""
+    thresholds = [float(t) for t in np.atleast_1d(thresholds)]
+    levels = len(thresholds)
+    ext, a_ext, b_ext = mirror_extend(values, a, b, mirror)
+    coeffs = decompose(ext, a_ext, b_ext)
+    shape = np.array(ext.shape)
+    widths = b_ext - a_ext
+    scale = 3 ** levels
+    lattice = shape * scale
+    rho_grid = (values.real ** 2 + values.imag ** 2).ravel()
+    seeds = np.flatnonzero(rho_grid <= thresholds[0])
+    empty = (np.empty((0, 3)), np.empty(0), np.empty(0, dtype=np.int64))
+    if seeds.size == 0:
+        return empty
+    idx = (np.stack(np.unravel_index(seeds, values.shape), axis=1) * scale).astype(np.int64)
+    rho = rho_grid[seeds]
+    level = np.zeros(idx.shape[0], dtype=np.int64)
+    grid, n, beta = oversampled_grid(coeffs, a_ext, b_ext, sigma, m)
+    offs = np.stack(np.meshgrid([-1, 0, 1], [-1, 0, 1], [-1, 0, 1], indexing="ij")).reshape(3, 27).T
+    for ell in range(1, levels + 1):
+        keep = rho <= thresholds[ell - 1]
+        if not keep.any():
+            return empty
+        parents, plevel = idx[keep], level[keep]
+        step = 3 ** (levels - ell)
+        idx = ((parents[:, None, :] + offs[None, :, :] * step).reshape(-1, 3)) % lattice
+        level = np.full(idx.shape[0], ell, dtype=np.int64)
+        level[13::27] = plevel
+        coords = a_ext + idx * (widths / lattice)
+        vals = gather_eval(grid, n, m, beta, coords, a_ext, b_ext)
+        rho = vals.real ** 2 + vals.imag ** 2
+    if final_filter is not None:
+        keep = rho <= float(final_filter)
+        idx, rho, level = idx[keep], rho[keep], level[keep]
+    if idx.shape[0] == 0:
+        return empty
+    keys = (idx[:, 0] * lattice[1] + idx[:, 1]) * lattice[2] + idx[:, 2]
+    order = np.argsort(keys, kind="stable")
+    return a_ext + idx[order] * (widths / lattice), rho[order], level[order]

@@ -15,13 +15,17 @@ from .nufft import (
     rescale_coeffs,
 )
 from .rectilinear import basis_matrix, eval_rectilinear
+from .tube import Snapshot, TubePointCloud, computational_domain, snapshot_spectral, tube_eval
 
 __all__ = [
     "AccuracyWarning",
     "DomainBox",
     "NufftParams",
     "NufftPlan",
+    "Snapshot",
     "SpectralField",
+    "TubePointCloud",
+    "computational_domain",
     "basis_matrix",
     "eval_direct",
     "eval_nufft",
@@ -29,6 +33,8 @@ __all__ = [
     "map_to_torus",
     "regular_grid",
     "rescale_coeffs",
+    "snapshot_spectral",
+    "tube_eval",
 ]
 
 __version__ = "0.1.0"

@@ -66,6 +66,18 @@ SIGNATURES = {
         ctypes.c_int,
         [ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
     ),
+    "vfn_decompose": (
+        ctypes.c_int,
+        [ctypes.c_int, _c_i64_3, _c_f64_3, _c_f64_3, ctypes.c_int * 3, _vp, _vp, ctypes.c_int, _vp],
+    ),
+    "vfn_tube_eval": (
+        ctypes.c_int,
+        [ctypes.POINTER(_vp), ctypes.c_int, _vp, _c_i64_3, _c_f64_3, _c_f64_3, ctypes.c_int * 3,
+         _vp, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+         ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int), _vp],
+    ),
+    "vfn_tube_copy": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "vfn_tube_destroy": (ctypes.c_int, [_vp]),
     "vfn_plan_last_timing": (
         ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
     ),

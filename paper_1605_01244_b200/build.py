@@ -9,7 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvfnfft.so")
-SOURCES = ["vfn_host.cpp", "vfn_kernels.cu", "vfn_gather.cu", "vfn_gather_m6.cu", "vfn_rect.cu", "vfn_direct.cu", "vfn_util.cu", "vfn_api.cu"]
+SOURCES = ["vfn_host.cpp", "vfn_kernels.cu", "vfn_gather.cu", "vfn_gather_m6.cu", "vfn_rect.cu", "vfn_direct.cu", "vfn_util.cu", "vfn_tube.cu", "vfn_api.cu"]
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

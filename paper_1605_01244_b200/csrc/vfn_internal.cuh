@@ -44,10 +44,29 @@ struct DeviceGuard {
   }
 };
 
-// Grow-only device buffer owned by a plan.
+// Grow-only device buffer; owns its allocation (freed on release() or
+// destruction), movable, not copyable.
 struct DevBuf {
   void* ptr = nullptr;
   size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), bytes(o.bytes) {
+    o.ptr = nullptr;
+    o.bytes = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      ptr = o.ptr;
+      bytes = o.bytes;
+      o.ptr = nullptr;
+      o.bytes = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
   int ensure(size_t need) {
     if (need <= bytes) return VFN_OK;
     if (ptr) cudaFree(ptr);

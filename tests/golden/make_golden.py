@@ -182,6 +182,28 @@ def rectilinear_cases():
     save("rect_cases.npz", **out)
 
 
+
+
+def tube_case():
+    """tube_eval on the reference's single-vortex snapshot (tests/test_tube.py
+    fixture): thresholds (0.4, 0.3), plus (0.4,) and a final filter."""
+    from vortexfourier.gpe import Snapshot, snapshot_spectral
+    from vortexfourier.tube import tube_eval
+
+    dom = vf.DomainBox((-10.0, -10.0, -10.0), (10.0, 10.0, 10.0))
+    spec = vf.VortexSpec(position=(0.0, 0.0, 0.0), direction=(0.0, 0.0, 1.0))
+    init = vf.initial_field(dom, (16, 16, 16), [spec])
+    snap = Snapshot(dom, init.values, (True, True, True), 0.0)
+    out = {"values": snap.values, "a": np.array(dom.a), "b": np.array(dom.b),
+           "mirror": np.array(snap.mirror), "spectral": snapshot_spectral(snap).coeffs}
+    for tag, thr, ff in (("two", [0.4, 0.3], None), ("one", [0.4], None), ("filt", [0.4, 0.3], 0.15)):
+        cloud = tube_eval(snap, thr, final_filter=ff)
+        out[f"{tag}_points"] = cloud.points
+        out[f"{tag}_density"] = cloud.density
+        out[f"{tag}_level"] = cloud.level
+    save("tube_case.npz", **out)
+
+
 if __name__ == "__main__":
     nufft_cases()
     torus_edges()
@@ -189,3 +211,4 @@ if __name__ == "__main__":
     config1()
     cluster_small()
     rectilinear_cases()
+    tube_case()

@@ -342,3 +342,47 @@ def test_box_widths_agree(vfb, offset_box):
         assert plan.geometry(len(pts))[0][0] == bxy
         l2, linf = rel_err(out, ref)
         assert l2 < 1e-13 and linf < 1e-13, (bxy, l2, linf)
+
+
+# ---------------------------------------------------------------- SURVEY 8f next rows
+
+
+def _tube_snap(vfb):
+    g = golden("tube_case.npz")
+    dom = vfb.DomainBox(tuple(g["a"]), tuple(g["b"]))
+    return g, vfb.Snapshot(dom, g["values"], tuple(bool(x) for x in g["mirror"]), 0.0)
+
+
+def test_snapshot_spectral_matches_reference(vfb):
+    g, snap = _tube_snap(vfb)
+    spec = vfb.snapshot_spectral(snap)
+    assert spec.domain.b == (30.0, 30.0, 30.0)
+    l2, linf = rel_err(spec.coeffs, g["spectral"])
+    assert l2 < 1e-14 and linf < 1e-13, (l2, linf)
+
+
+@pytest.mark.parametrize("tag,thr,ff", [("two", [0.4, 0.3], None), ("one", [0.4], None),
+                                        ("filt", [0.4, 0.3], 0.15)])
+def test_tube_eval_matches_reference(vfb, tag, thr, ff):
+    """Same point set, levels and lattice order as the reference (bit-exact),
+    densities to rounding (reference test_tube.py:85-115)."""
+    g, snap = _tube_snap(vfb)
+    cloud = vfb.tube_eval(snap, thr, final_filter=ff)
+    np.testing.assert_array_equal(cloud.points, g[f"{tag}_points"])
+    np.testing.assert_array_equal(cloud.level, g[f"{tag}_level"])
+    np.testing.assert_allclose(cloud.density, g[f"{tag}_density"], rtol=0, atol=1e-13)
+    if tag == "two":
+        assert np.unique(cloud.level, return_counts=True)[1].tolist() == [16, 992, 26208]
+
+
+def test_tube_empty_outcomes(vfb):
+    import warnings as w
+
+    dom = vfb.DomainBox((0.0, 0.0, 0.0), (1.0, 1.0, 1.0))
+    snap = vfb.Snapshot(dom, np.ones((8, 8, 8)), (False, False, False), 0.0)
+    with pytest.warns(RuntimeWarning, match="empty cloud"):
+        cloud = vfb.tube_eval(snap, [0.5])
+    assert len(cloud) == 0 and cloud.points.shape == (0, 3)
+    with w.catch_warnings():
+        w.simplefilter("error")
+        assert len(vfb.tube_eval(snap, [1.5, 0.5])) == 0

@@ -77,3 +77,16 @@ def test_rectilinear_argument_errors(unit_box):
 def test_points_shape_errors(unit_box):
     with pytest.raises(ValueError, match=r"\(M, 3\)"):
         vfb.map_to_torus(np.zeros((4, 2)), unit_box)
+
+
+def test_tube_argument_errors():
+    dom = vfb.DomainBox((0.0, 0.0, 0.0), (1.0, 1.0, 1.0))
+    snap = vfb.Snapshot(dom, np.ones((8, 8, 8)), (False, False, False), 0.0)
+    with pytest.raises(ValueError, match="thresholds"):
+        vfb.tube_eval(snap, [])
+    for bad in ([0.0], [0.2, -1.0]):
+        with pytest.raises(ValueError, match="positive"):
+            vfb.tube_eval(snap, bad)
+    with pytest.raises(ValueError, match="inconsistent"):
+        vfb.TubePointCloud(np.zeros((4, 3)), np.zeros(3), np.zeros(3, dtype=np.int64))
+    assert vfb.computational_domain(dom, (True, False, True)).b == (2.0, 1.0, 2.0)

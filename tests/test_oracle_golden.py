@@ -126,3 +126,18 @@ def test_domain_violation():
     assert O.domain_violation(pts, a, b) == 1
     assert O.domain_violation(pts[[0, 2]], a, b) == 1
     assert O.domain_violation(pts[:1], a, b) == -1
+
+
+def test_tube_oracle_matches_reference():
+    """The oracle's snapshot_spectral and tube_eval restatements reproduce the
+    reference (tube.py:58-127, gpe.py:90-113) bit for bit."""
+    g = golden("tube_case.npz")
+    ext, a, b = O.mirror_extend(g["values"], g["a"], g["b"], g["mirror"])
+    np.testing.assert_array_equal(O.decompose(ext, a, b), g["spectral"])
+    for tag, thr, ff in (("two", [0.4, 0.3], None), ("one", [0.4], None), ("filt", [0.4, 0.3], 0.15)):
+        p, rho, lev = O.tube_eval(g["values"], g["a"], g["b"], g["mirror"], thr, ff)
+        np.testing.assert_array_equal(p, g[f"{tag}_points"])
+        np.testing.assert_array_equal(rho, g[f"{tag}_density"])
+        np.testing.assert_array_equal(lev, g[f"{tag}_level"])
+    levels, counts = np.unique(g["two_level"], return_counts=True)
+    assert counts.tolist() == [16, 992, 26208]  # reference test_tube.py:85-89
