@@ -86,8 +86,8 @@ def snapshot_spectral(snap) -> SpectralField:
     out = np.empty(shape, dtype=np.complex128)
     dev = _device_of(None)
     _lib.check(
-        _lib.load().vfn_decompose(dev, _lib.i64x3(values.shape), _lib.f64x3(snap.domain.a),
-                                  _lib.f64x3(snap.domain.b), mirror, values.ctypes.data,
+        _lib.load().vfn_decompose(dev, values.ctypes.data, _lib.i64x3(values.shape),
+                                  _lib.f64x3(snap.domain.a), _lib.f64x3(snap.domain.b), mirror,
                                   out.ctypes.data, 0, _stream_of(dev))
     )
     return SpectralField(dom, out)
