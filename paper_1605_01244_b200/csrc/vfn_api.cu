@@ -1,4 +1,5 @@
 // extern "C" entry points of libvfnfft (see include/vfnfft.h).
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -244,6 +245,8 @@ int vfn_plan_destroy(vfn_plan* p) {
   for (DevBuf* b : bufs) b->release();
   for (int i = 0; i < 4; ++i)
     if (p->ev[i]) cudaEventDestroy(p->ev[i]);
+  for (int i = 0; i < 2; ++i)
+    if (p->copy_stream[i]) cudaStreamDestroy(p->copy_stream[i]);
   delete p;
   return VFN_OK;
 }
@@ -390,24 +393,40 @@ int vfn_plan_bin(vfn_plan* p, const double* points, int64_t M, uint32_t* keys, i
   return VFN_OK;
 }
 
-int vfn_plan_eval(vfn_plan* p, const double* points, int64_t M, double* out, int on_device,
-                  int64_t* first_bad_row, void* stream) {
-  if (!p || (M > 0 && (!points || !out))) return fail(VFN_ERR_INVALID, "null argument");
-  if (M < 0 || M > INT32_MAX) return fail(VFN_ERR_INVALID, "point count out of range");
-  if (first_bad_row) *first_bad_row = -1;
-  if (M == 0) return VFN_OK;
-  DeviceGuard guard(p->device);
-  cudaStream_t s = as_stream(stream);
-  VFN_CUDA(cudaEventRecord(p->ev[0], s));
+}  // extern "C"
+
+namespace {
+
+constexpr unsigned char kBadByte = 0x7f;  // memset sentinel: 0x7f7f... > any row
+constexpr int64_t kBadSentinel = 0x7f7f7f7f7f7f7f7fLL;
+
+// Enqueue one evaluation of M device-resident points on stream s (no host
+// synchronisation unless the geometry has to be sampled): map + key + sort,
+// then the gather.  bad_dev receives the first out-of-domain row (relative).
+int eval_enqueue(vfn_plan* p, const double* pts_dev, int64_t M, double2* out_dev, int64_t* bad_dev,
+                 cudaStream_t s, const BinGeom* fixed) {
   BinGeom g;
-  const double* pts_dev;
-  int64_t* bad_dev;
-  VFN_CHECK(bin_points(p, points, M, on_device, &g, &pts_dev, &bad_dev, s));
-  double2* out_dev = reinterpret_cast<double2*>(out);
-  if (!on_device) {
-    VFN_CHECK(p->out.ensure(sizeof(double2) * M));
-    out_dev = p->out.as<double2>();
+  if (fixed) {
+    g = *fixed;
+    p->last_geom = g;
+    p->has_last_geom = true;
+  } else {
+    VFN_CHECK(choose_geometry(p, M, pts_dev, s, &g));
   }
+  const bool want_u = p->gather_variant != 1 && m6_applicable(p, g);
+  VFN_CUDA(cudaMemsetAsync(bad_dev, kBadByte, sizeof(int64_t), s));
+  VFN_CHECK(p->keys.ensure(sizeof(uint32_t) * M));
+  VFN_CHECK(p->keys_sorted.ensure(sizeof(uint32_t) * M));
+  VFN_CHECK(p->idx.ensure(sizeof(int32_t) * M));
+  VFN_CHECK(p->perm.ensure(sizeof(int32_t) * M));
+  double* u = nullptr;
+  if (want_u) {
+    VFN_CHECK(p->uvals.ensure(sizeof(double) * 3 * M));
+    u = p->uvals.as<double>();
+  }
+  VFN_CHECK(map_and_key(p, pts_dev, M, g, p->keys.as<uint32_t>(), p->idx.as<int32_t>(), u, bad_dev, s));
+  VFN_CHECK(sort_pairs(p, p->keys.as<uint32_t>(), p->keys_sorted.as<uint32_t>(), p->idx.as<int32_t>(),
+                       p->perm.as<int32_t>(), M, key_bits_for(g.nboxes * g.cells_per_box), s));
   VFN_CUDA(cudaEventRecord(p->ev[1], s));
   bool used = false;
   if (p->gather_variant != 1)
@@ -418,18 +437,113 @@ int vfn_plan_eval(vfn_plan* p, const double* points, int64_t M, double* out, int
     VFN_CHECK(gather_simple(p, pts_dev, M, p->perm.as<int32_t>(), out_dev, s));
   }
   VFN_CUDA(cudaEventRecord(p->ev[2], s));
+  return VFN_OK;
+}
+
+int outside(int64_t bad, int64_t* first_bad_row) {
+  if (first_bad_row) *first_bad_row = bad;
+  return fail(VFN_ERR_OUTSIDE, "point (row " + std::to_string(bad) + ") lies outside the domain");
+}
+
+// Host buffers, large M: chunks of points flow H2D (copy stream) -> evaluate
+// (caller's stream) -> D2H (second copy stream), double-buffered, so the PCIe
+// transfers of neighbouring chunks overlap the computation (pinned memory
+// makes the copies asynchronous).
+int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* out,
+                        int64_t* first_bad_row, cudaStream_t s) {
+  const int64_t chunk = std::max<int64_t>((int64_t)1 << 22, (M + 7) / 8);
+  const int64_t nc = (M + chunk - 1) / chunk;
+  for (int i = 0; i < 2; ++i) {
+    if (!p->copy_stream[i]) VFN_CUDA(cudaStreamCreateWithFlags(&p->copy_stream[i], cudaStreamNonBlocking));
+  }
+  cudaStream_t sin = p->copy_stream[0], sout = p->copy_stream[1];
+  VFN_CHECK(p->pts.ensure(sizeof(double) * 3 * 2 * chunk));
+  VFN_CHECK(p->out.ensure(sizeof(double2) * 2 * chunk));
+  VFN_CHECK(p->misc.ensure(sizeof(int64_t) * (nc + 8)));
+  int64_t* bad_dev = p->misc.as<int64_t>();
+  std::vector<cudaEvent_t> ev(3 * nc);
+  for (auto& e : ev) VFN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  auto e_in = [&](int64_t i) { return ev[3 * i]; };
+  auto e_comp = [&](int64_t i) { return ev[3 * i + 1]; };
+  auto e_out = [&](int64_t i) { return ev[3 * i + 2]; };
+  int st = VFN_OK;
+  BinGeom g;
+  bool have_g = false;
+  VFN_CUDA(cudaEventRecord(p->ev[0], s));
+  for (int64_t i = 0; i < nc && st == VFN_OK; ++i) {
+    const int64_t lo = i * chunk, n = std::min(chunk, M - lo);
+    double* pbuf = p->pts.as<double>() + 3 * chunk * (i & 1);
+    double2* obuf = p->out.as<double2>() + chunk * (i & 1);
+    if (i >= 2) cudaStreamWaitEvent(sin, e_comp(i - 2), 0);
+    cudaMemcpyAsync(pbuf, points + 3 * lo, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, sin);
+    cudaEventRecord(e_in(i), sin);
+    cudaStreamWaitEvent(s, e_in(i), 0);
+    if (i >= 2) cudaStreamWaitEvent(s, e_out(i - 2), 0);
+    // one geometry for all chunks (decided on the first), no mid-pipeline syncs
+    st = eval_enqueue(p, pbuf, n, obuf, bad_dev + i, s, have_g ? &g : nullptr);
+    if (st != VFN_OK) break;
+    if (!have_g) {
+      g = p->last_geom;
+      have_g = true;
+    }
+    cudaEventRecord(e_comp(i), s);
+    cudaStreamWaitEvent(sout, e_comp(i), 0);
+    cudaMemcpyAsync(out + 2 * lo, obuf, sizeof(double2) * n, cudaMemcpyDeviceToHost, sout);
+    cudaEventRecord(e_out(i), sout);
+  }
+  std::vector<int64_t> bad(nc, kBadSentinel);
+  if (st == VFN_OK) {
+    cudaStreamWaitEvent(s, e_out(nc - 1), 0);
+    cudaMemcpyAsync(bad.data(), bad_dev, sizeof(int64_t) * nc, cudaMemcpyDeviceToHost, s);
+    cudaEventRecord(p->ev[3], s);
+  }
+  cudaError_t e = cudaStreamSynchronize(s);
+  cudaStreamSynchronize(sin);
+  cudaStreamSynchronize(sout);
+  for (auto& x : ev) cudaEventDestroy(x);
+  if (st != VFN_OK) return st;
+  if (e != cudaSuccess) return fail(VFN_ERR_CUDA, std::string("pipelined evaluate: ") + cudaGetErrorString(e));
+  cudaEventElapsedTime(&p->last_gather_ms, p->ev[1], p->ev[2]);
+  cudaEventElapsedTime(&p->last_total_ms, p->ev[0], p->ev[3]);
+  for (int64_t i = 0; i < nc; ++i)
+    if (bad[i] != kBadSentinel) return outside(i * chunk + bad[i], first_bad_row);
+  return VFN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vfn_plan_eval(vfn_plan* p, const double* points, int64_t M, double* out, int on_device,
+                  int64_t* first_bad_row, void* stream) {
+  if (!p || (M > 0 && (!points || !out))) return fail(VFN_ERR_INVALID, "null argument");
+  if (M < 0 || M > INT32_MAX) return fail(VFN_ERR_INVALID, "point count out of range");
+  if (first_bad_row) *first_bad_row = -1;
+  if (M == 0) return VFN_OK;
+  DeviceGuard guard(p->device);
+  cudaStream_t s = as_stream(stream);
+  if (!on_device && M >= ((int64_t)1 << 23))
+    return eval_host_pipelined(p, points, M, out, first_bad_row, s);
+  VFN_CUDA(cudaEventRecord(p->ev[0], s));
+  const void* pdev = nullptr;
+  VFN_CHECK(stage_in(p->pts, points, sizeof(double) * 3 * M, on_device, &pdev, s));
+  double2* out_dev = reinterpret_cast<double2*>(out);
+  if (!on_device) {
+    VFN_CHECK(p->out.ensure(sizeof(double2) * M));
+    out_dev = p->out.as<double2>();
+  }
+  VFN_CHECK(p->misc.ensure(64));
+  int64_t* bad_dev = p->misc.as<int64_t>();
+  VFN_CHECK(eval_enqueue(p, static_cast<const double*>(pdev), M, out_dev, bad_dev, s, nullptr));
   if (!on_device)
     VFN_CUDA(cudaMemcpyAsync(out, out_dev, sizeof(double2) * M, cudaMemcpyDeviceToHost, s));
-  int64_t bad = INT64_MAX;
+  int64_t bad = kBadSentinel;
   VFN_CUDA(cudaMemcpyAsync(&bad, bad_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   VFN_CUDA(cudaEventRecord(p->ev[3], s));
   VFN_CUDA(cudaStreamSynchronize(s));
   cudaEventElapsedTime(&p->last_gather_ms, p->ev[1], p->ev[2]);
   cudaEventElapsedTime(&p->last_total_ms, p->ev[0], p->ev[3]);
-  if (bad != INT64_MAX) {
-    if (first_bad_row) *first_bad_row = bad;
-    return fail(VFN_ERR_OUTSIDE, "point (row " + std::to_string(bad) + ") lies outside the domain");
-  }
+  if (bad != kBadSentinel) return outside(bad, first_bad_row);
   return VFN_OK;
 }
 

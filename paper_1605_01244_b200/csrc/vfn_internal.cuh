@@ -145,6 +145,7 @@ struct vfn_plan {
   // evaluate scratch (grow-only)
   vfn::DevBuf pts, out, uvals, keys, keys_sorted, idx, perm, sort_tmp, box_start, items, units, uscratch, misc;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t copy_stream[2] = {nullptr, nullptr};  // H2D / D2H of the pipelined host path
   float last_gather_ms = 0.f, last_total_ms = 0.f;
   vfn::BinGeom last_geom;
   bool has_last_geom = false;
