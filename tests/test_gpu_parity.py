@@ -386,3 +386,29 @@ def test_tube_empty_outcomes(vfb):
     with w.catch_warnings():
         w.simplefilter("error")
         assert len(vfb.tube_eval(snap, [1.5, 0.5])) == 0
+
+
+def test_pipelined_host_path(vfb, unit_box):
+    """Host buffers with M >= 2^23 take the chunked H2D/evaluate/D2H pipeline:
+    same bits as the device-resident path for a fixed box width, and the first
+    bad row is reported with its global index."""
+    import torch
+
+    spec = random_spectral(unit_box, (32, 32, 32), 97)
+    rng = np.random.default_rng(98)
+    M = (1 << 23) + 12345
+    pts = rng.uniform(0.0, 1.0, (M, 3))
+    plan = vfb.NufftPlan(spec)
+    plan.set_box(2)
+    host = plan.evaluate(pts)
+    dev = plan.evaluate(torch.as_tensor(pts, device="cuda")).cpu().numpy()
+    np.testing.assert_array_equal(host, dev)
+    sub = rng.choice(M, 3000, replace=False)
+    ref = O.nufft_eval(spec.coeffs, unit_box.a, unit_box.b, pts[sub])
+    l2, linf = rel_err(host[sub], ref)
+    assert l2 < 1e-13 and linf < 1e-13
+    bad = pts.copy()
+    bad[M - 7] = (0.5, 1.5, 0.5)  # in the second chunk
+    bad[M - 3] = (np.nan, 0.5, 0.5)
+    with pytest.raises(ValueError, match=rf"\(row {M - 7}\)"):
+        plan.evaluate(bad)
