@@ -412,3 +412,22 @@ def test_pipelined_host_path(vfb, unit_box):
     bad[M - 3] = (np.nan, 0.5, 0.5)
     with pytest.raises(ValueError, match=rf"\(row {M - 7}\)"):
         plan.evaluate(bad)
+
+
+@pytest.mark.parametrize("shape,sigma", [((18, 22, 26), 2.0), ((20, 30, 10), 1.6)])
+def test_ragged_grids_many_points(vfb, offset_box, shape, sigma):
+    """Oversampled sizes that are not multiples of the 4x4x8 tile (36x44x52,
+    32x48x16 at sigma 1.6) with enough points for many work items per CTA,
+    at both box widths, against the oracle."""
+    spec = random_spectral(offset_box, shape, 99)
+    rng = np.random.default_rng(100)
+    pts = rng.uniform(offset_box.a, offset_box.b, (300000, 3))
+    plan = vfb.NufftPlan(spec, vfb.NufftParams(oversampling=sigma))
+    sub = rng.choice(len(pts), 4000, replace=False)
+    grid, n, beta = O.oversampled_grid(spec.coeffs, offset_box.a, offset_box.b, sigma, 6)
+    ref = O.gather_eval(grid, n, 6, beta, pts[sub], offset_box.a, offset_box.b)
+    for bxy in (1, 2):
+        plan.set_box(bxy)
+        out = plan.evaluate(pts)
+        l2, linf = rel_err(out[sub], ref)
+        assert l2 < 1e-13 and linf < 1e-13, (bxy, l2, linf)
