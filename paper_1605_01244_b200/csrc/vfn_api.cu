@@ -54,6 +54,17 @@ int stage_in(DevBuf& buf, const void* src, size_t bytes, int on_device, const vo
   return VFN_OK;
 }
 
+// The sort's value input is iota (0..M-1); it never changes, so it is kept
+// in the plan and K1 only (re)writes it when a call needs more entries.
+int32_t* iota_for(vfn_plan* p, int64_t M, bool* write) {
+  void* before = p->idx.ptr;
+  if (p->idx.ensure(sizeof(int32_t) * M) != VFN_OK) return nullptr;
+  if (p->idx.ptr != before) p->iota_len = 0;
+  *write = p->iota_len < M;
+  if (*write) p->iota_len = M;
+  return p->idx.as<int32_t>();
+}
+
 int key_bits_for(int64_t nkeys) {
   int bits = 1;
   while (bits < 32 && ((int64_t)1 << bits) < nkeys) ++bits;
@@ -355,14 +366,17 @@ static int bin_points(vfn_plan* p, const double* points, int64_t M, int on_devic
   VFN_CUDA(cudaMemcpyAsync(*bad_dev, &sentinel, sizeof(int64_t), cudaMemcpyHostToDevice, s));
   VFN_CHECK(p->keys.ensure(sizeof(uint32_t) * M));
   VFN_CHECK(p->keys_sorted.ensure(sizeof(uint32_t) * M));
-  VFN_CHECK(p->idx.ensure(sizeof(int32_t) * M));
   VFN_CHECK(p->perm.ensure(sizeof(int32_t) * M));
+  bool write_iota = false;
+  int32_t* iota = iota_for(p, M, &write_iota);
+  if (!iota) return fail(VFN_ERR_NOMEM, "iota allocation failed");
   double* u = nullptr;
   if (want_u) {
     VFN_CHECK(p->uvals.ensure(sizeof(double) * 3 * M));
     u = p->uvals.as<double>();
   }
-  VFN_CHECK(map_and_key(p, *pts_dev, M, g, p->keys.as<uint32_t>(), p->idx.as<int32_t>(), u, *bad_dev, s));
+  VFN_CHECK(map_and_key(p, *pts_dev, M, g, p->keys.as<uint32_t>(), write_iota ? iota : nullptr, u,
+                        *bad_dev, s));
   VFN_CHECK(sort_pairs(p, p->keys.as<uint32_t>(), p->keys_sorted.as<uint32_t>(),
                        p->idx.as<int32_t>(), p->perm.as<int32_t>(), M, key_bits_for(g.nboxes * g.cells_per_box), s));
   return VFN_OK;
@@ -417,14 +431,17 @@ int eval_enqueue(vfn_plan* p, const double* pts_dev, int64_t M, double2* out_dev
   VFN_CUDA(cudaMemsetAsync(bad_dev, kBadByte, sizeof(int64_t), s));
   VFN_CHECK(p->keys.ensure(sizeof(uint32_t) * M));
   VFN_CHECK(p->keys_sorted.ensure(sizeof(uint32_t) * M));
-  VFN_CHECK(p->idx.ensure(sizeof(int32_t) * M));
   VFN_CHECK(p->perm.ensure(sizeof(int32_t) * M));
+  bool write_iota = false;
+  int32_t* iota = iota_for(p, M, &write_iota);
+  if (!iota) return fail(VFN_ERR_NOMEM, "iota allocation failed");
   double* u = nullptr;
   if (want_u) {
     VFN_CHECK(p->uvals.ensure(sizeof(double) * 3 * M));
     u = p->uvals.as<double>();
   }
-  VFN_CHECK(map_and_key(p, pts_dev, M, g, p->keys.as<uint32_t>(), p->idx.as<int32_t>(), u, bad_dev, s));
+  VFN_CHECK(map_and_key(p, pts_dev, M, g, p->keys.as<uint32_t>(), write_iota ? iota : nullptr, u,
+                        bad_dev, s));
   VFN_CHECK(sort_pairs(p, p->keys.as<uint32_t>(), p->keys_sorted.as<uint32_t>(), p->idx.as<int32_t>(),
                        p->perm.as<int32_t>(), M, key_bits_for(g.nboxes * g.cells_per_box), s));
   VFN_CUDA(cudaEventRecord(p->ev[1], s));

@@ -149,6 +149,7 @@ struct vfn_plan {
   float last_gather_ms = 0.f, last_total_ms = 0.f;
   vfn::BinGeom last_geom;
   bool has_last_geom = false;
+  int64_t iota_len = 0;  // idx[0..iota_len) holds 0, 1, 2, ... (the sort's values)
 };
 
 namespace vfn {
