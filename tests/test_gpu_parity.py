@@ -431,3 +431,22 @@ def test_ragged_grids_many_points(vfb, offset_box, shape, sigma):
         out = plan.evaluate(pts)
         l2, linf = rel_err(out[sub], ref)
         assert l2 < 1e-13 and linf < 1e-13, (bxy, l2, linf)
+
+
+def test_c_abi_from_plain_c(tmp_path):
+    """The boundary works without Python: examples/c_api_demo.c links
+    libvfnfft.so directly, evaluates against vfn_direct_eval and checks the
+    outside-point status (exit code 0 on success)."""
+    import subprocess
+
+    from conftest import REPO
+
+    exe = tmp_path / "c_api_demo"
+    lib = f"{REPO}/paper_1605_01244_b200"
+    cc = subprocess.run(["gcc", "-O2", "-I", f"{REPO}/include", f"{REPO}/examples/c_api_demo.c",
+                         "-L", lib, "-lvfnfft", f"-Wl,-rpath,{lib}", "-lm", "-o", str(exe)],
+                        capture_output=True, text=True)
+    assert cc.returncode == 0, cc.stderr
+    run = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert run.returncode == 0, run.stdout + run.stderr
+    assert "first bad row 17" in run.stdout
