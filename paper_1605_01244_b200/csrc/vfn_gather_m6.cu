@@ -154,7 +154,7 @@ __device__ __forceinline__ UnitPoints load_unit_points(const Args& A, int4 desc,
 }
 
 template <int BXY, int KC>
-__device__ __forceinline__ void gather_unit(const Args& A, const double (&cb)[4][2], double* wt,
+__device__ __forceinline__ void gather_unit(const Args& A, const double* __restrict__ scb, double* wt,
                                             unsigned tile_s, int tile, int ox, int oy, int oz,
                                             int4 desc, const UnitPoints& up, int lane) {
   constexpr int XB = BXY + 12, YB = BXY + 12;  // box footprint rows per axis
@@ -188,8 +188,9 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double (&cb)[4]
     double w00 = 0.0, w01 = 0.0, w10 = 0.0, w11 = 0.0;
 #pragma unroll
     for (int kc = 0; kc < 4; ++kc) {
-      dmma(w00, w01, pw, cb[kc][0]);
-      dmma(w10, w11, pw, cb[kc][1]);
+      const double2 c = *reinterpret_cast<const double2*>(scb + 2 * kc);  // (nb 0, nb 1)
+      dmma(w00, w01, pw, c.x);
+      dmma(w10, w11, pw, c.y);
       pw *= x4;
     }
     double* row = d == 2 ? wA + g * kAS + kAO : (d == 0 ? wX : wY) + g * kXS + kXO;
@@ -305,18 +306,23 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   int* ctr = done + 2;                                       // next CTA unit to hand out
   int* loaded = done + 4;                                    // loaded[2]: item ordinal per buffer
   double* wts = reinterpret_cast<double*>(ctl + 48);         // [kWarps][kWarpW]
+  double* scb_all = wts + kWarps * kWarpW;                    // [32 lanes][8]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tig = lane & 3;
   for (int i = tid; i < kWarps * kWarpW; i += blockDim.x) wts[i] = 0.0;  // zero pads
-  double cb[4][2];  // B fragments of the weights DMMA: C[d = 4 kc + tig][j = 8 nb + g]
+  // B fragments of the weights DMMA, C[d = 4 kc + tig][j = 8 nb + g], per
+  // lane in shared memory (kept out of the register budget)
+  if (warp == 0) {
 #pragma unroll
-  for (int kc = 0; kc < 4; ++kc)
+    for (int kc = 0; kc < 4; ++kc)
 #pragma unroll
-    for (int nb = 0; nb < 2; ++nb) {
-      const int d = 4 * kc + tig, j = 8 * nb + g;
-      cb[kc][nb] = (d <= A.deg && j < 13) ? A.poly[j * (A.deg + 1) + d] : 0.0;
-    }
+      for (int nb = 0; nb < 2; ++nb) {
+        const int d = 4 * kc + tig, j = 8 * nb + g;
+        scb_all[lane * 8 + 2 * kc + nb] = (d <= A.deg && j < 13) ? A.poly[j * (A.deg + 1) + d] : 0.0;
+      }
+  }
+  const double* scb = scb_all + lane * 8;
   // this CTA's k-th item: strided over the tile-ordered item list, so the
   // 148 CTAs work on neighbouring tiles at any moment and share the tiles'
   // halos through L2 (contiguous blocks per CTA measured 38% more DRAM reads)
@@ -401,9 +407,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     while (*reinterpret_cast<volatile int*>(&loaded[b]) != kk) __nanosleep(64);
     mbar_wait(bar_s + 8 * b, (kk >> 1) & 1);
     if ((desc.y >> 4) & 1)
-      gather_unit<BXY, 5>(A, cb, wt, tile_s, tile, t0 * 4, t1 * 4, t2 * kTZ, desc, up, lane);
+      gather_unit<BXY, 5>(A, scb, wt, tile_s, tile, t0 * 4, t1 * 4, t2 * kTZ, desc, up, lane);
     else
-      gather_unit<BXY, 4>(A, cb, wt, tile_s, tile, t0 * 4, t1 * 4, t2 * kTZ, desc, up, lane);
+      gather_unit<BXY, 4>(A, scb, wt, tile_s, tile, t0 * 4, t1 * 4, t2 * kTZ, desc, up, lane);
     if (lane == 0) {
       if (atomicAdd(&done[b], 1) == item.z - item.y - 1) {  // last unit of item kk
         done[b] = 0;
@@ -510,7 +516,7 @@ int make_grid_tmap(vfn_plan* p) {
 }
 
 static size_t m6_smem_bytes() {
-  return 1024 + 2 * m6::kTileBytes + 48 + sizeof(double) * m6::kWarps * m6::kWarpW;  // ctl: bars, done, ctr
+  return 1024 + 2 * m6::kTileBytes + 48 + sizeof(double) * (m6::kWarps * m6::kWarpW + 32 * 8);
 }
 
 bool m6_applicable(const vfn_plan* p, const BinGeom& g) {
