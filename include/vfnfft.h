@@ -23,6 +23,14 @@
  *                        + decompose fourier.py:183-188)
  *   vfn_tube_eval     <- tube_eval                 tube.py:58-127 (one reused plan)
  *
+ * File formats feeding the path, native and multithreaded:
+ *   vfn_snapshot_*    <- read_snapshot / write_snapshot   snapshots.py:29-72
+ *   vfn_csv_read, vfn_table_*  <- read_points_csv         fields.py:160-174
+ *   vfn_csv_write     <- write_points_csv                  fields.py:146-157
+ *   vfn_field_write   <- write_field                       fields.py:67-95
+ *   vfn_vtk_write     <- write_vtk_rectilinear             fields.py:119-143
+ *   vfn_density       <- values.real**2 + values.imag**2   cli.py:94, :113
+ *
  * Conventions
  *   - complex numbers are interleaved (re, im) doubles, numpy complex128;
  *   - points are (M, 3) row-major doubles; coefficients are (N1, N2, N3)
@@ -52,7 +60,8 @@ typedef enum {
   VFN_ERR_CUDA = -3,      /* CUDA runtime error                               */
   VFN_ERR_CUFFT = -4,     /* cuFFT error                                      */
   VFN_ERR_CUBLAS = -5,    /* cuBLAS error                                     */
-  VFN_ERR_NOMEM = -6      /* device allocation failed                         */
+  VFN_ERR_NOMEM = -6,     /* device allocation failed                         */
+  VFN_ERR_IO = -7         /* file open / read / write failed -> OSError        */
 } vfn_status;
 
 typedef struct vfn_plan vfn_plan;
@@ -144,7 +153,8 @@ int vfn_decompose(int device, const double* values, const int64_t shape[3], cons
  * parents of the next 3x-refined 27-point stencils, evaluated through one
  * plan (sigma, m).  Result (host-copied by vfn_tube_copy): count points
  * (count*3 doubles), densities, levels, sorted by lattice key.  *no_seeds
- * is set when no sample passes the first threshold (the reference warns). */
+ * is set when no sample passes the first threshold (the reference warns).
+ * `values` may be host or device memory (copied with cudaMemcpyDefault). */
 typedef struct vfn_tube vfn_tube;
 int vfn_tube_eval(vfn_tube** out, int device, const double* values, const int64_t shape[3],
                   const double a[3], const double b[3], const int mirror[3],
@@ -152,6 +162,61 @@ int vfn_tube_eval(vfn_tube** out, int device, const double* values, const int64_
                   double sigma, int m, int64_t* count, int* no_seeds, void* stream);
 int vfn_tube_copy(const vfn_tube* tube, double* points, double* density, int64_t* level);
 int vfn_tube_destroy(vfn_tube* tube);
+
+/* ------------------------------------------------------------ file formats
+ * Byte-compatible with the reference writers/readers; format violations
+ * return VFN_ERR_INVALID with the reference's message, OS failures
+ * VFN_ERR_IO.  `on_device` buffers are staged through pinned host memory
+ * with the file reads / writes overlapping the copies on `stream`. */
+
+/* SFS1 header (snapshots.py:1-15): physical box, grid, mirror flags, time. */
+typedef struct {
+  double a[3], b[3];
+  int64_t shape[3];
+  int mirror[3];
+  double time;
+} vfn_snapshot_info;
+
+/* Header only, validated against the file size (snapshots.py:50-71). */
+int vfn_snapshot_info_read(const char* path, vfn_snapshot_info* info);
+/* Header + payload into `values` (shape[0]*shape[1]*shape[2] complex,
+ * `capacity` complex elements available). */
+int vfn_snapshot_read(const char* path, vfn_snapshot_info* info, double* values, int64_t capacity,
+                      int on_device, int device, void* stream);
+int vfn_snapshot_write(const char* path, const vfn_snapshot_info* info, const double* values,
+                       int on_device, int device, void* stream);
+
+/* Points CSV (fields.py:146-174): header row of names, one row per point,
+ * parsed as Python float() does.  The table owns the parsed columns. */
+typedef struct vfn_table vfn_table;
+int vfn_csv_read(const char* path, vfn_table** out, int64_t* rows, int* cols);
+int vfn_table_name(const vfn_table* t, int col, const char** name);
+int vfn_table_column(const vfn_table* t, int col, double* out);
+/* Columns cols[0..2] interleaved as (rows, 3) points (host or device). */
+int vfn_table_points(const vfn_table* t, const int cols[3], double* points, int on_device,
+                     int device, void* stream);
+int vfn_table_destroy(vfn_table* t);
+/* x1,x2,x3 + ncols named columns, values as Python repr(); column c is
+ * read at columns[c][i * strides[c]], float64 (kinds[c] = 0) or int64
+ * (kinds[c] = 1).  Host buffers. */
+int vfn_csv_write(const char* path, const double* points, int64_t M, int ncols,
+                  const char* const* names, const void* const* columns, const int64_t* strides,
+                  const int* kinds);
+
+/* rho[i] = re_i*re_i + im_i*im_i, each product rounded (numpy, no FMA). */
+int vfn_density(int device, const double* values, int64_t n, double* rho, int on_device,
+                void* stream);
+
+/* Rectilinear field = text header + raw psi + raw rho (fields.py:67-95). */
+int vfn_field_write(const char* hdr_path, const char* psi_path, const char* rho_path,
+                    const char* psi_name, const char* rho_name, const int64_t shape[3],
+                    const double* const coords[3], const double* values, const double* density,
+                    int has_time, double time, int on_device, int device, void* stream);
+/* Legacy binary VTK rectilinear grid, scalars big-endian float32 with the
+ * first index fastest (fields.py:119-143). */
+int vfn_vtk_write(const char* path, const char* title, const int64_t shape[3],
+                  const double* const coords[3], int nscalars, const char* const* names,
+                  const double* const* scalars, int on_device, int device, void* stream);
 
 /* Utility (not a reference interface): measured sustained FP64 FMA rate of
  * `device` in TFLOP/s over ~`seconds`, the roofline denominator bench.py

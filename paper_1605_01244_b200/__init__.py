@@ -4,6 +4,7 @@ package `vortexfourier` (scattered-point and rectilinear-grid evaluation of a
 kernels through the C ABI in include/vfnfft.h (libvfnfft.so, built in-tree).
 """
 
+from . import formats, pipeline
 from .fourier import DomainBox, SpectralField, regular_grid
 from .nufft import (
     AccuracyWarning,
@@ -26,6 +27,8 @@ __all__ = [
     "SpectralField",
     "TubePointCloud",
     "computational_domain",
+    "formats",
+    "pipeline",
     "basis_matrix",
     "eval_direct",
     "eval_nufft",

@@ -18,10 +18,20 @@ LIB_PATH = os.path.join(HERE, "libvfnfft.so")
 VFN_OK = 0
 VFN_ERR_INVALID = -1
 VFN_ERR_OUTSIDE = -2
+VFN_ERR_IO = -7
 
 _c_i64_3 = ctypes.c_int64 * 3
 _c_f64_3 = ctypes.c_double * 3
 _vp = ctypes.c_void_p
+_cp = ctypes.c_char_p
+
+
+class SnapshotInfo(ctypes.Structure):
+    """vfn_snapshot_info (include/vfnfft.h): the SFS1 header fields."""
+
+    _fields_ = [("a", ctypes.c_double * 3), ("b", ctypes.c_double * 3),
+                ("shape", ctypes.c_int64 * 3), ("mirror", ctypes.c_int * 3),
+                ("time", ctypes.c_double)]
 
 # name -> (restype, argtypes); mirrors include/vfnfft.h
 SIGNATURES = {
@@ -78,6 +88,42 @@ SIGNATURES = {
     ),
     "vfn_tube_copy": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "vfn_tube_destroy": (ctypes.c_int, [_vp]),
+    "vfn_snapshot_info_read": (ctypes.c_int, [_cp, ctypes.POINTER(SnapshotInfo)]),
+    "vfn_snapshot_read": (
+        ctypes.c_int,
+        [_cp, ctypes.POINTER(SnapshotInfo), _vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _vp],
+    ),
+    "vfn_snapshot_write": (
+        ctypes.c_int, [_cp, ctypes.POINTER(SnapshotInfo), _vp, ctypes.c_int, ctypes.c_int, _vp]
+    ),
+    "vfn_csv_read": (
+        ctypes.c_int,
+        [_cp, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)],
+    ),
+    "vfn_table_name": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(_cp)]),
+    "vfn_table_column": (ctypes.c_int, [_vp, ctypes.c_int, _vp]),
+    "vfn_table_points": (
+        ctypes.c_int, [_vp, ctypes.c_int * 3, _vp, ctypes.c_int, ctypes.c_int, _vp]
+    ),
+    "vfn_table_destroy": (ctypes.c_int, [_vp]),
+    "vfn_csv_write": (
+        ctypes.c_int,
+        [_cp, _vp, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(_cp), ctypes.POINTER(_vp),
+         ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)],
+    ),
+    "vfn_density": (
+        ctypes.c_int, [ctypes.c_int, _vp, ctypes.c_int64, _vp, ctypes.c_int, _vp]
+    ),
+    "vfn_field_write": (
+        ctypes.c_int,
+        [_cp, _cp, _cp, _cp, _cp, _c_i64_3, _vp * 3, _vp, _vp, ctypes.c_int, ctypes.c_double,
+         ctypes.c_int, ctypes.c_int, _vp],
+    ),
+    "vfn_vtk_write": (
+        ctypes.c_int,
+        [_cp, _cp, _c_i64_3, _vp * 3, ctypes.c_int, ctypes.POINTER(_cp), ctypes.POINTER(_vp),
+         ctypes.c_int, ctypes.c_int, _vp],
+    ),
     "vfn_plan_last_timing": (
         ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
     ),
@@ -114,6 +160,8 @@ def check(status: int) -> None:
     msg = load().vfn_last_error().decode(errors="replace")
     if status in (VFN_ERR_INVALID, VFN_ERR_OUTSIDE):
         raise ValueError(msg)
+    if status == VFN_ERR_IO:
+        raise OSError(msg)
     raise VfnError(f"vfnfft error {status}: {msg}")
 
 

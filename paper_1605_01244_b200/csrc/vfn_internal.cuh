@@ -186,4 +186,8 @@ int launch_m6(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t*
               const int32_t* box_start, double2* out, const BinGeom& g, int64_t M,
               cudaStream_t s);
 
+// file-format kernels (vfn_io_kernels.cu)
+int launch_density(const double2* v, int64_t n, double* rho, cudaStream_t s);
+int launch_vtk_pack(const double* in, const int64_t shape[3], uint32_t* out, cudaStream_t s);
+
 }  // namespace vfn

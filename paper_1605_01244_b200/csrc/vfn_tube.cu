@@ -263,7 +263,8 @@ int vfn_tube_eval(vfn_tube** out, int device, const double* values, const int64_
   DevBuf vin, coeffs, rho0, flag, pos, tmp, idxA, idxB, rhoA, rhoB, coords, vals, keys, keys2, iota, perm;
   int st = VFN_OK;
   VFN_CHECK(vin.ensure(sizeof(double2) * n));
-  VFN_CUDA(cudaMemcpyAsync(vin.ptr, values, sizeof(double2) * n, cudaMemcpyHostToDevice, s));
+  // host or device samples (UVA): a snapshot read straight into HBM skips the host
+  VFN_CUDA(cudaMemcpyAsync(vin.ptr, values, sizeof(double2) * n, cudaMemcpyDefault, s));
   int64_t ne = n;
   for (int d = 0; d < 3; ++d) ne *= mirror[d] ? 2 : 1;
   VFN_CHECK(coeffs.ensure(sizeof(double2) * ne));

@@ -23,14 +23,16 @@ import numpy as np
 
 from . import _lib
 from .fourier import DomainBox, SpectralField
-from .nufft import NufftParams, _device_of, _stream_of
+from .nufft import NufftParams, _device_of, _is_cuda_tensor, _stream_of, _torch
 
 __all__ = ["Snapshot", "TubePointCloud", "computational_domain", "snapshot_spectral", "tube_eval"]
 
 
 @dataclass(frozen=True)
 class Snapshot:
-    """Samples on the physical grid plus mirror flags (gpe.py:62-78)."""
+    """Samples on the physical grid plus mirror flags (gpe.py:62-78).
+    ``values`` is a complex128 numpy array or a CUDA tensor (a snapshot file
+    read straight into HBM, formats.read_snapshot(..., device=...))."""
 
     domain: DomainBox
     values: np.ndarray
@@ -39,7 +41,10 @@ class Snapshot:
 
     def __post_init__(self):
         object.__setattr__(self, "mirror", tuple(bool(m) for m in self.mirror))
-        object.__setattr__(self, "values", np.ascontiguousarray(self.values, dtype=np.complex128))
+        if _is_cuda_tensor(self.values):
+            object.__setattr__(self, "values", self.values.to(_torch().complex128).contiguous())
+        else:
+            object.__setattr__(self, "values", np.ascontiguousarray(self.values, dtype=np.complex128))
         if self.values.ndim != 3:
             raise ValueError("snapshot values must be a 3D array")
 
@@ -70,25 +75,37 @@ def computational_domain(domain, mirror) -> DomainBox:
 
 
 def _snap_args(snap):
-    values = np.ascontiguousarray(np.asarray(snap.values), dtype=np.complex128)
+    """(values, on_device, mirror flags): CUDA tensors stay on the device."""
+    if _is_cuda_tensor(snap.values):
+        values = snap.values.to(_torch().complex128).contiguous()
+        on_dev = 1
+    else:
+        values = np.ascontiguousarray(np.asarray(snap.values), dtype=np.complex128)
+        on_dev = 0
     if values.ndim != 3:
         raise ValueError("snapshot values must be a 3D array")
     mirror = (ctypes.c_int * 3)(*[1 if m else 0 for m in snap.mirror])
-    return values, mirror
+    return values, on_dev, mirror
 
 
 def snapshot_spectral(snap) -> SpectralField:
     """Coefficients of the snapshot's mirror-extended field on the
-    computational box (gpe.py:110-113), computed on the device."""
-    values, mirror = _snap_args(snap)
+    computational box (gpe.py:110-113), computed on the device.  Device
+    samples give device coefficients (no host round trip); host samples give
+    host coefficients."""
+    values, on_dev, mirror = _snap_args(snap)
     dom = computational_domain(snap.domain, snap.mirror)
-    shape = tuple(s * (2 if m else 1) for s, m in zip(values.shape, snap.mirror))
-    out = np.empty(shape, dtype=np.complex128)
-    dev = _device_of(None)
+    shape = tuple(int(s) * (2 if m else 1) for s, m in zip(values.shape, snap.mirror))
+    dev = _device_of(values)
+    if on_dev:
+        t = _torch()
+        out = t.empty(shape, dtype=t.complex128, device=values.device)
+    else:
+        out = np.empty(shape, dtype=np.complex128)
     _lib.check(
-        _lib.load().vfn_decompose(dev, values.ctypes.data, _lib.i64x3(values.shape),
+        _lib.load().vfn_decompose(dev, _lib.ptr(values), _lib.i64x3(values.shape),
                                   _lib.f64x3(snap.domain.a), _lib.f64x3(snap.domain.b), mirror,
-                                  out.ctypes.data, 0, _stream_of(dev))
+                                  _lib.ptr(out), on_dev, _stream_of(dev))
     )
     return SpectralField(dom, out)
 
@@ -106,16 +123,16 @@ def tube_eval(snap, thresholds, final_filter: float | None = None,
     if not thresholds or any(t <= 0 for t in thresholds):
         raise ValueError("thresholds must be a nonempty sequence of positive values")
     params = params or NufftParams()
-    values, mirror = _snap_args(snap)
+    values, _, mirror = _snap_args(snap)
     thr = np.asarray(thresholds, dtype=np.float64)
-    dev = _device_of(None)
+    dev = _device_of(values)
     lib = _lib.load()
     handle = ctypes.c_void_p()
     count = ctypes.c_int64(0)
     no_seeds = ctypes.c_int(0)
     ff = float(final_filter) if final_filter is not None else math.nan
     _lib.check(
-        lib.vfn_tube_eval(ctypes.byref(handle), dev, values.ctypes.data, _lib.i64x3(values.shape),
+        lib.vfn_tube_eval(ctypes.byref(handle), dev, _lib.ptr(values), _lib.i64x3(values.shape),
                           _lib.f64x3(snap.domain.a), _lib.f64x3(snap.domain.b), mirror,
                           thr.ctypes.data, len(thresholds), int(final_filter is not None), ff,
                           float(params.oversampling), int(params.cutoff), ctypes.byref(count),
