@@ -62,6 +62,8 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--gather", type=int, default=0, help="0 auto, 1 simple, 2 box/DMMA")
+    p.add_argument("--cutoff", type=int, default=6,
+                   help="window half-width m (BASELINE's metric is quoted at the default 6)")
     return p.parse_args()
 
 
@@ -388,7 +390,7 @@ def run_ours(args):
     for v in plan._n:
         ng *= v
     result["roofline"]["algorithmic_bytes"] = 40 * M + 16 * ng  # points in/out + grid once
-    if tr is not None and world == 1:
+    if tr is not None and world == 1 and CUTOFF == 6:  # the committed capture is m = 6
         result["roofline"]["traffic"] = tr[0]
         result["roofline"]["traffic_source"] = tr[1]
     result["gpu_launches"] = launches_per_step(plan, M) * args.steps
@@ -583,7 +585,9 @@ def run_reference(args):
 
 
 def main():
+    global CUTOFF
     args = parse()
+    CUTOFF = args.cutoff
     if args.impl == "reference":
         run_reference(args)
     elif args.workload == "c4":

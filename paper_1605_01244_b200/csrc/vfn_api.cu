@@ -85,13 +85,14 @@ BinGeom make_geometry(const vfn_plan* p, int bxy) {
   BinGeom g;
   const int K = ((2 * p->m + 1) + 3) / 4 * 4;  // DMMA k-extent
   const int bk = K - 2 * p->m;                  // box depth in cells (2 or 4)
-  const bool m6 = p->m == 6 && p->has_tmap;     // vfn_gather_m6.cu: 4x4x8 tiles, depth-8 boxes
+  const bool tc = tc_supported(p->m) && p->has_tmap;  // vfn_gather_tc.cu: 4x4xTZ tiles, depth-TZ boxes
+  const int tz = tc ? tc_tile_depth(p->m) : bk;
   g.box[0] = bxy;
   g.box[1] = bxy;
-  g.box[2] = m6 ? 8 : bk;
+  g.box[2] = tz;
   g.tile[0] = 4;
   g.tile[1] = 4;
-  g.tile[2] = m6 ? 8 : bk;
+  g.tile[2] = tz;
   for (int d = 0; d < 3; ++d) {
     g.ntile[d] = (int)((p->n[d] + g.tile[d] - 1) / g.tile[d]);
     g.nbox[d] = g.tile[d] / g.box[d];
@@ -154,10 +155,11 @@ int choose_geometry(vfn_plan* p, int64_t M, const double* pts_dev, cudaStream_t 
   if (bxy == 0) {
     const double cells = (double)p->n[0] * (double)p->n[1] * (double)p->n[2];
     bxy = M >= cells ? 1 : 2;
-    if (pts_dev && p->m == 6 && p->has_tmap && M >= (int64_t)1 << 20) {
+    if (pts_dev && tc_supported(p->m) && p->has_tmap && M >= (int64_t)1 << 20) {
+      // 1 x 1 columns once a column's box (TZ cells) holds >= ~32 points
       double rho = 0.0;
       VFN_CHECK(local_density(p, pts_dev, M, s, &rho));
-      bxy = rho >= 32.0 ? 1 : 2;
+      bxy = rho * tc_tile_depth(p->m) / 8.0 >= 32.0 ? 1 : 2;
     }
   }
   *g = make_geometry(p, bxy);
@@ -359,7 +361,7 @@ static int bin_points(vfn_plan* p, const double* points, int64_t M, int on_devic
   *pts_dev = static_cast<const double*>(pdev);
   VFN_CHECK(choose_geometry(p, M, *pts_dev, s, gout));
   const BinGeom& g = *gout;
-  const bool want_u = p->gather_variant != 1 && m6_applicable(p, g);
+  const bool want_u = p->gather_variant != 1 && tc_applicable(p, g);
   VFN_CHECK(p->misc.ensure(64));
   *bad_dev = p->misc.as<int64_t>();
   const int64_t sentinel = INT64_MAX;
@@ -427,7 +429,7 @@ int eval_enqueue(vfn_plan* p, const double* pts_dev, int64_t M, double2* out_dev
   } else {
     VFN_CHECK(choose_geometry(p, M, pts_dev, s, &g));
   }
-  const bool want_u = p->gather_variant != 1 && m6_applicable(p, g);
+  const bool want_u = p->gather_variant != 1 && tc_applicable(p, g);
   VFN_CUDA(cudaMemsetAsync(bad_dev, kBadByte, sizeof(int64_t), s));
   VFN_CHECK(p->keys.ensure(sizeof(uint32_t) * M));
   VFN_CHECK(p->keys_sorted.ensure(sizeof(uint32_t) * M));

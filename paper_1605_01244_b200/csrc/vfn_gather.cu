@@ -305,7 +305,7 @@ int gather_boxes(vfn_plan* p, const double* pts, int64_t M, const BinGeom& g,
                  const uint32_t* keys_sorted, const int32_t* perm, double2* out, cudaStream_t s,
                  bool* used) {
   *used = false;
-  const bool m6 = m6_applicable(p, g);
+  const bool tc = tc_applicable(p, g);
   const int K = 4 * ((2 * p->m + 1 + 3) / 4);
   const int KC = K / 4;
   const int X = g.tile[0] + 2 * p->m, Y = g.tile[1] + 2 * p->m, Z = g.tile[2] + 2 * p->m;
@@ -313,7 +313,7 @@ int gather_boxes(vfn_plan* p, const double* pts, int64_t M, const BinGeom& g,
   while (SZ % 8 != 4) ++SZ;  // odd multiple of 4 complex: conflict-free B fragments
   const int WS = (std::max(g.box[0], g.box[1]) + 2 * p->m + 1) | 1;
   const size_t smem = dmma_smem_bytes(X, Y, SZ, p->m, p->poly.deg, WS);
-  if (!m6 && (smem > 200 * 1024 || g.box[0] + 2 * p->m > kMaxRowW ||
+  if (!tc && (smem > 200 * 1024 || g.box[0] + 2 * p->m > kMaxRowW ||
               g.box[1] + 2 * p->m > kMaxRowW || g.boxes_per_tile > kMaxBoxes || KC > 7 ||
               g.box[2] != K - 2 * p->m))
     return VFN_OK;  // not applicable: caller uses the thread-per-point gather
@@ -335,8 +335,8 @@ int gather_boxes(vfn_plan* p, const double* pts, int64_t M, const BinGeom& g,
   VFN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp2, nitems, ioff, (int)(g.ntiles + 1), s));
   VFN_CHECK(p->sort_tmp.ensure(std::max(tmp, tmp2)));
   VFN_CUDA(cub::DeviceScan::ExclusiveSum(p->sort_tmp.ptr, tmp, counts, bstart, (int)(nb + 1), s));
-  if (m6) {
-    int st = launch_m6(p, p->uvals.as<double>(), perm, keys_sorted, bstart, out, g, M, s);
+  if (tc) {
+    int st = launch_tc(p, p->uvals.as<double>(), perm, keys_sorted, bstart, out, g, M, s);
     if (st == VFN_OK) *used = true;
     return st;
   }

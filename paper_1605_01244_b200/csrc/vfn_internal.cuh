@@ -181,8 +181,10 @@ int rect_eval(int device, const int64_t nmodes[3], const double a[3], const doub
 BinGeom make_geometry(const vfn_plan* p, int bxy);
 int choose_geometry(vfn_plan* p, int64_t M, const double* pts_dev, cudaStream_t s, BinGeom* g);
 int make_grid_tmap(vfn_plan* p);
-bool m6_applicable(const vfn_plan* p, const BinGeom& g);
-int launch_m6(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t* keys_sorted,
+bool tc_supported(int m);      // tensor-core gather covers this cutoff
+int tc_tile_depth(int m);     // its tile / box depth in cells (20 - 2m)
+bool tc_applicable(const vfn_plan* p, const BinGeom& g);
+int launch_tc(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t* keys_sorted,
               const int32_t* box_start, double2* out, const BinGeom& g, int64_t M,
               cudaStream_t s);
 

@@ -61,6 +61,12 @@ def nufft_cases():
         (OFFSET_BOX, (10, 20, 10), 73, 1.6, 6, 200),
         (UNIT_BOX, (12, 12, 12), 81, 2.0, 13, 60),
         (UNIT_BOX, (8, 8, 8), 82, 2.0, 1, 60),
+        # cutoffs the tensor-core gather covers besides m = 6 (eps 1e-8, 1e-10,
+        # a sigma = 1.5 m = 3 plan) and one past it (m = 7, general path)
+        (OFFSET_BOX, (16, 16, 16), 74, 2.0, 4, 300),
+        (OFFSET_BOX, (12, 20, 16), 75, 2.0, 5, 300),
+        (UNIT_BOX, (20, 16, 12), 76, 1.5, 3, 400),
+        (OFFSET_BOX, (8, 24, 12), 77, 2.0, 7, 200),
     ]
     out = {}
     for i, (box, shape, seed, sigma, m, npts) in enumerate(cases):

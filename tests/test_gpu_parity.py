@@ -433,6 +433,40 @@ def test_ragged_grids_many_points(vfb, offset_box, shape, sigma):
         assert l2 < 1e-13 and linf < 1e-13, (bxy, l2, linf)
 
 
+@pytest.mark.parametrize("m", [3, 4, 5])
+def test_tensor_core_gather_other_cutoffs(vfb, offset_box, m):
+    """The tensor-core gather at m = 3, 4, 5 (tiles 4x4x(20-2m)): uniform
+    points plus a dense cluster (boxes with many units, every k-chunk count),
+    at both box widths, against the oracle's gather on the same grid and
+    against the thread-per-point gather."""
+    shape = (18, 22, 26)
+    spec = random_spectral(offset_box, shape, 110 + m)
+    rng = np.random.default_rng(120 + m)
+    a, b = np.array(offset_box.a), np.array(offset_box.b)
+    uni = rng.uniform(a, b, (150000, 3))
+    clu = np.clip(rng.normal((a + b) / 2, 0.01 * (b - a), (50000, 3)), a, np.nextafter(b, a))
+    pts = np.vstack([uni, clu])
+    plan = vfb.NufftPlan(spec, vfb.NufftParams(cutoff=m, eps=0.999))
+    box, tile = plan.geometry(len(pts))
+    assert tile == (4, 4, 20 - 2 * m)
+    sub = np.concatenate([rng.choice(150000, 2500, replace=False), 150000 + rng.choice(50000, 1500, replace=False)])
+    grid, n, beta = O.oversampled_grid(spec.coeffs, offset_box.a, offset_box.b, 2.0, m)
+    ref = O.gather_eval(grid, n, m, beta, pts[sub], offset_box.a, offset_box.b)
+    outs = []
+    for bxy in (1, 2):
+        plan.set_box(bxy)
+        out = plan.evaluate(pts)
+        l2, linf = rel_err(out[sub], ref)
+        assert l2 < 1e-13 and linf < 1e-13, (m, bxy, l2, linf)
+        outs.append(out)
+    plan.set_box(0)
+    plan.set_gather(1)  # thread per point
+    simple = plan.evaluate(pts)
+    for out in outs:
+        l2, linf = rel_err(out, simple)
+        assert l2 < 1e-13 and linf < 1e-13
+
+
 def test_c_abi_from_plain_c(tmp_path):
     """The boundary works without Python: examples/c_api_demo.c links
     libvfnfft.so directly, evaluates against vfn_direct_eval and checks the
