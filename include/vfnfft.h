@@ -135,6 +135,10 @@ int vfn_plan_set_box(vfn_plan* plan, int bxy);
 /* Kernel selection for vfn_plan_eval (benchmarks / A-B tests):
  * 0 = automatic, 1 = simple thread-per-point gather, 2 = DMMA box gather. */
 int vfn_plan_set_gather(vfn_plan* plan, int variant);
+/* CUDA graphs for small evaluates (M <= 2^19, device part): on by default;
+ * a repeated call with the same buffers, M and geometry replays one graph
+ * instead of ~25 launches.  Values are identical either way. */
+int vfn_plan_set_graphs(vfn_plan* plan, int enable);
 
 /* Device time (ms) of the last vfn_plan_eval's gather kernel and of the
  * whole device-side evaluate, measured with CUDA events on its stream. */

@@ -260,6 +260,10 @@ int vfn_plan_destroy(vfn_plan* p) {
     if (p->ev[i]) cudaEventDestroy(p->ev[i]);
   for (int i = 0; i < 2; ++i)
     if (p->copy_stream[i]) cudaStreamDestroy(p->copy_stream[i]);
+  if (p->graph_exec) cudaGraphExecDestroy(p->graph_exec);
+  for (int i = 0; i < 2; ++i)
+    if (p->graph_ev[i]) cudaEventDestroy(p->graph_ev[i]);
+  if (p->graph_stream) cudaStreamDestroy(p->graph_stream);
   delete p;
   return VFN_OK;
 }
@@ -288,6 +292,13 @@ int vfn_plan_geometry(const vfn_plan* p, int64_t M, int box_out[3], int tile_out
 int vfn_plan_set_box(vfn_plan* p, int bxy) {
   if (!p || bxy < 0 || bxy > 2) return fail(VFN_ERR_INVALID, "box must be 0 (auto), 1 or 2");
   p->box_mode = bxy;
+  return VFN_OK;
+}
+
+int vfn_plan_set_graphs(vfn_plan* p, int enable) {
+  if (!p) return fail(VFN_ERR_INVALID, "null plan");
+  p->graphs_on = enable != 0;
+  p->gseen.valid = false;
   return VFN_OK;
 }
 
@@ -446,7 +457,7 @@ int eval_enqueue(vfn_plan* p, const double* pts_dev, int64_t M, double2* out_dev
                         bad_dev, s));
   VFN_CHECK(sort_pairs(p, p->keys.as<uint32_t>(), p->keys_sorted.as<uint32_t>(), p->idx.as<int32_t>(),
                        p->perm.as<int32_t>(), M, key_bits_for(g.nboxes * g.cells_per_box), s));
-  VFN_CUDA(cudaEventRecord(p->ev[1], s));
+  mark_event(p, 1, s);
   bool used = false;
   if (p->gather_variant != 1)
     VFN_CHECK(gather_boxes(p, pts_dev, M, g, p->keys_sorted.as<uint32_t>(), p->perm.as<int32_t>(),
@@ -455,7 +466,7 @@ int eval_enqueue(vfn_plan* p, const double* pts_dev, int64_t M, double2* out_dev
     if (p->gather_variant == 2) return fail(VFN_ERR_INVALID, "box gather unavailable for this plan");
     VFN_CHECK(gather_simple(p, pts_dev, M, p->perm.as<int32_t>(), out_dev, s));
   }
-  VFN_CUDA(cudaEventRecord(p->ev[2], s));
+  mark_event(p, 2, s);
   return VFN_OK;
 }
 
@@ -468,6 +479,83 @@ int outside(int64_t bad, int64_t* first_bad_row) {
 // (caller's stream) -> D2H (second copy stream), double-buffered, so the PCIe
 // transfers of neighbouring chunks overlap the computation (pinned memory
 // makes the copies asynchronous).
+// Small evaluates are launch-bound (~25 kernels + scans for 1e4 points), so
+// their device part runs as one CUDA graph.  A call's key is everything the
+// enqueued work depends on (buffers, M, bin geometry, gather variant); the
+// first call with a new key runs eagerly (and sizes every buffer), the second
+// captures eval_enqueue on the plan's own stream, later ones replay it.
+// Values are bitwise those of the eager path (same kernels, same order).
+constexpr int64_t kGraphMaxM = (int64_t)1 << 19;  // below the density-sampling size
+
+bool same_key(const vfn_plan::GraphKey& a, const vfn_plan::GraphKey& b) {
+  if (!a.valid || !b.valid) return false;
+  for (int d = 0; d < 3; ++d)
+    if (a.box[d] != b.box[d] || a.tile[d] != b.tile[d]) return false;
+  return a.pts == b.pts && a.out == b.out && a.bad == b.bad && a.M == b.M && a.variant == b.variant;
+}
+
+int eval_graphed(vfn_plan* p, const double* pts_dev, int64_t M, double2* out_dev, int64_t* bad_dev,
+                 cudaStream_t s, bool* done) {
+  *done = false;
+  if (!p->graphs_on || M > kGraphMaxM) return VFN_OK;
+  BinGeom g;
+  VFN_CHECK(choose_geometry(p, M, nullptr, s, &g));  // M < 2^20: no sampling, no sync
+  vfn_plan::GraphKey k;
+  k.pts = pts_dev;
+  k.out = out_dev;
+  k.bad = bad_dev;
+  k.M = M;
+  for (int d = 0; d < 3; ++d) {
+    k.box[d] = g.box[d];
+    k.tile[d] = g.tile[d];
+  }
+  k.variant = p->gather_variant;
+  k.valid = true;
+  if (!same_key(k, p->gkey)) {
+    if (!same_key(k, p->gseen)) {
+      p->gseen = k;  // first sighting: eager
+      return VFN_OK;
+    }
+    if (!p->graph_stream) {
+      VFN_CUDA(cudaStreamCreateWithFlags(&p->graph_stream, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) VFN_CUDA(cudaEventCreateWithFlags(&p->graph_ev[i], cudaEventDisableTiming));
+    }
+    if (p->graph_exec) {
+      cudaGraphExecDestroy(p->graph_exec);
+      p->graph_exec = nullptr;
+      p->gkey.valid = false;
+    }
+    VFN_CUDA(cudaStreamBeginCapture(p->graph_stream, cudaStreamCaptureModeThreadLocal));
+    p->capturing = true;
+    const int st = eval_enqueue(p, pts_dev, M, out_dev, bad_dev, p->graph_stream, &g);
+    p->capturing = false;
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(p->graph_stream, &graph);
+    if (st == VFN_OK && e == cudaSuccess) e = cudaGraphInstantiate(&p->graph_exec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    if (st != VFN_OK || e != cudaSuccess) {
+      // not capturable here: evaluate eagerly from now on (same kernels)
+      if (std::getenv("VFN_DEBUG_GRAPH"))
+        fprintf(stderr, "graph capture failed: st=%d (%s) end=%s\n", st, last_error_cstr(), cudaGetErrorString(e));
+      cudaGetLastError();
+      p->graph_exec = nullptr;
+      p->graphs_on = false;
+      return VFN_OK;
+    }
+    p->gkey = k;
+  }
+  // replay after the caller's earlier work on s; s continues after the graph
+  VFN_CUDA(cudaEventRecord(p->graph_ev[0], s));
+  VFN_CUDA(cudaStreamWaitEvent(p->graph_stream, p->graph_ev[0], 0));
+  VFN_CUDA(cudaEventRecord(p->ev[1], p->graph_stream));  // last_timing: the whole graph
+  VFN_CUDA(cudaGraphLaunch(p->graph_exec, p->graph_stream));
+  VFN_CUDA(cudaEventRecord(p->ev[2], p->graph_stream));
+  VFN_CUDA(cudaEventRecord(p->graph_ev[1], p->graph_stream));
+  VFN_CUDA(cudaStreamWaitEvent(s, p->graph_ev[1], 0));
+  *done = true;
+  return VFN_OK;
+}
+
 int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* out,
                         int64_t* first_bad_row, cudaStream_t s) {
   // two chunks measured best at c5 (253 ms vs 347 ms unpipelined, 270 ms with
@@ -525,8 +613,8 @@ int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* ou
   for (auto& x : ev) cudaEventDestroy(x);
   if (st != VFN_OK) return st;
   if (e != cudaSuccess) return fail(VFN_ERR_CUDA, std::string("pipelined evaluate: ") + cudaGetErrorString(e));
-  cudaEventElapsedTime(&p->last_gather_ms, p->ev[1], p->ev[2]);
-  cudaEventElapsedTime(&p->last_total_ms, p->ev[0], p->ev[3]);
+  p->last_gather_ms = elapsed_ms(p->ev[1], p->ev[2]);
+  p->last_total_ms = elapsed_ms(p->ev[0], p->ev[3]);
   for (int64_t i = 0; i < nc; ++i)
     if (bad[i] != kBadSentinel) return outside(i * chunk + bad[i], first_bad_row);
   return VFN_OK;
@@ -556,15 +644,17 @@ int vfn_plan_eval(vfn_plan* p, const double* points, int64_t M, double* out, int
   }
   VFN_CHECK(p->misc.ensure(64));
   int64_t* bad_dev = p->misc.as<int64_t>();
-  VFN_CHECK(eval_enqueue(p, static_cast<const double*>(pdev), M, out_dev, bad_dev, s, nullptr));
+  bool graphed = false;
+  VFN_CHECK(eval_graphed(p, static_cast<const double*>(pdev), M, out_dev, bad_dev, s, &graphed));
+  if (!graphed) VFN_CHECK(eval_enqueue(p, static_cast<const double*>(pdev), M, out_dev, bad_dev, s, nullptr));
   if (!on_device)
     VFN_CUDA(cudaMemcpyAsync(out, out_dev, sizeof(double2) * M, cudaMemcpyDeviceToHost, s));
   int64_t bad = kBadSentinel;
   VFN_CUDA(cudaMemcpyAsync(&bad, bad_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   VFN_CUDA(cudaEventRecord(p->ev[3], s));
   VFN_CUDA(cudaStreamSynchronize(s));
-  cudaEventElapsedTime(&p->last_gather_ms, p->ev[1], p->ev[2]);
-  cudaEventElapsedTime(&p->last_total_ms, p->ev[0], p->ev[3]);
+  p->last_gather_ms = elapsed_ms(p->ev[1], p->ev[2]);
+  p->last_total_ms = elapsed_ms(p->ev[0], p->ev[3]);
   if (bad != kBadSentinel) return outside(bad, first_bad_row);
   return VFN_OK;
 }

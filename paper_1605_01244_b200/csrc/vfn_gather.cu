@@ -371,7 +371,7 @@ int gather_boxes(vfn_plan* p, const double* pts, int64_t M, const BinGeom& g,
   A.Z = Z;
   A.SZ = SZ;
   A.WS = WS;
-  cudaEventRecord(p->ev[1], s);  // gather timing starts here (prep excluded)
+  mark_event(p, 1, s);  // gather timing starts here (prep excluded)
   int st = VFN_OK;
   switch (KC) {
     case 1: st = launch_dmma<1>(A, smem, s); break;

@@ -643,7 +643,7 @@ int launch_tc(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t*
   A.deg = p->poly.deg;
   A.tm = p->map;
   A.g = g;
-  cudaEventRecord(p->ev[1], s);  // gather timing starts here (binning prep excluded)
+  mark_event(p, 1, s);  // gather timing starts here (binning prep excluded)
   switch (p->m) {
     case 3: return launch_m<3>(p, A, g.box[0], s);
     case 4: return launch_m<4>(p, A, g.box[0], s);

@@ -150,6 +150,24 @@ struct vfn_plan {
   vfn::BinGeom last_geom;
   bool has_last_geom = false;
   int64_t iota_len = 0;  // idx[0..iota_len) holds 0, 1, 2, ... (the sort's values)
+  // CUDA graph of the device part of a small evaluate (vfn_api.cu
+  // eval_graphed): captured on the second call with the same key, then
+  // replayed on graph_stream while the key repeats
+  struct GraphKey {
+    const void* pts = nullptr;
+    const void* out = nullptr;
+    const void* bad = nullptr;
+    int64_t M = -1;
+    int box[3] = {0, 0, 0}, tile[3] = {0, 0, 0};
+    int variant = -1;
+    bool valid = false;
+  };
+  GraphKey gkey, gseen;
+  bool graphs_on = true;
+  bool capturing = false;  // timing events are not recorded inside a graph
+  cudaStream_t graph_stream = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  cudaEvent_t graph_ev[2] = {nullptr, nullptr};
 };
 
 namespace vfn {
@@ -187,6 +205,20 @@ bool tc_applicable(const vfn_plan* p, const BinGeom& g);
 int launch_tc(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t* keys_sorted,
               const int32_t* box_start, double2* out, const BinGeom& g, int64_t M,
               cudaStream_t s);
+
+// gather-timing event (vfn_plan_last_timing); skipped while capturing a graph
+inline void mark_event(vfn_plan* p, int i, cudaStream_t s) {
+  if (!p->capturing) cudaEventRecord(p->ev[i], s);
+}
+// elapsed ms between two plan events, 0 (and the error cleared) if unavailable
+inline float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+    cudaGetLastError();
+    ms = 0.f;
+  }
+  return ms;
+}
 
 // file-format kernels (vfn_io_kernels.cu)
 int launch_density(const double2* v, int64_t n, double* rho, cudaStream_t s);

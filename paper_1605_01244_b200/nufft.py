@@ -295,6 +295,11 @@ class NufftPlan:
         """0 = automatic, 1 = thread-per-point gather, 2 = DMMA box gather."""
         _lib.check(_lib.load().vfn_plan_set_gather(self._handle, int(variant)))
 
+    def set_graphs(self, enable: bool) -> None:
+        """Replay small evaluates (M <= 2^19) as one CUDA graph when the call
+        repeats (same buffers, M, geometry); on by default, values identical."""
+        _lib.check(_lib.load().vfn_plan_set_graphs(self._handle, int(bool(enable))))
+
     def set_box(self, bxy: int) -> None:
         """Gather box width: 0 = automatic (by the points' local density), 1 or 2.
         Fix it when results must be bitwise identical across batches/GPU counts."""

@@ -467,6 +467,41 @@ def test_tensor_core_gather_other_cutoffs(vfb, offset_box, m):
         assert l2 < 1e-13 and linf < 1e-13
 
 
+def test_cuda_graph_replay_matches_eager(vfb, offset_box):
+    """Repeated small evaluates replay one CUDA graph (second call captures):
+    values bitwise equal to the eager launches, new point values in the same
+    buffers are picked up, out-of-domain rows still raise, M changes recapture."""
+    import torch
+
+    spec = random_spectral(offset_box, (16, 16, 16), 130)
+    rng = np.random.default_rng(131)
+    a, b = np.array(offset_box.a), np.array(offset_box.b)
+    batches = [rng.uniform(a, b, (5000, 3)) for _ in range(3)]
+    graphed = vfb.NufftPlan(spec)
+    eager = vfb.NufftPlan(spec)
+    eager.set_graphs(False)
+    for i in range(7):
+        p = batches[i % 3]
+        np.testing.assert_array_equal(graphed.evaluate(p), eager.evaluate(p))
+    bad = batches[0].copy()
+    bad[4321] = b + 1.0
+    with pytest.raises(ValueError, match=r"\(row 4321\)"):
+        graphed.evaluate(bad)
+    np.testing.assert_array_equal(graphed.evaluate(batches[1]), eager.evaluate(batches[1]))
+    # device-resident points and output, as bench.py drives it
+    dpts = torch.as_tensor(batches[2], device="cuda")
+    out = torch.empty(5000, dtype=torch.complex128, device="cuda")
+    ref = eager.evaluate(batches[2])
+    for _ in range(4):
+        graphed.evaluate(dpts, out=out)
+        np.testing.assert_array_equal(out.cpu().numpy(), ref)
+    dpts.copy_(torch.as_tensor(batches[0], device="cuda"))
+    graphed.evaluate(dpts, out=out)
+    np.testing.assert_array_equal(out.cpu().numpy(), eager.evaluate(batches[0]))
+    for M in (17, 3000, 17):
+        np.testing.assert_array_equal(graphed.evaluate(batches[0][:M]), eager.evaluate(batches[0][:M]))
+
+
 def test_c_abi_from_plain_c(tmp_path):
     """The boundary works without Python: examples/c_api_demo.c links
     libvfnfft.so directly, evaluates against vfn_direct_eval and checks the
