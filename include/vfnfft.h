@@ -85,7 +85,10 @@ int vfn_plan_create(vfn_plan** out, int device, const int64_t nmodes[3],
 /* Evaluate the series at M points (nufft.py:244-272).
  *   points : M*3 doubles; out : M complex128 in input order.
  *   On VFN_ERR_OUTSIDE *first_bad_row holds the first offending row index
- *   (NaN coordinates count as outside), and `out` is unspecified.         */
+ *   (NaN coordinates count as outside), and `out` is unspecified.
+ *   Any M >= 0 (device memory permitting): one sort + gather handles up to
+ *   2^30 points, larger calls run as batches with one bin geometry; host
+ *   buffers of >= 2^23 points are pipelined (H2D / evaluate / D2H overlap). */
 int vfn_plan_eval(vfn_plan* plan, const double* points, int64_t M, double* out,
                   int on_device, int64_t* first_bad_row, void* stream);
 

@@ -479,6 +479,49 @@ int outside(int64_t bad, int64_t* first_bad_row) {
 // (caller's stream) -> D2H (second copy stream), double-buffered, so the PCIe
 // transfers of neighbouring chunks overlap the computation (pinned memory
 // makes the copies asynchronous).
+// One sort + gather handles at most max_batch() points (32-bit sort values
+// and unit offsets); larger calls run as consecutive batches with the first
+// batch's bin geometry, so every point's value is the one a single call
+// would give it (HBM holds ~3e9 points with their scratch on a B200).
+int64_t max_batch() {
+  int64_t b = (int64_t)1 << 30;
+  if (const char* e = std::getenv("VFN_MAX_BATCH")) b = std::max<int64_t>(1 << 10, std::atoll(e));
+  return b;
+}
+
+int eval_device_batches(vfn_plan* p, const double* points, int64_t M, double* out, int on_device,
+                        int64_t* first_bad_row, cudaStream_t s) {
+  const int64_t bsz = max_batch(), nb = (M + bsz - 1) / bsz;
+  VFN_CUDA(cudaEventRecord(p->ev[0], s));
+  const void* pdev = nullptr;
+  VFN_CHECK(stage_in(p->pts, points, sizeof(double) * 3 * M, on_device, &pdev, s));
+  double2* out_dev = reinterpret_cast<double2*>(out);
+  if (!on_device) {
+    VFN_CHECK(p->out.ensure(sizeof(double2) * M));
+    out_dev = p->out.as<double2>();
+  }
+  VFN_CHECK(p->misc.ensure(sizeof(int64_t) * (nb + 8)));
+  int64_t* bad_dev = p->misc.as<int64_t>();
+  BinGeom g;
+  for (int64_t i = 0; i < nb; ++i) {
+    const int64_t lo = i * bsz, n = std::min(bsz, M - lo);
+    VFN_CHECK(eval_enqueue(p, static_cast<const double*>(pdev) + 3 * lo, n, out_dev + lo, bad_dev + i, s,
+                           i ? &g : nullptr));
+    if (i == 0) g = p->last_geom;
+  }
+  if (!on_device)
+    VFN_CUDA(cudaMemcpyAsync(out, out_dev, sizeof(double2) * M, cudaMemcpyDeviceToHost, s));
+  std::vector<int64_t> bad(nb, kBadSentinel);
+  VFN_CUDA(cudaMemcpyAsync(bad.data(), bad_dev, sizeof(int64_t) * nb, cudaMemcpyDeviceToHost, s));
+  VFN_CUDA(cudaEventRecord(p->ev[3], s));
+  VFN_CUDA(cudaStreamSynchronize(s));
+  p->last_gather_ms = elapsed_ms(p->ev[1], p->ev[2]);
+  p->last_total_ms = elapsed_ms(p->ev[0], p->ev[3]);
+  for (int64_t i = 0; i < nb; ++i)
+    if (bad[i] != kBadSentinel) return outside(i * bsz + bad[i], first_bad_row);
+  return VFN_OK;
+}
+
 // Small evaluates are launch-bound (~25 kernels + scans for 1e4 points), so
 // their device part runs as one CUDA graph.  A call's key is everything the
 // enqueued work depends on (buffers, M, bin geometry, gather variant); the
@@ -560,7 +603,7 @@ int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* ou
                         int64_t* first_bad_row, cudaStream_t s) {
   // two chunks measured best at c5 (253 ms vs 347 ms unpipelined, 270 ms with
   // four: smaller chunks bin more sparsely and repeat the per-call prep)
-  int64_t chunk = std::max<int64_t>((int64_t)1 << 22, (M + 1) / 2);
+  int64_t chunk = std::min(std::max<int64_t>((int64_t)1 << 22, (M + 1) / 2), max_batch());
   if (const char* e = std::getenv("VFN_PIPE_CHUNK")) chunk = std::max<int64_t>(1 << 16, std::atoll(e));
   const int64_t nc = (M + chunk - 1) / chunk;
   for (int i = 0; i < 2; ++i) {
@@ -627,13 +670,14 @@ extern "C" {
 int vfn_plan_eval(vfn_plan* p, const double* points, int64_t M, double* out, int on_device,
                   int64_t* first_bad_row, void* stream) {
   if (!p || (M > 0 && (!points || !out))) return fail(VFN_ERR_INVALID, "null argument");
-  if (M < 0 || M > INT32_MAX) return fail(VFN_ERR_INVALID, "point count out of range");
+  if (M < 0) return fail(VFN_ERR_INVALID, "point count out of range");
   if (first_bad_row) *first_bad_row = -1;
   if (M == 0) return VFN_OK;
   DeviceGuard guard(p->device);
   cudaStream_t s = as_stream(stream);
   if (!on_device && M >= ((int64_t)1 << 23))
     return eval_host_pipelined(p, points, M, out, first_bad_row, s);
+  if (M > max_batch()) return eval_device_batches(p, points, M, out, on_device, first_bad_row, s);
   VFN_CUDA(cudaEventRecord(p->ev[0], s));
   const void* pdev = nullptr;
   VFN_CHECK(stage_in(p->pts, points, sizeof(double) * 3 * M, on_device, &pdev, s));

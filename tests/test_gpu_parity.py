@@ -502,6 +502,35 @@ def test_cuda_graph_replay_matches_eager(vfb, offset_box):
         np.testing.assert_array_equal(graphed.evaluate(batches[0][:M]), eager.evaluate(batches[0][:M]))
 
 
+def test_batched_evaluate_beyond_batch_limit(vfb, offset_box, monkeypatch):
+    """Calls larger than one sort batch (2^30 points; lowered here through
+    VFN_MAX_BATCH) run as consecutive batches with one geometry: bitwise the
+    single-batch values, outside rows reported with their global index, for
+    device, host and pipelined-host inputs."""
+    import torch
+
+    spec = random_spectral(offset_box, (16, 16, 16), 140)
+    rng = np.random.default_rng(141)
+    a, b = np.array(offset_box.a), np.array(offset_box.b)
+    pts = rng.uniform(a, b, (100000, 3))
+    plan = vfb.NufftPlan(spec)
+    plan.set_box(2)
+    ref = plan.evaluate(pts)
+    monkeypatch.setenv("VFN_MAX_BATCH", "30000")
+    np.testing.assert_array_equal(plan.evaluate(pts), ref)
+    dev = plan.evaluate(torch.as_tensor(pts, device="cuda"))
+    np.testing.assert_array_equal(dev.cpu().numpy(), ref)
+    bad = pts.copy()
+    bad[71234] = np.nan
+    with pytest.raises(ValueError, match=r"\(row 71234\)"):
+        plan.evaluate(bad)
+    big = rng.uniform(a, b, (1 << 23, 3))
+    monkeypatch.delenv("VFN_MAX_BATCH")
+    ref_big = plan.evaluate(big)
+    monkeypatch.setenv("VFN_MAX_BATCH", str(1 << 21))
+    np.testing.assert_array_equal(plan.evaluate(big), ref_big)
+
+
 def test_c_abi_from_plain_c(tmp_path):
     """The boundary works without Python: examples/c_api_demo.c links
     libvfnfft.so directly, evaluates against vfn_direct_eval and checks the
