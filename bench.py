@@ -58,7 +58,7 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--workload", choices=["c1", "c2", "c3", "c4", "c5"], default="c5")
+    p.add_argument("--workload", choices=["c1", "c2", "c3", "c4", "c5", "tube"], default="c5")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--gather", type=int, default=0, help="0 auto, 1 simple, 2 box/DMMA")
@@ -512,6 +512,78 @@ def run_rect(args):
     print(json.dumps(result), flush=True)
 
 
+def run_tube(args):
+    """tube_eval (tube.py:58-127) on a synthetic two-vortex
+    snapshot (64^3 samples on [-8,8)^3, mirrored on all axes -> 128^3
+    computational box), thresholds (0.2, 0.05) as the reference's
+    acceptance criterion 7.  One step = one whole call: decompose, plan,
+    seeds, two refinement passes, compaction and sort, cloud to host."""
+    import torch
+
+    import paper_1605_01244_b200 as vfb
+
+    world, rank, local = dist_setup(args)
+    if rank != 0:
+        return
+    dev = torch.device("cuda", local)
+    shape = (64, 64, 64)
+    box = workloads.VORTEX_BOX
+    values = workloads.vortex_pair_field(shape, box)
+    mirror = (True, True, True)
+    thr = [0.2, 0.05]
+    snap = vfb.Snapshot(vfb.DomainBox(*box), values, mirror, 0.0)
+    dsnap = vfb.Snapshot(vfb.DomainBox(*box), torch.as_tensor(values, device=dev), mirror, 0.0)
+    for _ in range(args.warmup):
+        cloud = vfb.tube_eval(dsnap, thr)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cloud = vfb.tube_eval(dsnap, thr)
+    torch.cuda.synchronize()
+    step_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    clk = clocks.stop()
+    t0 = time.perf_counter()
+    host_cloud = vfb.tube_eval(snap, thr)
+    e2e_ms = (time.perf_counter() - t0) * 1e3
+    result = {
+        "metric": "tube_eval wall time (snapshot -> refined low-density cloud)",
+        "value": step_ms,
+        "unit": "ms",
+        "n_gpus": 1,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": step_ms,
+        "higher_is_better": False,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic two-vortex snapshot (workloads.vortex_pair_field)",
+        "config": {"workload": "tube: 64^3 samples on [-8,8)^3, mirror (T,T,T), thresholds (0.2, 0.05), sigma 2, m 6",
+                   "cloud_points": len(cloud)},
+        "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": int(values.nbytes),
+                "d2h_bytes_per_step": int(len(host_cloud) * (24 + 8 + 8))},
+        "roofline": None,
+        "gpu_launches": None,
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline:
+        from oracle import nfft_oracle as O
+
+        t0 = time.perf_counter()
+        rp, rd, rl = O.tube_eval(values, np.array(box[0]), np.array(box[1]), mirror, thr)
+        cpu_s = time.perf_counter() - t0
+        result["cpu_baseline"] = {"value": cpu_s * 1e3, "unit": "ms", "cores": len(os.sched_getaffinity(0)),
+                                  "kind": "port",
+                                  "sample": "one full call of oracle.tube_eval (numpy restatement of tube.py:58-127)"}
+        same = rp.shape == host_cloud.points.shape and np.array_equal(rp, host_cloud.points) and \
+            np.array_equal(rl, host_cloud.level)
+        result["parity_vs_cpu"] = {"points": int(len(rp)), "points_and_levels_identical": bool(same),
+                                   "density_rel_linf": float(np.abs(rd - host_cloud.density).max() / np.abs(rd).max())
+                                   if same and len(rd) else None}
+    print(json.dumps(result), flush=True)
+
+
 def launches_per_step(plan, M: int) -> int:
     """Kernels of ours launched by one evaluate: map+key, the CUB onesweep
     radix sort (1 histogram + one pass per 8 key bits), box offsets and the
@@ -525,6 +597,30 @@ def run_reference(args):
     if rank != 0:
         return
     name = args.workload
+    if name == "tube":
+        from oracle import nfft_oracle as O
+
+        box = workloads.VORTEX_BOX
+        values = workloads.vortex_pair_field((64, 64, 64), box)
+        times = []
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            O.tube_eval(values, np.array(box[0]), np.array(box[1]), (True, True, True), [0.2, 0.05])
+            if i >= args.warmup:
+                times.append(time.perf_counter() - t0)
+        ms = float(np.mean(times)) * 1e3
+        print(json.dumps({
+            "metric": "tube_eval wall time (snapshot -> refined low-density cloud)", "value": ms, "unit": "ms",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic two-vortex snapshot (workloads.vortex_pair_field)",
+            "config": {"workload": "tube: 64^3 samples on [-8,8)^3, mirror (T,T,T), thresholds (0.2, 0.05), sigma 2, m 6"},
+            "impl": "reference",
+            "cpu_baseline": {"value": ms, "unit": "ms", "cores": len(os.sched_getaffinity(0)), "kind": "port",
+                             "sample": "one full call of oracle.tube_eval per step (numpy restatement of tube.py:58-127)"},
+            "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }), flush=True)
+        return
     coeffs = workloads.coefficients(name)
     if name == "c4":
         from oracle import nfft_oracle as O
@@ -592,6 +688,8 @@ def main():
         run_reference(args)
     elif args.workload == "c4":
         run_rect(args)
+    elif args.workload == "tube":
+        run_tube(args)
     else:
         run_ours(args)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1 and args.impl == "ours":

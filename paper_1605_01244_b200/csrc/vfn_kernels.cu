@@ -1,7 +1,11 @@
 // Point mapping / binning (K0+K1), grid build (K2 deconvolve+pad, K3 cuFFT,
 // K3b ghost padding) and the simple thread-per-point gather (K4 v1).
 #include <algorithm>
+#include <array>
+#include <map>
+#include <mutex>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -10,6 +14,62 @@
 #include "vfn_device.cuh"
 
 namespace vfn {
+
+// ------------------------------------------------------------ cuFFT plans
+// Process-wide cache of Z2Z 3D plans keyed by (device, dims): plan creation
+// (and its workspace allocation) costs milliseconds, far more than the
+// transform at the sizes tube_eval / snapshot_spectral / small plans use.
+// One plan's workspace is shared by its executions, so each execution waits
+// on the previous one's completion event (cross-stream safe).
+namespace {
+struct FftEntry {
+  cufftHandle h = 0;
+  cudaEvent_t done = nullptr;
+  uint64_t stamp = 0;
+};
+std::mutex g_fft_mu;
+std::map<std::array<int64_t, 4>, FftEntry> g_fft;
+uint64_t g_fft_clock = 0;
+constexpr size_t kFftCacheMax = 6;
+}  // namespace
+
+int fft_forward(const int64_t n[3], double2* data, cudaStream_t s) {
+  int dev = 0;
+  VFN_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_fft_mu);
+  const std::array<int64_t, 4> key = {dev, n[0], n[1], n[2]};
+  auto it = g_fft.find(key);
+  if (it == g_fft.end()) {
+    if (g_fft.size() >= kFftCacheMax) {  // evict the least recently used plan
+      auto lru = g_fft.begin();
+      for (auto j = g_fft.begin(); j != g_fft.end(); ++j)
+        if (j->second.stamp < lru->second.stamp) lru = j;
+      if (lru->second.done) cudaEventSynchronize(lru->second.done);
+      cufftDestroy(lru->second.h);
+      if (lru->second.done) cudaEventDestroy(lru->second.done);
+      g_fft.erase(lru);
+    }
+    FftEntry e;
+    if (cufftPlan3d(&e.h, (int)n[0], (int)n[1], (int)n[2], CUFFT_Z2Z) != CUFFT_SUCCESS)
+      return fail(VFN_ERR_CUFFT, "cufftPlan3d failed");
+    if (cudaEventCreateWithFlags(&e.done, cudaEventDisableTiming) != cudaSuccess) {
+      cufftDestroy(e.h);
+      return fail(VFN_ERR_CUDA, "fft event creation failed");
+    }
+    it = g_fft.emplace(key, e).first;
+  }
+  FftEntry& e = it->second;
+  e.stamp = ++g_fft_clock;
+  VFN_CUDA(cudaStreamWaitEvent(s, e.done, 0));  // previous use of the workspace
+  cufftResult r = cufftSetStream(e.h, s);
+  if (r == CUFFT_SUCCESS)
+    r = cufftExecZ2Z(e.h, reinterpret_cast<cufftDoubleComplex*>(data), reinterpret_cast<cufftDoubleComplex*>(data),
+                     CUFFT_FORWARD);
+  if (r != CUFFT_SUCCESS) return fail(VFN_ERR_CUFFT, "cuFFT Z2Z forward failed (code " + std::to_string((int)r) + ")");
+  VFN_CUDA(cudaEventRecord(e.done, s));
+  return VFN_OK;
+}
+
 
 // ------------------------------------------------------------------ K0 + K1
 // One pass over the points: domain check (first bad row by atomicMin,
@@ -178,11 +238,8 @@ int build_grid(vfn_plan* p, const double* coeffs_dev, cudaStream_t s) {
 
   double* dfac = nullptr;
   double2* buf = nullptr;
-  cufftHandle plan = 0;
-  bool have_plan = false;
   int status = VFN_OK;
   auto cleanup = [&]() {
-    if (have_plan) cufftDestroy(plan);
     if (buf) cudaFree(buf);
     if (dfac) cudaFree(dfac);
   };
@@ -209,18 +266,14 @@ int build_grid(vfn_plan* p, const double* coeffs_dev, cudaStream_t s) {
     cleanup();
     return fail(VFN_ERR_CUDA, std::string("deconvolve/pad: ") + cudaGetErrorString(e));
   }
-  // K3: unnormalised forward 3D FFT (nufft.py:242)
-  cufftResult r = cufftPlan3d(&plan, (int)n0, (int)n1, (int)n2, CUFFT_Z2Z);
-  if (r == CUFFT_SUCCESS) {
-    have_plan = true;
-    r = cufftSetStream(plan, s);
-  }
-  if (r == CUFFT_SUCCESS)
-    r = cufftExecZ2Z(plan, reinterpret_cast<cufftDoubleComplex*>(buf),
-                     reinterpret_cast<cufftDoubleComplex*>(buf), CUFFT_FORWARD);
-  if (r != CUFFT_SUCCESS) {
-    cleanup();
-    return fail(VFN_ERR_CUFFT, "cuFFT Z2Z forward failed (code " + std::to_string((int)r) + ")");
+  // K3: unnormalised forward 3D FFT (nufft.py:242), cached cuFFT plan
+  {
+    const int64_t nn[3] = {n0, n1, n2};
+    const int fst = fft_forward(nn, buf, s);
+    if (fst != VFN_OK) {
+      cleanup();
+      return fst;
+    }
   }
   // K3b: ghost padding
   const int64_t Ptot = p->P[0] * p->P[1] * p->P[2];

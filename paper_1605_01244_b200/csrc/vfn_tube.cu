@@ -75,21 +75,11 @@ static int spectral_device(const double2* values_dev, const int64_t N[3], const 
   k_mirror<<<grid_blocks(total), 256, 0, s>>>(values_dev, N[0], N[1], N[2], E[0], E[1], E[2],
                                               ext.as<double2>());
   VFN_CUDA(cudaGetLastError());
-  cufftHandle plan;
-  if (cufftPlan3d(&plan, (int)E[0], (int)E[1], (int)E[2], CUFFT_Z2Z) != CUFFT_SUCCESS)
-    return fail(VFN_ERR_CUFFT, "cufftPlan3d failed");
-  cufftResult r = cufftSetStream(plan, s);
-  if (r == CUFFT_SUCCESS)
-    r = cufftExecZ2Z(plan, ext.as<cufftDoubleComplex>(), ext.as<cufftDoubleComplex>(), CUFFT_FORWARD);
-  if (r != CUFFT_SUCCESS) {
-    cufftDestroy(plan);
-    return fail(VFN_ERR_CUFFT, "cuFFT forward failed");
-  }
+  VFN_CHECK(fft_forward(E, ext.as<double2>(), s));  // cached cuFFT plan
   k_shift_scale<<<grid_blocks(total), 256, 0, s>>>(ext.as<double2>(), E[0], E[1], E[2], scale,
                                                    coeffs_dev);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  cufftDestroy(plan);
   ext.release();
   if (e != cudaSuccess) return fail(VFN_ERR_CUDA, std::string("spectral: ") + cudaGetErrorString(e));
   return VFN_OK;

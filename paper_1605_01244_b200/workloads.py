@@ -70,10 +70,10 @@ def _transverse_frame(direction):
     return u1, u2
 
 
-def vortex_pair_spectrum(shape=(128, 128, 128), box=VORTEX_BOX) -> np.ndarray:
-    """Centred coefficients of psi = prod_i tanh(r_i/sqrt2) e^{i theta_i} for a
-    line through (0,0,+1/2) along x and one through (0,0,-1/2) along y,
-    transformed like the reference's decompose (fourier.py:183-188)."""
+def vortex_pair_field(shape=(128, 128, 128), box=VORTEX_BOX) -> np.ndarray:
+    """psi = prod_i tanh(r_i/sqrt2) e^{i theta_i} sampled on the box's grid for a
+    line through (0,0,+1/2) along x and one through (0,0,-1/2) along y
+    (reference frame vortex.py:246-284)."""
     a, b = np.asarray(box[0]), np.asarray(box[1])
     axes = [a[d] + (b[d] - a[d]) * np.arange(shape[d]) / shape[d] for d in range(3)]
     psi = np.ones(shape, dtype=np.complex128)
@@ -83,6 +83,14 @@ def vortex_pair_spectrum(shape=(128, 128, 128), box=VORTEX_BOX) -> np.ndarray:
         s1 = w[0][:, None, None] * u1[0] + w[1][None, :, None] * u1[1] + w[2][None, None, :] * u1[2]
         s2 = w[0][:, None, None] * u2[0] + w[1][None, :, None] * u2[1] + w[2][None, None, :] * u2[2]
         psi *= np.tanh(np.hypot(s1, s2) / np.sqrt(2.0)) * np.exp(1j * np.arctan2(s2, s1))
+    return psi
+
+
+def vortex_pair_spectrum(shape=(128, 128, 128), box=VORTEX_BOX) -> np.ndarray:
+    """Centred coefficients of vortex_pair_field, transformed like the
+    reference's decompose (fourier.py:183-188)."""
+    a, b = np.asarray(box[0]), np.asarray(box[1])
+    psi = vortex_pair_field(shape, box)
     import scipy.fft
 
     scale = float(np.prod(np.sqrt(b - a) / np.asarray(shape)))
