@@ -601,9 +601,12 @@ int eval_graphed(vfn_plan* p, const double* pts_dev, int64_t M, double2* out_dev
 
 int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* out,
                         int64_t* first_bad_row, cudaStream_t s) {
-  // two chunks measured best at c5 (253 ms vs 347 ms unpipelined, 270 ms with
-  // four: smaller chunks bin more sparsely and repeat the per-call prep)
-  int64_t chunk = std::min(std::max<int64_t>((int64_t)1 << 22, (M + 1) / 2), max_batch());
+  // Each chunk's gather re-reads every grid tile its points touch, so small
+  // chunks cost tile traffic (c5, 2^28 points: 2 chunks 254 ms, 3 chunks
+  // 244 ms, 4 chunks 270 ms, 8 chunks 380 ms; unpipelined 347 ms): three
+  // chunks from 2^26 points, else two.
+  const int64_t parts = M >= ((int64_t)1 << 26) ? 3 : 2;
+  int64_t chunk = std::min(std::max<int64_t>((int64_t)1 << 22, (M + parts - 1) / parts), max_batch());
   if (const char* e = std::getenv("VFN_PIPE_CHUNK")) chunk = std::max<int64_t>(1 << 16, std::atoll(e));
   const int64_t nc = (M + chunk - 1) / chunk;
   for (int i = 0; i < 2; ++i) {
