@@ -602,13 +602,55 @@ int eval_graphed(vfn_plan* p, const double* pts_dev, int64_t M, double2* out_dev
 int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* out,
                         int64_t* first_bad_row, cudaStream_t s) {
   // Each chunk's gather re-reads every grid tile its points touch, so small
-  // chunks cost tile traffic (c5, 2^28 points: 2 chunks 254 ms, 3 chunks
-  // 244 ms, 4 chunks 270 ms, 8 chunks 380 ms; unpipelined 347 ms): three
-  // chunks from 2^26 points, else two.
-  const int64_t parts = M >= ((int64_t)1 << 26) ? 3 : 2;
-  int64_t chunk = std::min(std::max<int64_t>((int64_t)1 << 22, (M + parts - 1) / parts), max_batch());
-  if (const char* e = std::getenv("VFN_PIPE_CHUNK")) chunk = std::max<int64_t>(1 << 16, std::atoll(e));
-  const int64_t nc = (M + chunk - 1) / chunk;
+  // chunks cost tile traffic (c5, 2^28 points: 2 equal chunks 254 ms, 3 equal
+  // 244 ms, 4 equal 270 ms, 8 equal 380 ms; unpipelined 347 ms).  From 2^26
+  // points: short first and last chunks (less fill and drain) around two
+  // long ones, 0.12/0.38/0.38/0.12 (238 ms); else two halves.
+  // VFN_PIPE_SPLIT="f0,f1,..." sets the fractions, VFN_PIPE_CHUNK a fixed size.
+  std::vector<double> frac;
+  if (const char* e = std::getenv("VFN_PIPE_SPLIT")) {
+    for (const char* q = e; *q;) {
+      char* end = nullptr;
+      const double f = std::strtod(q, &end);
+      if (end == q) break;
+      if (f > 0) frac.push_back(f);
+      q = *end == ',' ? end + 1 : end;
+    }
+  }
+  if (frac.empty()) {
+    if (M >= ((int64_t)1 << 26))
+      frac = {0.12, 0.38, 0.38, 0.12};
+    else
+      frac = {0.5, 0.5};
+  }
+  std::vector<int64_t> lo_of{0};
+  if (const char* e = std::getenv("VFN_PIPE_CHUNK")) {
+    const int64_t c = std::max<int64_t>(1 << 16, std::atoll(e));
+    for (int64_t x = c; x < M; x += c) lo_of.push_back(x);
+  } else {
+    double tot = 0;
+    for (double f : frac) tot += f;
+    double acc = 0;
+    for (size_t i = 0; i + 1 < frac.size(); ++i) {
+      acc += frac[i];
+      const int64_t b = std::min<int64_t>(M, (int64_t)(acc / tot * (double)M));
+      if (b > lo_of.back()) lo_of.push_back(b);
+    }
+  }
+  // split any chunk above the batch limit
+  {
+    std::vector<int64_t> v{0};
+    lo_of.push_back(M);
+    for (size_t i = 0; i + 1 < lo_of.size(); ++i)
+      for (int64_t x = lo_of[i] + max_batch(); x < lo_of[i + 1]; x += max_batch()) v.push_back(x);
+    for (size_t i = 1; i + 1 < lo_of.size(); ++i) v.push_back(lo_of[i]);
+    std::sort(v.begin(), v.end());
+    v.push_back(M);
+    lo_of = v;
+  }
+  const int64_t nc = (int64_t)lo_of.size() - 1;
+  int64_t chunk = 0;
+  for (int64_t i = 0; i < nc; ++i) chunk = std::max(chunk, lo_of[i + 1] - lo_of[i]);
   for (int i = 0; i < 2; ++i) {
     if (!p->copy_stream[i]) VFN_CUDA(cudaStreamCreateWithFlags(&p->copy_stream[i], cudaStreamNonBlocking));
   }
@@ -627,7 +669,7 @@ int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* ou
   bool have_g = false;
   VFN_CUDA(cudaEventRecord(p->ev[0], s));
   for (int64_t i = 0; i < nc && st == VFN_OK; ++i) {
-    const int64_t lo = i * chunk, n = std::min(chunk, M - lo);
+    const int64_t lo = lo_of[i], n = lo_of[i + 1] - lo;
     double* pbuf = p->pts.as<double>() + 3 * chunk * (i & 1);
     double2* obuf = p->out.as<double2>() + chunk * (i & 1);
     if (i >= 2) cudaStreamWaitEvent(sin, e_comp(i - 2), 0);
@@ -662,7 +704,7 @@ int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* ou
   p->last_gather_ms = elapsed_ms(p->ev[1], p->ev[2]);
   p->last_total_ms = elapsed_ms(p->ev[0], p->ev[3]);
   for (int64_t i = 0; i < nc; ++i)
-    if (bad[i] != kBadSentinel) return outside(i * chunk + bad[i], first_bad_row);
+    if (bad[i] != kBadSentinel) return outside(lo_of[i] + bad[i], first_bad_row);
   return VFN_OK;
 }
 

@@ -1,6 +1,7 @@
 """e2e (pinned host in/out) time of one c5 evaluate for several pipeline
-chunk sizes (VFN_PIPE_CHUNK), device-resident step for reference.
-Usage: python tools/e2e_chunks.py [chunk ...]"""
+schedules, device-resident step for reference.  Each argument is a chunk
+size (VFN_PIPE_CHUNK) or a comma list of chunk fractions (VFN_PIPE_SPLIT).
+Usage: python tools/e2e_chunks.py [134217728 | 0.2,0.6,0.2 ...]"""
 import os
 import sys
 import time
@@ -32,12 +33,17 @@ for _ in range(3):
     plan.evaluate(pts, out=out)
 torch.cuda.synchronize()
 print("device", round((time.perf_counter() - t) / 3 * 1e3, 1), "ms", flush=True)
+ref = None
 for c in sys.argv[1:] or ["134217728", "67108864", "33554432"]:
-    os.environ["VFN_PIPE_CHUNK"] = c
+    os.environ.pop("VFN_PIPE_CHUNK", None)
+    os.environ.pop("VFN_PIPE_SPLIT", None)
+    os.environ["VFN_PIPE_SPLIT" if "," in c else "VFN_PIPE_CHUNK"] = c
     plan.evaluate(pn, out=on)
     ts = []
     for _ in range(3):
         t = time.perf_counter()
         plan.evaluate(pn, out=on)
         ts.append((time.perf_counter() - t) * 1e3)
-    print("chunk", c, "e2e", [round(x, 1) for x in ts], "gather/total ms", plan.last_timing(), flush=True)
+    if ref is None:
+        ref = on.copy()
+    print("schedule", c, "e2e", [round(x, 1) for x in ts], "bitwise", bool(np.array_equal(on, ref)), flush=True)
