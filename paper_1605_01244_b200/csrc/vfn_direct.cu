@@ -1,67 +1,78 @@
 // K6: exact NDFT (nufft.py:129-149) on the device — the reference's
-// eval_direct, O(N1 N2 N3) complex MACs per point.  Thread per point; the
-// per-axis exponentials e_d[k] = exp(2 pi i k t_d), k = j - N_d/2, are formed
-// with sincospi in a per-thread table; the sum runs axis 3 innermost.
+// eval_direct, O(N1 N2 N3) complex MACs per point, as dense products on the
+// FP64 tensor cores.  Per chunk of P points:
+//   E_d[p, j] = exp(2 pi i k_j t_d(p)),  k_j = j - N_d/2,  t = (x - a)/(b - a)
+//   T[p, (k0, k1)] = sum_k2 E_2[p, k2] C[k0, k1, k2]          (cuBLAS ZGEMM)
+//   f[p] = norm * sum_k0 E_0[p, k0] sum_k1 E_1[p, k1] T[p, (k0, k1)]   (warp per point)
+// — the reference's separable basis (nufft.py:141-148) with the axis-3 sum
+// for all points of the chunk done as one ZGEMM.
+#include <cublas_v2.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "vfn_device.cuh"
 
 namespace vfn {
 
-constexpr int kDirectMaxN = 1024;
+// basis rows of the chunk (p < P, all three axes) and the domain check
+__global__ void k_direct_basis(const double* __restrict__ pts, int64_t P, int64_t row0, TorusMap tm,
+                               int N0, int N1, int N2, double2* __restrict__ E0, double2* __restrict__ E1,
+                               double2* __restrict__ E2, unsigned long long* __restrict__ bad) {
+  const int64_t Ns = (int64_t)N0 + N1 + N2;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= P * Ns) return;
+  const int64_t p = e / Ns;
+  int j = (int)(e % Ns), d = 0, N = N0;
+  double2* E = E0;
+  if (j >= N0) {
+    j -= N0;
+    d = 1;
+    N = N1;
+    E = E1;
+    if (j >= N1) {
+      j -= N1;
+      d = 2;
+      N = N2;
+      E = E2;
+    }
+  }
+  const double x = pts[3 * p + d];
+  if (j == 0 && !inside(x, tm.a[d], tm.b[d])) atomicMin(bad, (unsigned long long)(row0 + p));
+  const double t = (x - tm.a[d]) / (tm.b[d] - tm.a[d]);  // nufft.py:143
+  double s, c;
+  sincospi(2.0 * (double)(j - N / 2) * t, &s, &c);       // exp(2 pi i k t), exact argument reduction
+  E[p * N + j] = make_double2(c, s);
+}
 
-__global__ void k_direct(const double2* __restrict__ c, int N0, int N1, int N2,
-                         const double* __restrict__ pts, int64_t M, TorusMap tm, double norm,
-                         double2* __restrict__ out, unsigned long long* __restrict__ bad) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= M) return;
-  double2 e[3][kDirectMaxN / 4];  // chunked below when N_d is larger
-  double t[3];
-  bool ok = true;
-  for (int d = 0; d < 3; ++d) {
-    double x = pts[3 * i + d];
-    ok = ok && inside(x, tm.a[d], tm.b[d]);
-    t[d] = (x - tm.a[d]) / (tm.b[d] - tm.a[d]);
-  }
-  if (!ok) {
-    atomicMin(bad, (unsigned long long)i);
-    return;
-  }
-  const int Nd[3] = {N0, N1, N2};
-  // tables for axes 0 and 1 (<= 256 entries each in registers/local memory);
-  // axis 2 phases are rebuilt per chunk
-  for (int d = 0; d < 2; ++d)
-    for (int j = 0; j < Nd[d] && j < kDirectMaxN / 4; ++j) {
-      double s, co;
-      sincospi(2.0 * (double)(j - Nd[d] / 2) * t[d], &s, &co);
-      e[d][j] = make_double2(co, s);
-    }
+// warp per point: f = norm * sum_k0 E0[k0] sum_k1 E1[k1] T[k0, k1]
+__global__ void k_direct_reduce(const double2* __restrict__ T, const double2* __restrict__ E0,
+                                const double2* __restrict__ E1, int64_t P, int N0, int N1, double norm,
+                                double2* __restrict__ out) {
+  const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (p >= P) return;
+  const double2* t = T + p * (int64_t)N0 * N1;
   double ar = 0.0, ai = 0.0;
-  for (int j0 = 0; j0 < N0; ++j0) {
-    double2 e0;
-    if (j0 < kDirectMaxN / 4) e0 = e[0][j0];
-    else { double s, co; sincospi(2.0 * (double)(j0 - N0 / 2) * t[0], &s, &co); e0 = make_double2(co, s); }
+  for (int k0 = 0; k0 < N0; ++k0) {
     double br = 0.0, bi = 0.0;
-    for (int j1 = 0; j1 < N1; ++j1) {
-      double2 e1;
-      if (j1 < kDirectMaxN / 4) e1 = e[1][j1];
-      else { double s, co; sincospi(2.0 * (double)(j1 - N1 / 2) * t[1], &s, &co); e1 = make_double2(co, s); }
-      const double2* row = c + ((int64_t)j0 * N1 + j1) * N2;
-      double cr = 0.0, ci = 0.0;
-      for (int j2 = 0; j2 < N2; ++j2) {
-        double s, co;
-        sincospi(2.0 * (double)(j2 - N2 / 2) * t[2], &s, &co);
-        double2 v = row[j2];
-        cr += v.x * co - v.y * s;
-        ci += v.x * s + v.y * co;
-      }
-      br += e1.x * cr - e1.y * ci;
-      bi += e1.x * ci + e1.y * cr;
+    for (int k1 = lane; k1 < N1; k1 += 32) {
+      const double2 e = E1[p * N1 + k1], v = t[(int64_t)k0 * N1 + k1];
+      br = fma(e.x, v.x, fma(-e.y, v.y, br));
+      bi = fma(e.x, v.y, fma(e.y, v.x, bi));
     }
-    ar += e0.x * br - e0.y * bi;
-    ai += e0.x * bi + e0.y * br;
+    const double2 e0 = E0[p * N0 + k0];
+    ar = fma(e0.x, br, fma(-e0.y, bi, ar));
+    ai = fma(e0.x, bi, fma(e0.y, br, ai));
   }
-  out[i] = make_double2(ar * norm, ai * norm);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ar += __shfl_xor_sync(0xffffffffu, ar, o);
+    ai += __shfl_xor_sync(0xffffffffu, ai, o);
+  }
+  if (lane == 0) out[p] = make_double2(ar * norm, ai * norm);
 }
 
 }  // namespace vfn
@@ -76,12 +87,14 @@ extern "C" int vfn_direct_eval(int device, const int64_t nm[3], const double a[3
     return fail(VFN_ERR_INVALID, "null argument");
   if (first_bad_row) *first_bad_row = -1;
   for (int d = 0; d < 3; ++d)
-    if (nm[d] <= 0 || nm[d] % 2 != 0 || nm[d] > kDirectMaxN)
-      return fail(VFN_ERR_INVALID, "direct sum needs even mode counts in 2..1024");
+    if (nm[d] <= 0 || nm[d] % 2 != 0 || nm[d] > (1 << 20))
+      return fail(VFN_ERR_INVALID, "direct sum needs even, positive mode counts");
   if (M < 0) return fail(VFN_ERR_INVALID, "negative point count");
   if (M == 0) return VFN_OK;
   DeviceGuard guard(device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cublasHandle_t h = static_cast<cublasHandle_t>(blas_handle(device));
+  if (!h) return fail(VFN_ERR_CUBLAS, "cublasCreate failed");
   TorusMap tm;
   double vol = 1.0;
   for (int d = 0; d < 3; ++d) {
@@ -90,33 +103,70 @@ extern "C" int vfn_direct_eval(int device, const int64_t nm[3], const double a[3
     tm.amb[d] = a[d] - b[d];
     vol *= b[d] - a[d];
   }
-  const size_t cb = sizeof(double2) * nm[0] * nm[1] * nm[2];
-  DevBuf C, P, O, B;
+  const int N0 = (int)nm[0], N1 = (int)nm[1], N2 = (int)nm[2];
+  const int64_t N01 = (int64_t)N0 * N1;
+  const size_t cb = sizeof(double2) * N01 * N2;
+  // chunk so the intermediate T (P x N0 N1 complex) stays near 1 GB
+  const int64_t P = std::max<int64_t>(1, std::min<int64_t>(M, ((int64_t)1 << 26) / N01));
+  // grow-only scratch per device, reused across calls (one host thread at a
+  // time, like rect_eval): a 0.5-1 GB intermediate is not reallocated per call
+  struct Scratch {
+    DevBuf C, Pt, O, B, E, T;
+  };
+  static std::mutex smu;
+  static std::map<int, Scratch*> scratch;
+  Scratch* sc;
+  {
+    std::lock_guard<std::mutex> lock(smu);
+    Scratch*& slot = scratch[device];
+    if (!slot) slot = new Scratch();
+    sc = slot;
+  }
+  DevBuf &C = sc->C, &Pt = sc->Pt, &O = sc->O, &B = sc->B, &E = sc->E, &T = sc->T;
   const double2* cd = reinterpret_cast<const double2*>(coeffs);
   const double* pd = points;
   double2* od = reinterpret_cast<double2*>(out);
   if (!on_device) {
     VFN_CHECK(C.ensure(cb));
-    VFN_CHECK(P.ensure(sizeof(double) * 3 * M));
+    VFN_CHECK(Pt.ensure(sizeof(double) * 3 * M));
     VFN_CHECK(O.ensure(sizeof(double2) * M));
     VFN_CUDA(cudaMemcpyAsync(C.ptr, coeffs, cb, cudaMemcpyHostToDevice, s));
-    VFN_CUDA(cudaMemcpyAsync(P.ptr, points, sizeof(double) * 3 * M, cudaMemcpyHostToDevice, s));
+    VFN_CUDA(cudaMemcpyAsync(Pt.ptr, points, sizeof(double) * 3 * M, cudaMemcpyHostToDevice, s));
     cd = C.as<double2>();
-    pd = P.as<double>();
+    pd = Pt.as<double>();
     od = O.as<double2>();
   }
   VFN_CHECK(B.ensure(sizeof(unsigned long long)));
+  VFN_CHECK(E.ensure(sizeof(double2) * P * ((int64_t)N0 + N1 + N2)));
+  VFN_CHECK(T.ensure(sizeof(double2) * P * N01));
   const unsigned long long sentinel = ~0ull;
   VFN_CUDA(cudaMemcpyAsync(B.ptr, &sentinel, sizeof(sentinel), cudaMemcpyHostToDevice, s));
-  k_direct<<<(unsigned)((M + 63) / 64), 64, 0, s>>>(cd, (int)nm[0], (int)nm[1], (int)nm[2], pd, M,
-                                                   tm, 1.0 / std::sqrt(vol), od,
-                                                   B.as<unsigned long long>());
-  VFN_CUDA(cudaGetLastError());
+  if (cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) return fail(VFN_ERR_CUBLAS, "cublasSetStream failed");
+  const double norm = 1.0 / std::sqrt(vol);
+  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+  for (int64_t lo = 0; lo < M; lo += P) {
+    const int64_t n = std::min(P, M - lo);
+    double2* E0 = E.as<double2>();
+    double2* E1 = E0 + n * N0;
+    double2* E2 = E1 + n * N1;
+    const int64_t nb = n * ((int64_t)N0 + N1 + N2);
+    k_direct_basis<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(pd + 3 * lo, n, lo, tm, N0, N1, N2, E0, E1, E2,
+                                                                B.as<unsigned long long>());
+    VFN_CUDA(cudaGetLastError());
+    // column-major: T (N0N1 x n) = C^T (N0N1 x N2) * E2 (N2 x n); C is (N2 x N0N1) col-major
+    const cublasStatus_t r =
+        cublasZgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)N01, (int)n, N2, &one,
+                    reinterpret_cast<const cuDoubleComplex*>(cd), N2, reinterpret_cast<const cuDoubleComplex*>(E2),
+                    N2, &zero, T.as<cuDoubleComplex>(), (int)N01);
+    if (r != CUBLAS_STATUS_SUCCESS) return fail(VFN_ERR_CUBLAS, "cublasZgemm failed (" + std::to_string((int)r) + ")");
+    k_direct_reduce<<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(T.as<double2>(), E0, E1, n, N0, N1, norm,
+                                                                      od + lo);
+    VFN_CUDA(cudaGetLastError());
+  }
   if (!on_device) VFN_CUDA(cudaMemcpyAsync(out, od, sizeof(double2) * M, cudaMemcpyDeviceToHost, s));
   unsigned long long bad = sentinel;
   VFN_CUDA(cudaMemcpyAsync(&bad, B.ptr, sizeof(bad), cudaMemcpyDeviceToHost, s));
   VFN_CUDA(cudaStreamSynchronize(s));
-  C.release(); P.release(); O.release(); B.release();
   if (bad != sentinel) {
     if (first_bad_row) *first_bad_row = (int64_t)bad;
     return fail(VFN_ERR_OUTSIDE, "point (row " + std::to_string(bad) + ") lies outside the domain");

@@ -26,7 +26,7 @@ __global__ void k_basis(const double* __restrict__ y, int64_t M, int64_t N, doub
   E[e] = make_double2(c * r, s * r);
 }
 
-static cublasHandle_t handle_for(int device) {
+cublasHandle_t handle_for(int device) {
   static std::mutex mu;
   static std::map<int, cublasHandle_t> handles;
   std::lock_guard<std::mutex> lock(mu);
@@ -38,6 +38,8 @@ static cublasHandle_t handle_for(int device) {
   handles[device] = h;
   return h;
 }
+
+void* blas_handle(int device) { return handle_for(device); }
 
 #define VFN_BLAS(expr)                                                                        \
   do {                                                                                        \
