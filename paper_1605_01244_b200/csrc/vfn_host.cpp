@@ -5,6 +5,10 @@
 #include <cstdlib>
 #include <string>
 #include <vector>
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "vfn_internal.cuh"
 
@@ -76,7 +80,7 @@ static long double phi(long double v, int m, long double beta, long double i0b) 
 // c = j - m, converted to monomials in delta (Horner-evaluated on the GPU).
 // The degree is the smallest one whose max error on a dense check grid is
 // below 4e-15 (phi <= 1; a few ulp of Horner rounding), capped at max_deg.
-int fit_window_poly(int m, double beta, double* coef, int max_deg) {
+static int fit_window_poly_uncached(int m, double beta, double* coef, int max_deg) {
   const long double i0b = i0l(beta);
   const int W = 2 * m + 1;
   int chosen = max_deg;
@@ -138,6 +142,33 @@ int fit_window_poly(int m, double beta, double* coef, int max_deg) {
   }
   for (size_t i = 0; i < best.size(); ++i) coef[i] = (double)best[i];
   return chosen;
+}
+
+// The fit costs milliseconds of long-double work and depends only on
+// (m, beta, max_deg): cached process-wide, so repeated plans (tube_eval, a
+// plan per snapshot) skip it.
+int fit_window_poly(int m, double beta, double* coef, int max_deg) {
+  struct Fit {
+    int deg;
+    std::vector<double> coef;
+  };
+  static std::mutex mu;
+  static std::map<std::tuple<int, double, int>, Fit> cache;
+  const auto key = std::make_tuple(m, beta, max_deg);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      std::copy(it->second.coef.begin(), it->second.coef.end(), coef);
+      return it->second.deg;
+    }
+  }
+  Fit f;
+  f.deg = fit_window_poly_uncached(m, beta, coef, max_deg);
+  f.coef.assign(coef, coef + (size_t)(2 * m + 1) * (f.deg + 1));
+  std::lock_guard<std::mutex> lock(mu);
+  cache.emplace(key, std::move(f));
+  return cache.find(key)->second.deg;
 }
 
 }  // namespace vfn

@@ -142,6 +142,8 @@ struct vfn_plan {
   int box_mode = 0;          // 0 auto, 1 or 2: gather box width in cells (vfn_plan_set_box)
   CUtensorMap tmap;        // TMA view of `grid` for the m = 6 gather
   bool has_tmap = false;
+  vfn::DevBuf fftbuf, dfacbuf;  // grid-build scratch (fftbuf kept only if keep_fftbuf)
+  bool keep_fftbuf = false;
   // evaluate scratch (grow-only)
   vfn::DevBuf pts, out, uvals, keys, keys_sorted, idx, perm, sort_tmp, box_start, items, units, uscratch, misc;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};

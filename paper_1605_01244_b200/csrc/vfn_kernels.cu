@@ -236,21 +236,18 @@ int build_grid(vfn_plan* p, const double* coeffs_dev, cudaStream_t s) {
   const double vol = (p->b[0] - p->a[0]) * (p->b[1] - p->a[1]) * (p->b[2] - p->a[2]);
   const double scale = 1.0 / std::sqrt(vol) / ((double)n0 * (double)n1 * (double)n2);
 
-  double* dfac = nullptr;
-  double2* buf = nullptr;
+  // scratch: the FFT buffer is kept by plans that are rebuilt in place
+  // (keep_fftbuf, tube_eval's cached plan), else released at the end
   int status = VFN_OK;
   auto cleanup = [&]() {
-    if (buf) cudaFree(buf);
-    if (dfac) cudaFree(dfac);
+    if (!p->keep_fftbuf) p->fftbuf.release();
   };
   const int64_t total = n0 * n1 * n2;
-  cudaError_t e = cudaMalloc(&dfac, sizeof(double) * (N0 + N1 + N2));
-  if (e == cudaSuccess) e = cudaMalloc(&buf, sizeof(double2) * total);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    cleanup();
-    return fail(VFN_ERR_NOMEM, std::string("grid allocation failed: ") + cudaGetErrorString(e));
-  }
+  VFN_CHECK(p->dfacbuf.ensure(sizeof(double) * (N0 + N1 + N2)));
+  VFN_CHECK(p->fftbuf.ensure(sizeof(double2) * total));
+  double* dfac = p->dfacbuf.as<double>();
+  double2* buf = p->fftbuf.as<double2>();
+  cudaError_t e = cudaSuccess;
   std::vector<double> h(N0 + N1 + N2);
   std::copy(fac[0].begin(), fac[0].end(), h.begin());
   std::copy(fac[1].begin(), fac[1].end(), h.begin() + N0);
@@ -277,12 +274,14 @@ int build_grid(vfn_plan* p, const double* coeffs_dev, cudaStream_t s) {
   }
   // K3b: ghost padding
   const int64_t Ptot = p->P[0] * p->P[1] * p->P[2];
-  e = cudaMalloc(&p->grid, sizeof(double2) * Ptot);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    p->grid = nullptr;
-    cleanup();
-    return fail(VFN_ERR_NOMEM, std::string("padded grid allocation failed: ") + cudaGetErrorString(e));
+  if (!p->grid) {  // a rebuild keeps the plan's grid (and its tensor map)
+    e = cudaMalloc(&p->grid, sizeof(double2) * Ptot);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      p->grid = nullptr;
+      cleanup();
+      return fail(VFN_ERR_NOMEM, std::string("padded grid allocation failed: ") + cudaGetErrorString(e));
+    }
   }
   k_halo<<<grid_blocks(Ptot), 256, 0, s>>>(buf, n0, n1, n2, p->grid, p->P[0], p->P[1], p->P[2],
                                            p->m);

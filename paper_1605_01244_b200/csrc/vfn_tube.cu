@@ -12,6 +12,8 @@
 #include <cub/device/device_scan.cuh>
 
 #include <cmath>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -23,7 +25,13 @@ struct vfn_tube {
   vfn::DevBuf points, density, level;
 };
 
+#include <chrono>
 namespace vfn {
+static double tube_now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+#define TUBE_T(tag) do { if (dbg) { cudaStreamSynchronize(s); double t_ = tube_now_ms(); fprintf(stderr, "tube %-12s %8.2f ms\n", tag, t_ - t_last); t_last = t_; } } while (0)
+
 
 // ------------------------------------------------------------------ spectral
 
@@ -205,6 +213,25 @@ using namespace vfn;
 
 extern "C" {
 
+namespace {
+struct TubeScratch {
+  std::mutex mu;
+  vfn::DevBuf vin, coeffs, rho0, flag, pos, tmp, idxA, idxB, rhoA, rhoB, coords, vals, keys, keys2, iota, perm;
+  vfn_plan* plan = nullptr;
+  int64_t E[3] = {0, 0, 0};
+  double a[3] = {0, 0, 0}, bx[3] = {0, 0, 0}, sigma = 0;
+  int m = 0;
+};
+TubeScratch* tube_scratch(int device) {
+  static std::mutex mu;
+  static std::map<int, TubeScratch*> all;
+  std::lock_guard<std::mutex> lock(mu);
+  TubeScratch*& t = all[device];
+  if (!t) t = new TubeScratch();
+  return t;
+}
+}  // namespace
+
 int vfn_decompose(int device, const double* values, const int64_t shape[3], const double a[3],
                   const double b[3], const int mirror[3], double* coeffs_out, int on_device,
                   void* stream) {
@@ -249,8 +276,17 @@ int vfn_tube_eval(vfn_tube** out, int device, const double* values, const int64_
   *no_seeds = 0;
   DeviceGuard guard(device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const bool dbg = std::getenv("VFN_DEBUG_TUBE") != nullptr;
+  double t_last = tube_now_ms();
   const int64_t n = shape[0] * shape[1] * shape[2];
-  DevBuf vin, coeffs, rho0, flag, pos, tmp, idxA, idxB, rhoA, rhoB, coords, vals, keys, keys2, iota, perm;
+  // per-device scratch and plan, reused across calls (calls on one device
+  // are serialised by its mutex): no allocation churn after the first call
+  TubeScratch* ts = tube_scratch(device);
+  std::lock_guard<std::mutex> tube_lock(ts->mu);
+  DevBuf &vin = ts->vin, &coeffs = ts->coeffs, &rho0 = ts->rho0, &flag = ts->flag, &pos = ts->pos,
+         &tmp = ts->tmp, &idxA = ts->idxA, &idxB = ts->idxB, &rhoA = ts->rhoA, &rhoB = ts->rhoB,
+         &coords = ts->coords, &vals = ts->vals, &keys = ts->keys, &keys2 = ts->keys2, &iota = ts->iota,
+         &perm = ts->perm;
   int st = VFN_OK;
   VFN_CHECK(vin.ensure(sizeof(double2) * n));
   // host or device samples (UVA): a snapshot read straight into HBM skips the host
@@ -260,7 +296,9 @@ int vfn_tube_eval(vfn_tube** out, int device, const double* values, const int64_
   VFN_CHECK(coeffs.ensure(sizeof(double2) * ne));
   int64_t E[3];
   double bx[3];
+  TUBE_T("upload");
   VFN_CHECK(spectral_device(vin.as<double2>(), shape, a, b, mirror, coeffs.as<double2>(), E, bx, s));
+  TUBE_T("spectral");
 
   // lattice at the finest spacing h / 3^L (tube.py:82-83); step like numpy: widths / lattice
   int64_t mult = 1;
@@ -291,9 +329,28 @@ int vfn_tube_eval(vfn_tube** out, int device, const double* values, const int64_
                                          shape[2], mult, idxA.as<longlong4>(), rhoA.as<double>());
   VFN_CUDA(cudaGetLastError());
 
-  vfn_plan* plan = nullptr;
-  VFN_CHECK(vfn_plan_create(&plan, device, E, a, bx, sigma, m, coeffs.as<double>(), 1, stream));
-  coeffs.release();
+  TUBE_T("seeds");
+  // the plan of the previous call is rebuilt in place when its geometry
+  // matches (grid, tensor map, evaluate scratch and FFT buffer reused)
+  bool same = ts->plan && ts->sigma == sigma && ts->m == m;
+  for (int d = 0; d < 3 && same; ++d) same = ts->E[d] == E[d] && ts->a[d] == a[d] && ts->bx[d] == bx[d];
+  if (same) {
+    VFN_CHECK(build_grid(ts->plan, coeffs.as<double>(), s));
+  } else {
+    if (ts->plan) vfn_plan_destroy(ts->plan);
+    ts->plan = nullptr;
+    VFN_CHECK(vfn_plan_create(&ts->plan, device, E, a, bx, sigma, m, coeffs.as<double>(), 1, stream));
+    ts->plan->keep_fftbuf = true;
+    ts->sigma = sigma;
+    ts->m = m;
+    for (int d = 0; d < 3; ++d) {
+      ts->E[d] = E[d];
+      ts->a[d] = a[d];
+      ts->bx[d] = bx[d];
+    }
+  }
+  vfn_plan* plan = ts->plan;
+  TUBE_T("plan");
   int64_t cur = P;  // points of the current generation (idxA, rhoA)
   bool emptied = false;
   for (int ell = 1; ell <= nthr && st == VFN_OK; ++ell) {
@@ -325,8 +382,9 @@ int vfn_tube_eval(vfn_tube** out, int device, const double* values, const int64_
     if (st != VFN_OK) break;
     k_rho<<<nblk(nk), 256, 0, s>>>(vals.as<double2>(), nk, rhoA.as<double>());
     cur = nk;
+    TUBE_T("pass");
   }
-  vfn_plan_destroy(plan);
+  TUBE_T("passes done");
   if (st != VFN_OK) return st;
   vfn_tube* t = new vfn_tube();
   t->device = device;
@@ -377,6 +435,7 @@ int vfn_tube_eval(vfn_tube** out, int device, const double* values, const int64_
                                    t->level.as<int64_t>());
   VFN_CUDA(cudaGetLastError());
   VFN_CUDA(cudaStreamSynchronize(s));
+  TUBE_T("sort+emit");
   t->count = cur;
   *count = cur;
   *out = t;
