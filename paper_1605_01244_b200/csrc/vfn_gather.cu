@@ -1,8 +1,11 @@
-// K4 v2: binned gather on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64).
+// K4 v2: the general binned gather on the FP64 tensor cores (DMMA,
+// mma.sync m8n8k4 f64) for the cutoffs the tensor-core gather of
+// vfn_gather_tc.cu does not cover (m = 1, 2, 7..13) and for planes without
+// TMA; the box counts / offsets built here feed both.
 //
 // Points arrive sorted by gather box: a box is bi x bj x bk
-// cells, bk = K - 2m with K = 4*KC the DMMA k-extent (16 at m = 6, so boxes
-// are 4 cells deep).  A "unit" is up to 8 points of one box.  For a unit, the
+// cells, bk = K - 2m with K = 4*KC the DMMA k-extent (16 at m = 7, so boxes
+// are 1 cell deep).  A "unit" is up to 8 points of one box.  For a unit, the
 // innermost contraction of the reference (axis 3, nufft.py:269) becomes a
 // dense product
 //     S[p, r] = sum_k  W2[p, k] * G[r, k]          p < 8 points, k < K,
