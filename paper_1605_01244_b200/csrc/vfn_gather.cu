@@ -5,7 +5,7 @@
 //
 // Points arrive sorted by gather box: a box is bi x bj x bk
 // cells, bk = K - 2m with K = 4*KC the DMMA k-extent (16 at m = 7, so boxes
-// are 1 cell deep).  A "unit" is up to 8 points of one box.  For a unit, the
+// are 2 cells deep).  A "unit" is up to 8 points of one box.  For a unit, the
 // innermost contraction of the reference (axis 3, nufft.py:269) becomes a
 // dense product
 //     S[p, r] = sum_k  W2[p, k] * G[r, k]          p < 8 points, k < K,
