@@ -87,11 +87,13 @@ BinGeom make_geometry(const vfn_plan* p, int bxy) {
   const int bk = K - 2 * p->m;                  // box depth in cells (2 or 4)
   const bool tc = tc_supported(p->m) && p->has_tmap;  // vfn_gather_tc.cu: 4x4xTZ tiles, depth-TZ boxes
   const int tz = tc ? tc_tile_depth(p->m) : bk;
+  int tx = 4, ty = 4;
+  if (tc) tc_tile_xy(p->m, &tx, &ty);
   g.box[0] = bxy;
   g.box[1] = bxy;
   g.box[2] = tz;
-  g.tile[0] = 4;
-  g.tile[1] = 4;
+  g.tile[0] = tx;
+  g.tile[1] = ty;
   g.tile[2] = tz;
   for (int d = 0; d < 3; ++d) {
     g.ntile[d] = (int)((p->n[d] + g.tile[d] - 1) / g.tile[d]);

@@ -1,10 +1,10 @@
-// K4 for cutoffs m = 3..6 (nufft.py:56 default m = 6; NufftParams.for_accuracy
-// nufft.py:67-73 gives m = 3..5 for eps = 1e-6..1e-10): binned gather on the
+// K4 for cutoffs m = 3..7 (nufft.py:56 default m = 6; NufftParams.for_accuracy
+// nufft.py:67-73 gives m = 3..7 for eps = 1e-6..1e-14): binned gather on the
 // FP64 tensor cores (DMMA, mma.sync.m8n8k4.f64), TMA-staged, double-buffered.
 // One template over the cutoff MC and the box width BXY.
 //
-// Geometry.  Tiles of 4 x 4 x TZ cells with TZ = 20 - 2m (8 at m = 6); their
-// (4+2m) x (4+2m) x 20 complex block of the ghost-padded grid (80 KB at
+// Geometry.  Tiles of 4 x 4 x TZ cells (4 x 2 x 6 at m = 7) with TZ = 20 - 2m
+// (8 at m = 6); their (4+2m) x (4+2m) x 20 complex block of the ghost-padded grid (80 KB at
 // m = 6) is one TMA copy (cp.async.bulk.tensor.3d) of the grid viewed as
 // doubles.  z-lines are always 20 complex = 320 B (= 64 B mod 128 B), so the
 // 8 rows x 4 depths a DMMA pair reads hit both bank halves evenly
@@ -49,14 +49,20 @@ constexpr int kXO = 1, kXS = 17;          // axes 1, 2 weight tables: j in [-1, 
 
 template <int MC>
 struct Cfg {
-  static_assert(MC >= 3 && MC <= 6, "tensor-core gather covers m = 3..6");
+  static_assert(MC >= 3 && MC <= 7, "tensor-core gather covers m = 3..7");
   static constexpr int W = 2 * MC + 1;            // stencil width
   static constexpr int TZ = kSZ - 2 * MC;         // tile / box depth in cells
-  static constexpr int SXY = 4 + 2 * MC;          // staged x, y extent
-  static constexpr int kTileBytes = SXY * SXY * kLine;
+  // tile x, y extents in cells: 4 x 4, and 4 x 2 at m = 7 so that two
+  // staged tiles still fit next to the weight tables
+  static constexpr int TX = 4, TY = MC == 7 ? 2 : 4;
+  static constexpr int SX = TX + 2 * MC, SY = TY + 2 * MC;  // staged x, y extents
+  static constexpr int kTileBytes = SX * SY * kLine;
   static constexpr int KCmin = (W + 3) / 4;       // fewest k-chunks a unit can use
-  // axis-3 weight table (A fragments): entry kAO + j holds phi_j, j in [-TZ, 21)
-  static constexpr int kAO = TZ, kAS = (TZ + 21) | 1;
+  // A fragments from a per-warp axis-3 table (entry kAO + j holds phi_j,
+  // j in [-TZ, 21)), or at m = 7 straight from the weight DMMA's registers
+  // by quad shuffles (no table: its shared memory holds the larger tiles)
+  static constexpr bool kShflA = MC == 7;
+  static constexpr int kAO = TZ, kAS = kShflA ? 0 : (TZ + 21) | 1;
   static constexpr int kWarpW = kUnitPts * (kAS + 2 * kXS);
 };
 
@@ -68,6 +74,7 @@ size_t smem_bytes(int mc) {
     case 3: return f(Cfg<3>::kTileBytes, Cfg<3>::kWarpW);
     case 4: return f(Cfg<4>::kTileBytes, Cfg<4>::kWarpW);
     case 5: return f(Cfg<5>::kTileBytes, Cfg<5>::kWarpW);
+    case 7: return f(Cfg<7>::kTileBytes, Cfg<7>::kWarpW);
     default: return f(Cfg<6>::kTileBytes, Cfg<6>::kWarpW);
   }
 }
@@ -139,7 +146,7 @@ __device__ __forceinline__ void issue_tile(const CUtensorMap* map, const Args& A
   const int t0 = tile / (G.ntile[2] * G.ntile[1]);
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // prior generic reads of dst
   mbar_expect_tx(bar, Cfg<MC>::kTileBytes);
-  tma_load_3d(dst, map, 2 * t2 * Cfg<MC>::TZ, t1 * 4, t0 * 4, bar);
+  tma_load_3d(dst, map, 2 * t2 * Cfg<MC>::TZ, t1 * Cfg<MC>::TY, t0 * Cfg<MC>::TX, bar);
 }
 
 // One 8-row DMMA tile: C_re/im[p, n] for the lane's B row at `addr`.
@@ -191,12 +198,12 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
                                             int4 desc, const UnitPoints& up, int lane) {
   using C = Cfg<MC>;
   constexpr int XB = BXY + 2 * MC, YB = BXY + 2 * MC;  // box footprint rows per axis
-  constexpr int NB = 4 / BXY;                          // boxes per tile along x and y
+  constexpr int NBY = C::TY / BXY;                     // boxes per tile along y
   constexpr int kAO = C::kAO, kAS = C::kAS;
   const int g = lane >> 2, tig = lane & 3;
   const int cnt = desc.y & 15, kz = desc.y >> 8;
-  const int bt = desc.z - tile * (NB * NB);
-  const int X0 = (bt / NB) * BXY, Y0 = (bt % NB) * BXY;
+  const int bt = desc.z - tile * ((C::TX / BXY) * NBY);
+  const int X0 = (bt / NBY) * BXY, Y0 = (bt % NBY) * BXY;
 
   const bool valid = g < cnt;
   const int64_t prow = up.prow;
@@ -214,9 +221,10 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
   // 4 k-chunks of 4 powers (the fits have degree 12..14 for m <= 8), 8
   // stencil columns per n-block
   constexpr int NBW = (C::W + 7) / 8;
-  double* wA = wt;                              // [8][kAS]  axis 3
+  double* wA = wt;                              // [8][kAS]  axis 3 (absent with kShflA)
   double* wX = wt + kUnitPts * kAS;             // [8][kXS]  axis 1
   double* wY = wX + kUnitPts * kXS;             // [8][kXS]  axis 2
+  double z00 = 0.0, z01 = 0.0, z10 = 0.0, z11 = 0.0;  // axis-3 weights in registers (kShflA)
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     const double x1 = dl[d], x2 = x1 * x1, x4 = x2 * x2;
@@ -229,6 +237,13 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
       if (NBW > 1) dmma(w10, w11, pw, c.y);
       pw *= x4;
     }
+    if (C::kShflA && d == 2) {
+      z00 = w00;
+      z01 = w01;
+      z10 = w10;
+      z11 = w11;
+      continue;
+    }
     double* row = d == 2 ? wA + g * kAS + kAO : (d == 0 ? wX : wY) + g * kXS + kXO;
     row[2 * tig] = w00;      // j = 2 tig, 2 tig + 1, 8 + 2 tig, 9 + 2 tig;
     row[2 * tig + 1] = w01;  // j >= W come out exactly 0 (zero coefficients)
@@ -240,24 +255,38 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
   __syncwarp();
   // A fragments: axis-3 weights of point g at staged depth kz + 4 kc + tig
   double a[KC];
-  const double* wa = wA + g * kAS + kAO + kz + tig - ck;
+  if constexpr (C::kShflA) {
+    // phi_j of point g sits in lane 4g + (j mod 8)/2, register (j / 8, j mod 2)
 #pragma unroll
-  for (int kc = 0; kc < KC; ++kc) a[kc] = inbox ? wa[4 * kc] : 0.0;
+    for (int kc = 0; kc < KC; ++kc) {
+      const int j = kz + 4 * kc + tig - ck;
+      const int src = 4 * g + ((j & 7) >> 1);
+      const double v00 = __shfl_sync(0xffffffffu, z00, src), v01 = __shfl_sync(0xffffffffu, z01, src);
+      const double v10 = __shfl_sync(0xffffffffu, z10, src), v11 = __shfl_sync(0xffffffffu, z11, src);
+      const double v = (j & 8) ? ((j & 1) ? v11 : v10) : ((j & 1) ? v01 : v00);
+      a[kc] = (inbox && j >= 0 && j < 16) ? v : 0.0;
+    }
+  } else {
+    const double* wa = wA + g * kAS + kAO + kz + tig - ck;
+#pragma unroll
+    for (int kc = 0; kc < KC; ++kc) a[kc] = inbox ? wa[4 * kc] : 0.0;
+  }
   const double* wx = wX + g * kXS + kXO - ci;  // wx[x], x in [0, 16); zero off the stencil
   const double* wy = wY + g * kXS + kXO - cj;  // wy[y]
 
-  const unsigned base = tile_s + (unsigned)((kz + tig) * 16 + (X0 * C::SXY + Y0) * kLine);
-  constexpr unsigned kX = C::SXY * kLine;  // x stride
+  const unsigned base = tile_s + (unsigned)((kz + tig) * 16 + (X0 * C::SY + Y0) * kLine);
+  constexpr unsigned kX = C::SY * kLine;  // x stride
   // parts of the YB rows: one R8 run per 8 rows, then R4 / R2 / R1 for the rest
   constexpr int Y8 = YB / 8;
   constexpr int R4 = (YB - 8 * Y8) >= 4;
   constexpr int R2 = (YB - 8 * Y8 - 4 * R4) >= 2;
   constexpr int R1 = (YB - 8 * Y8 - 4 * R4 - 2 * R2);
-  static_assert(Y8 <= 1 && R1 <= 1, "row schedule");
+  static_assert(Y8 <= 2 && R1 <= 1, "row schedule");
   double acc_re = 0.0, acc_im = 0.0;
-  if constexpr (Y8 == 1) {
+#pragma unroll
+  for (int y8 = 0; y8 < Y8; ++y8) {
     double t0r = 0.0, t1r = 0.0, t0i = 0.0, t1i = 0.0;
-    const unsigned ba = base + g * kLine;
+    const unsigned ba = base + (8 * y8 + g) * kLine;
 #pragma unroll
     for (int x = 0; x < XB; ++x) {
       double cr0, cr1, ci0_, ci1_;
@@ -268,7 +297,7 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
       t0i = fma(w, ci0_, t0i);
       t1i = fma(w, ci1_, t1i);
     }
-    const double wy0 = wy[2 * tig], wy1 = wy[2 * tig + 1];
+    const double wy0 = wy[8 * y8 + 2 * tig], wy1 = wy[8 * y8 + 2 * tig + 1];
     acc_re = fma(wy0, t0r, fma(wy1, t1r, acc_re));
     acc_im = fma(wy0, t0i, fma(wy1, t1i, acc_im));
   }
@@ -461,7 +490,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     // until the buffer's load for item kk has been issued
     while (*reinterpret_cast<volatile int*>(&loaded[b]) != kk) __nanosleep(64);
     mbar_wait(bar_s + 8 * b, (kk >> 1) & 1);
-    dispatch_unit<MC, BXY>(A, scb, wt, tile_s, tile, t0 * 4, t1 * 4, t2 * C::TZ, desc, up, lane);
+    dispatch_unit<MC, BXY>(A, scb, wt, tile_s, tile, t0 * C::TX, t1 * C::TY, t2 * C::TZ, desc, up, lane);
     if (lane == 0) {
       if (atomicAdd(&done[b], 1) == item.z - item.y - 1) {  // last unit of item kk
         done[b] = 0;
@@ -539,7 +568,12 @@ __global__ void k_tc_items(const int32_t* __restrict__ uoff, const int32_t* __re
     items[first + j] = make_int4((int)t, u0 + j * tc::kItemUnits, min(u1, u0 + (j + 1) * tc::kItemUnits), 0);
 }
 
-bool tc_supported(int m) { return m >= 3 && m <= 6; }
+bool tc_supported(int m) { return m >= 3 && m <= 7; }
+
+void tc_tile_xy(int m, int* tx, int* ty) {
+  *tx = 4;
+  *ty = m == 7 ? 2 : 4;
+}
 
 int tc_tile_depth(int m) { return tc::kSZ - 2 * m; }
 
@@ -558,10 +592,11 @@ int make_grid_tmap(vfn_plan* p) {
   using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                           CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-  const cuuint32_t sxy = (cuuint32_t)(4 + 2 * p->m);
+  int tx, ty;
+  tc_tile_xy(p->m, &tx, &ty);
   cuuint64_t dims[3] = {(cuuint64_t)(2 * p->P[2]), (cuuint64_t)p->P[1], (cuuint64_t)p->P[0]};
   cuuint64_t strides[2] = {(cuuint64_t)(2 * p->P[2] * 8), (cuuint64_t)(2 * p->P[2] * 8 * p->P[1])};
-  cuuint32_t box[3] = {2 * tc::kSZ, sxy, sxy};
+  cuuint32_t box[3] = {2 * tc::kSZ, (cuuint32_t)(ty + 2 * p->m), (cuuint32_t)(tx + 2 * p->m)};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = reinterpret_cast<Fn>(fn)(&p->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, p->grid, dims,
                                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -575,7 +610,9 @@ int make_grid_tmap(vfn_plan* p) {
 bool tc_applicable(const vfn_plan* p, const BinGeom& g) {
   if (!tc_supported(p->m) || !p->has_tmap || p->poly.deg > 15) return false;
   const int tz = tc_tile_depth(p->m);
-  return g.tile[0] == 4 && g.tile[1] == 4 && g.tile[2] == tz && g.box[2] == tz && g.box[0] == g.box[1] &&
+  int tx, ty;
+  tc_tile_xy(p->m, &tx, &ty);
+  return g.tile[0] == tx && g.tile[1] == ty && g.tile[2] == tz && g.box[2] == tz && g.box[0] == g.box[1] &&
          (g.box[0] == 1 || g.box[0] == 2);
 }
 
@@ -648,6 +685,7 @@ int launch_tc(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t*
     case 3: return launch_m<3>(p, A, g.box[0], s);
     case 4: return launch_m<4>(p, A, g.box[0], s);
     case 5: return launch_m<5>(p, A, g.box[0], s);
+    case 7: return launch_m<7>(p, A, g.box[0], s);
     default: return launch_m<6>(p, A, g.box[0], s);
   }
 }

@@ -207,6 +207,7 @@ int choose_geometry(vfn_plan* p, int64_t M, const double* pts_dev, cudaStream_t 
 int make_grid_tmap(vfn_plan* p);
 bool tc_supported(int m);      // tensor-core gather covers this cutoff
 int tc_tile_depth(int m);     // its tile / box depth in cells (20 - 2m)
+void tc_tile_xy(int m, int* tx, int* ty);  // its tile x, y extents in cells
 bool tc_applicable(const vfn_plan* p, const BinGeom& g);
 int launch_tc(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t* keys_sorted,
               const int32_t* box_start, double2* out, const BinGeom& g, int64_t M,
