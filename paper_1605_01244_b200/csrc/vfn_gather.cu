@@ -1,6 +1,6 @@
 // K4 v2: the general binned gather on the FP64 tensor cores (DMMA,
 // mma.sync m8n8k4 f64) for the cutoffs the tensor-core gather of
-// vfn_gather_tc.cu does not cover (m = 1, 2, 7..13) and for planes without
+// vfn_gather_tc.cu does not cover (m = 1, 8..13) and for planes without
 // TMA; the box counts / offsets built here feed both.
 //
 // Points arrive sorted by gather box: a box is bi x bj x bk

@@ -1,5 +1,5 @@
-// K4 for cutoffs m = 3..7 (nufft.py:56 default m = 6; NufftParams.for_accuracy
-// nufft.py:67-73 gives m = 3..7 for eps = 1e-6..1e-14): binned gather on the
+// K4 for cutoffs m = 2..7 (nufft.py:56 default m = 6; NufftParams.for_accuracy
+// nufft.py:67-73 gives m = 2..7 for eps = 1e-4..1e-14): binned gather on the
 // FP64 tensor cores (DMMA, mma.sync.m8n8k4.f64), TMA-staged, double-buffered.
 // One template over the cutoff MC and the box width BXY.
 //
@@ -49,7 +49,7 @@ constexpr int kXO = 1, kXS = 17;          // axes 1, 2 weight tables: j in [-1, 
 
 template <int MC>
 struct Cfg {
-  static_assert(MC >= 3 && MC <= 7, "tensor-core gather covers m = 3..7");
+  static_assert(MC >= 2 && MC <= 7, "tensor-core gather covers m = 2..7");
   static constexpr int W = 2 * MC + 1;            // stencil width
   static constexpr int TZ = kSZ - 2 * MC;         // tile / box depth in cells
   // tile x, y extents in cells: 4 x 4, and 4 x 2 at m = 7 so that two
@@ -71,6 +71,7 @@ size_t smem_bytes(int mc) {
     return (size_t)1024 + 2 * (size_t)tile + 48 + sizeof(double) * ((size_t)kWarps * warpw + 32 * 8);
   };
   switch (mc) {
+    case 2: return f(Cfg<2>::kTileBytes, Cfg<2>::kWarpW);
     case 3: return f(Cfg<3>::kTileBytes, Cfg<3>::kWarpW);
     case 4: return f(Cfg<4>::kTileBytes, Cfg<4>::kWarpW);
     case 5: return f(Cfg<5>::kTileBytes, Cfg<5>::kWarpW);
@@ -568,7 +569,7 @@ __global__ void k_tc_items(const int32_t* __restrict__ uoff, const int32_t* __re
     items[first + j] = make_int4((int)t, u0 + j * tc::kItemUnits, min(u1, u0 + (j + 1) * tc::kItemUnits), 0);
 }
 
-bool tc_supported(int m) { return m >= 3 && m <= 7; }
+bool tc_supported(int m) { return m >= 2 && m <= 7; }
 
 void tc_tile_xy(int m, int* tx, int* ty) {
   *tx = 4;
@@ -682,6 +683,7 @@ int launch_tc(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t*
   A.g = g;
   mark_event(p, 1, s);  // gather timing starts here (binning prep excluded)
   switch (p->m) {
+    case 2: return launch_m<2>(p, A, g.box[0], s);
     case 3: return launch_m<3>(p, A, g.box[0], s);
     case 4: return launch_m<4>(p, A, g.box[0], s);
     case 5: return launch_m<5>(p, A, g.box[0], s);

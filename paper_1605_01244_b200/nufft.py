@@ -366,7 +366,7 @@ class NufftPlan:
         nkeys *= box[0] * box[1] * box[2]
         bits = max(1, int(nkeys - 1).bit_length())
         sort = 2 + 2 * -(-bits // 8)
-        if 3 <= self.params.cutoff <= 7 and tile[2] == 20 - 2 * self.params.cutoff:
+        if 2 <= self.params.cutoff <= 7 and tile[2] == 20 - 2 * self.params.cutoff:
             prep = 1 + 2 + (1 + 2 + 1) + (1 + 2 + 1)  # box counts+scan, units+scan+write, items
         else:
             prep = 1 + 2 + 1 + 2 + 1                  # box counts+scan, tile units+scan, items

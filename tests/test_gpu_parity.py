@@ -433,9 +433,9 @@ def test_ragged_grids_many_points(vfb, offset_box, shape, sigma):
         assert l2 < 1e-13 and linf < 1e-13, (bxy, l2, linf)
 
 
-@pytest.mark.parametrize("m", [3, 4, 5, 7])
+@pytest.mark.parametrize("m", [2, 3, 4, 5, 7])
 def test_tensor_core_gather_other_cutoffs(vfb, offset_box, m):
-    """The tensor-core gather at m = 3, 4, 5, 7 (tiles 4x4x(20-2m), 4x2x6 at m = 7): uniform
+    """The tensor-core gather at m = 2, 3, 4, 5, 7 (tiles 4x4x(20-2m), 4x2x6 at m = 7): uniform
     points plus a dense cluster (boxes with many units, every k-chunk count),
     at both box widths, against the oracle's gather on the same grid and
     against the thread-per-point gather."""
