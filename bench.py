@@ -19,9 +19,13 @@ pad, 3D FFT) is built once per rank and reported separately.
 * ``cpu_baseline`` — the oracle port of the reference (oracle/nfft_oracle.py,
                 numpy, fork-sharded over all host cores) on a bounded sample.
 
-Multi-GPU (torchrun): rank 0 builds the coefficients and NCCL-broadcasts them;
-every rank builds its own replicated plan and evaluates a contiguous 1/N shard
-of the points (no data-path collective).  Timing is the max over ranks.
+Multi-GPU (torchrun): rank 0 builds the coefficients and NCCL-broadcasts them
+(the path's one exchange); every rank builds its own replicated plan and
+evaluates its block of points with no data-path collective.  The path splits
+into independent point blocks, so the default is weak scaling (each rank a
+full workload-sized block, ``value`` = all ranks' points / max-over-ranks
+time); ``--scaling strong`` splits one point set across the ranks instead.
+At N=1 both are the same run.
 """
 
 from __future__ import annotations
@@ -62,22 +66,29 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--gather", type=int, default=0, help="0 auto, 1 simple, 2 box/DMMA")
+    p.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                   help="weak: every rank evaluates its own full point set (the path shards into "
+                        "independent point blocks); strong: one point set split across the ranks")
     p.add_argument("--cutoff", type=int, default=6,
                    help="window half-width m (BASELINE's metric is quoted at the default 6)")
     return p.parse_args()
 
 
-def workload_config(name: str, n_gpus: int) -> dict:
+def workload_config(name: str, n_gpus: int, scaling: str = "weak") -> dict:
     w = workloads.WORKLOADS[name]
+    per_gpu = w.npoints if scaling == "weak" else -(-w.npoints // n_gpus)
     return {
         "workload": f"{name}: N={w.modes[0]}^3 complex128 coefficients, M={w.npoints} "
         f"{'Gaussian-cloud' if w.kind == 'cluster' else 'uniform'} points on "
         f"{list(w.box[0])}..{list(w.box[1])}, sigma={SIGMA}, m={CUTOFF}",
         "modes": list(w.modes),
-        "points": w.npoints,
+        "points": w.npoints * (n_gpus if scaling == "weak" else 1),
+        "points_per_gpu": per_gpu,
         "sigma": SIGMA,
         "m": CUTOFF,
-        "parallelism": f"points sharded over {n_gpus} GPU(s), oversampled grid replicated",
+        "parallelism": (f"{n_gpus} GPU(s), each evaluating its own {w.npoints}-point block (weak scaling); "
+                        if scaling == "weak" else f"{w.npoints} points split over {n_gpus} GPU(s); ")
+        + "coefficients NCCL-broadcast from rank 0, oversampled grid replicated",
         "l2_flush": "none needed: per-step inputs (points) exceed the 126 MB L2"
         if w.npoints * 24 > 2 * 126e6
         else "inputs smaller than L2 (warm-L2 number)",
@@ -285,8 +296,9 @@ def run_ours(args):
     if args.gather:
         plan.set_gather(args.gather)
 
-    # this rank's shard of the points, resident in HBM
-    lo, hi = shard_range(w.npoints, world, rank)
+    # this rank's block of points, resident in HBM: a whole workload-sized
+    # block per rank (weak) or a 1/world slice of one point set (strong)
+    lo, hi = shard_range(w.npoints, world, rank) if args.scaling == "strong" else (0, w.npoints)
     M = hi - lo
     if name == "c5":
         gen = torch.Generator(device=dev)
@@ -343,7 +355,7 @@ def run_ours(args):
         _lib.check(_lib.load().vfn_bench_fp64_peak(dev.index or 0, 0.5, ctypes.byref(tf), ctypes.byref(mhz)))
         peak = tf.value
 
-    total_points = w.npoints
+    total_points = w.npoints * (world if args.scaling == "weak" else 1)
     value = total_points / (step_ms * 1e-3)
     if rank != 0:
         return
@@ -358,11 +370,11 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": step_ms,
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic, seeded (SURVEY 8d recipe); no dataset exists for this benchmark",
-        "config": workload_config(name, world),
+        "config": workload_config(name, world, args.scaling),
         "e2e": {
             "value": total_points / (e2e_step * 1e-3),
             "unit": "points/s",
@@ -673,11 +685,11 @@ def run_reference(args):
         "warmup": args.warmup,
         "ms_per_step": float(np.mean([r["seconds"] for r in runs]) * 1e3),
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic, seeded (SURVEY 8d recipe)",
-        "config": workload_config(name, world),
+        "config": workload_config(name, world, args.scaling),
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
