@@ -319,6 +319,8 @@ class NufftPlan:
         is a caller-owned complex128 buffer of length M on the same side as
         ``points`` (e.g. pinned host memory), written in place and returned."""
         pts, on_dev, M = _points_arg(points)
+        if M and chunk == 0:  # the reference's chunk loop is range(0, M, chunk)
+            raise ValueError("range() arg 3 must not be zero")
         if out is None:
             out = _empty_like_points(pts, on_dev, M)
         else:
