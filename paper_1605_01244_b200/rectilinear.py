@@ -6,7 +6,6 @@ host helper and its argument checks (rectilinear.py:22-44), which
 
 from __future__ import annotations
 
-import ctypes
 
 import numpy as np
 
