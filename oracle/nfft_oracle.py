@@ -18,7 +18,6 @@ to /root/reference/pkg/src/vortexfourier/.
 
 from __future__ import annotations
 
-
 import numpy as np
 import scipy.fft
 

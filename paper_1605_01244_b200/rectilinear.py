@@ -6,7 +6,6 @@ host helper and its argument checks (rectilinear.py:22-44), which
 
 from __future__ import annotations
 
-
 import numpy as np
 
 from . import _lib
