@@ -154,13 +154,15 @@ int choose_geometry(vfn_plan* p, int64_t M, const double* pts_dev, cudaStream_t 
     const char* fb = std::getenv("VFN_BOX_XY");  // experiment override
     if (fb) bxy = std::atoi(fb) == 1 ? 1 : 2;
   }
+  const double cells = (double)p->n[0] * (double)p->n[1] * (double)p->n[2];
+  p->col_density = 8.0 * (double)M / cells;  // mean; the sample below sees clustering
   if (bxy == 0) {
-    const double cells = (double)p->n[0] * (double)p->n[1] * (double)p->n[2];
     bxy = M >= cells ? 1 : 2;
     if (pts_dev && tc_supported(p->m) && p->has_tmap && M >= (int64_t)1 << 20) {
       // 1 x 1 columns once a column's box (TZ cells) holds >= ~32 points
       double rho = 0.0;
       VFN_CHECK(local_density(p, pts_dev, M, s, &rho));
+      p->col_density = std::max(p->col_density, rho);
       bxy = rho * tc_tile_depth(p->m) / 8.0 >= 32.0 ? 1 : 2;
     }
   }

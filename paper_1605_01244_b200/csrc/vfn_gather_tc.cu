@@ -41,7 +41,10 @@ namespace vfn {
 namespace tc {
 
 constexpr int kUnitPts = 8;
-constexpr int kWarps = 16;
+// warps per CTA: 16 (128 registers each) keep the FP64 pipe fullest on
+// dense tiles; sparse tiles (< ~8 points per 1x1x8 column, e.g. 1e6 points on
+// 128^3) have too few units per staged tile for 16 warps and run 12
+constexpr int kWarpsDense = 16, kWarpsSparse = 12;
 constexpr int kSZ = 20;                   // staged z extent (TZ + 2m)
 constexpr int kLine = kSZ * 16;           // bytes per staged (x, y) line
 constexpr int kItemUnits = 48;            // units per work item
@@ -66,9 +69,9 @@ struct Cfg {
   static constexpr int kWarpW = kUnitPts * (kAS + 2 * kXS);
 };
 
-size_t smem_bytes(int mc) {
-  auto f = [](int tile, int warpw) {
-    return (size_t)1024 + 2 * (size_t)tile + 48 + sizeof(double) * ((size_t)kWarps * warpw + 32 * 8);
+size_t smem_bytes(int mc, int nw) {
+  auto f = [nw](int tile, int warpw) {
+    return (size_t)1024 + 2 * (size_t)tile + 48 + sizeof(double) * ((size_t)nw * warpw + 32 * 8);
   };
   switch (mc) {
     case 2: return f(Cfg<2>::kTileBytes, Cfg<2>::kWarpW);
@@ -378,7 +381,7 @@ __device__ __forceinline__ void dispatch_unit(const Args& A, const double* scb, 
   gather_unit<MC, BXY, 5>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane);
 }
 
-template <int MC, int BXY>
+template <int MC, int BXY, int kWarps>
 __global__ void __launch_bounds__(kWarps * 32, 1)
     k_gather_tc(const __grid_constant__ CUtensorMap tmap, const Args A) {
   using C = Cfg<MC>;
@@ -617,22 +620,25 @@ bool tc_applicable(const vfn_plan* p, const BinGeom& g) {
          (g.box[0] == 1 || g.box[0] == 2);
 }
 
-template <int MC, int BXY>
+template <int MC, int BXY, int NW>
 static int launch(vfn_plan* p, const tc::Args& A, cudaStream_t s) {
-  const size_t smem = tc::smem_bytes(MC);
-  VFN_CUDA(cudaFuncSetAttribute(tc::k_gather_tc<MC, BXY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem = tc::smem_bytes(MC, NW);
+  VFN_CUDA(cudaFuncSetAttribute(tc::k_gather_tc<MC, BXY, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  tc::k_gather_tc<MC, BXY><<<nsm, tc::kWarps * 32, smem, s>>>(p->tmap, A);
+  tc::k_gather_tc<MC, BXY, NW><<<nsm, NW * 32, smem, s>>>(p->tmap, A);
   VFN_CUDA(cudaGetLastError());
   return VFN_OK;
 }
 
 template <int MC>
 static int launch_m(vfn_plan* p, const tc::Args& A, int bxy, cudaStream_t s) {
-  return bxy == 1 ? launch<MC, 1>(p, A, s) : launch<MC, 2>(p, A, s);
+  const bool sparse = p->col_density < 8.0;  // points per 1x1x8 column (choose_geometry)
+  if (bxy == 1)
+    return sparse ? launch<MC, 1, tc::kWarpsSparse>(p, A, s) : launch<MC, 1, tc::kWarpsDense>(p, A, s);
+  return sparse ? launch<MC, 2, tc::kWarpsSparse>(p, A, s) : launch<MC, 2, tc::kWarpsDense>(p, A, s);
 }
 
 // Build units and items from the box offsets, then run the tensor-core gather.
