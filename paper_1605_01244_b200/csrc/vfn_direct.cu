@@ -111,6 +111,7 @@ extern "C" int vfn_direct_eval(int device, const int64_t nm[3], const double a[3
   // grow-only scratch per device, reused across calls (one host thread at a
   // time, like rect_eval): a 0.5-1 GB intermediate is not reallocated per call
   struct Scratch {
+    std::mutex mu;  // held for the whole call: one caller per device at a time
     DevBuf C, Pt, O, B, E, T;
   };
   static std::mutex smu;
@@ -122,6 +123,7 @@ extern "C" int vfn_direct_eval(int device, const int64_t nm[3], const double a[3
     if (!slot) slot = new Scratch();
     sc = slot;
   }
+  std::lock_guard<std::mutex> call_lock(sc->mu);
   DevBuf &C = sc->C, &Pt = sc->Pt, &O = sc->O, &B = sc->B, &E = sc->E, &T = sc->T;
   const double2* cd = reinterpret_cast<const double2*>(coeffs);
   const double* pd = points;

@@ -65,6 +65,7 @@ int rect_eval(int device, const int64_t nm[3], const double a[3], const double b
                         sizeof(double2) * M2 * N2};
   // grow-only scratch per device, reused across calls (one host thread at a time)
   struct Scratch {
+    std::mutex mu;  // held for the whole call: one caller per device at a time
     DevBuf C, T1, T2, F, E[3], Y[3];
   };
   static std::mutex smu;
@@ -76,6 +77,7 @@ int rect_eval(int device, const int64_t nm[3], const double a[3], const double b
     if (!slot) slot = new Scratch();
     sc = slot;
   }
+  std::lock_guard<std::mutex> call_lock(sc->mu);
   DevBuf &C = sc->C, &T1 = sc->T1, &T2 = sc->T2, &F = sc->F;
   DevBuf* E = sc->E;
   DevBuf* Y = sc->Y;
