@@ -538,6 +538,8 @@ bool same_key(const vfn_plan::GraphKey& a, const vfn_plan::GraphKey& b) {
   if (!a.valid || !b.valid) return false;
   for (int d = 0; d < 3; ++d)
     if (a.box[d] != b.box[d] || a.tile[d] != b.tile[d]) return false;
+  for (int i = 0; i < 12; ++i)
+    if (a.bufs[i] != b.bufs[i]) return false;
   return a.pts == b.pts && a.out == b.out && a.bad == b.bad && a.M == b.M && a.variant == b.variant;
 }
 
@@ -557,6 +559,10 @@ int eval_graphed(vfn_plan* p, const double* pts_dev, int64_t M, double2* out_dev
     k.tile[d] = g.tile[d];
   }
   k.variant = p->gather_variant;
+  const void* bufs[12] = {p->keys.ptr,  p->keys_sorted.ptr, p->idx.ptr,   p->perm.ptr,
+                          p->sort_tmp.ptr, p->box_start.ptr, p->items.ptr, p->units.ptr,
+                          p->uscratch.ptr, p->uvals.ptr, p->misc.ptr, p->pts.ptr};
+  for (int i = 0; i < 12; ++i) k.bufs[i] = bufs[i];
   k.valid = true;
   if (!same_key(k, p->gkey)) {
     if (!same_key(k, p->gseen)) {

@@ -163,6 +163,9 @@ struct vfn_plan {
     int64_t M = -1;
     int box[3] = {0, 0, 0}, tile[3] = {0, 0, 0};
     int variant = -1;
+    // the plan's scratch buffers the captured launches point into: a call
+    // that grew (reallocated) any of them invalidates the graph
+    const void* bufs[12] = {};
     bool valid = false;
   };
   GraphKey gkey, gseen;

@@ -500,6 +500,11 @@ def test_cuda_graph_replay_matches_eager(vfb, offset_box):
     np.testing.assert_array_equal(out.cpu().numpy(), eager.evaluate(batches[0]))
     for M in (17, 3000, 17):
         np.testing.assert_array_equal(graphed.evaluate(batches[0][:M]), eager.evaluate(batches[0][:M]))
+    # a larger call in between grows (reallocates) the plan's scratch: the
+    # graph captured before must not be replayed on the freed buffers
+    big = rng.uniform(a, b, (200000, 3))
+    for p in (batches[1], batches[1], big, batches[1], batches[1]):
+        np.testing.assert_array_equal(graphed.evaluate(p), eager.evaluate(p))
 
 
 def test_batched_evaluate_beyond_batch_limit(vfb, offset_box, monkeypatch):
