@@ -536,6 +536,23 @@ def test_batched_evaluate_beyond_batch_limit(vfb, offset_box, monkeypatch):
     np.testing.assert_array_equal(plan.evaluate(big), ref_big)
 
 
+@pytest.mark.parametrize("shape", [(2, 2, 64), (64, 2, 2), (2, 4, 2), (2, 2, 2), (4, 30, 2)])
+@pytest.mark.parametrize("m", [2, 6, 7])
+def test_tiny_and_anisotropic_grids(vfb, offset_box, shape, m):
+    """Mode counts of 2 along some axes (oversampled grids of 4 cells, far
+    smaller than one tile plus its halo) on every gather variant, vs the oracle."""
+    spec = random_spectral(offset_box, shape, 150 + m)
+    rng = np.random.default_rng(151 + m)
+    pts = rng.uniform(offset_box.a, offset_box.b, (3000, 3))
+    plan = vfb.NufftPlan(spec, vfb.NufftParams(cutoff=m, eps=0.999))
+    grid, n, beta = O.oversampled_grid(spec.coeffs, offset_box.a, offset_box.b, 2.0, m)
+    ref = O.gather_eval(grid, n, m, beta, pts, offset_box.a, offset_box.b)
+    for variant in (0, 1):
+        plan.set_gather(variant)
+        l2, linf = rel_err(plan.evaluate(pts), ref)
+        assert l2 < 1e-12 and linf < 1e-12, (shape, m, variant, l2, linf)
+
+
 def test_c_abi_from_plain_c(tmp_path):
     """The boundary works without Python: examples/c_api_demo.c links
     libvfnfft.so directly, evaluates against vfn_direct_eval and checks the
