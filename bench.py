@@ -244,8 +244,15 @@ def dist_setup(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        # VFN_DIST_BACKEND=gloo + fewer GPUs than ranks: plumbing check of the
+        # torchrun path on a 1-GPU box (ranks share a device; timings meaningless)
+        backend = os.environ.get("VFN_DIST_BACKEND", "nccl")
+        local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     return world, rank, local

@@ -44,3 +44,19 @@ def test_reference_arm_tube_workload():
     assert BASE_KEYS <= set(out)
     assert out["unit"] == "ms" and out["higher_is_better"] is False and out["value"] > 0
     assert out["config"]["workload"].startswith("tube")
+
+
+def test_reference_arm_under_torchrun_prints_once():
+    """N > 1 launch (torchrun, 2 ranks): rank 0 alone runs the reference arm
+    and prints one line; the other rank exits 0 without work."""
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29561", os.path.join(REPO, "bench.py"),
+           "--impl", "reference", "--gpus", "2", "--workload", "c1", "--steps", "1", "--warmup", "0",
+           "--cpu-seconds", "2"]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=REPO, env=env)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, res.stdout
+    out = json.loads(lines[0])
+    assert out["impl"] == "reference" and out["n_gpus"] == 2 and out["value"] > 0
