@@ -486,10 +486,21 @@ def run_rect(args):
     clk = clocks.stop()
     step_ms = e0.elapsed_time(e1) / args.steps
     npts = 256 ** 3
-    # e2e: host coefficients in, host values out
-    t0 = time.perf_counter()
-    host = vfb.eval_rectilinear(vfb.SpectralField(box, coeffs), axes)
-    e2e_ms = (time.perf_counter() - t0) * 1e3
+    # e2e through the public API: pinned host coefficients in, pinned host
+    # values out (the download overlaps the last pass slab by slab), warmed
+    # up like the device loop
+    c_pin = torch.empty(coeffs.shape, dtype=torch.complex128, pin_memory=True)
+    c_pin.copy_(torch.as_tensor(coeffs))
+    o_pin = torch.empty((256, 256, 256), dtype=torch.complex128, pin_memory=True)
+    spec_h = vfb.SpectralField(box, c_pin.numpy())
+    host = o_pin.numpy()
+    vfb.eval_rectilinear(spec_h, axes, out=host)
+    e2e_runs = []
+    for _ in range(max(2, min(args.steps, 5))):
+        t0 = time.perf_counter()
+        vfb.eval_rectilinear(spec_h, axes, out=host)
+        e2e_runs.append((time.perf_counter() - t0) * 1e3)
+    e2e_ms = float(np.mean(e2e_runs))
     N, Mx = 128, 256
     cmacs = N * N * N * Mx + N * N * Mx * Mx + N * Mx * Mx * Mx  # the three passes
     achieved = 8.0 * cmacs / (step_ms * 1e-3) / 1e12
@@ -516,11 +527,12 @@ def run_rect(args):
                    "modes": [128, 128, 128], "points": npts},
         "e2e": {"value": npts / (e2e_ms * 1e-3), "unit": "points/s",
                 "h2d_bytes_per_step": int(coeffs.nbytes + 3 * 256 * 8), "d2h_bytes_per_step": int(npts * 16),
-                "ms_per_step": e2e_ms},
+                "ms_per_step": e2e_ms,
+                "matches_device_result_bitwise": bool(np.array_equal(host, out.cpu().numpy()))},
         "roofline": {"bound": "fp64", "kernel": "3 ZGEMM passes (cuBLAS DMMA)", "achieved": achieved,
                      "peak": tf.value, "unit": "TFLOP/s", "frac": achieved / tf.value, "traffic": None,
                      "algorithmic": f"{cmacs} complex MACs = 8 flop each"},
-        "gpu_launches": None,
+        "gpu_launches": 3 * args.steps,  # k_basis per axis; the ZGEMMs are cuBLAS's
         "clocks": clk,
     }
     if cpu is not None:

@@ -5,6 +5,7 @@
 // complex GEMMs (cuBLAS ZGEMM, FP64 tensor-core DMMA on sm_100a).
 #include <cublas_v2.h>
 
+#include <algorithm>
 #include <map>
 #include <mutex>
 
@@ -50,6 +51,10 @@ void* blas_handle(int device) { return handle_for(device); }
     }                                                                                         \
   } while (0)
 
+// Host outputs: pass 3 runs in kRectSlabs slabs of output rows (m0), each
+// slab's D2H on a copy stream overlapping the next slab's GEMM.
+constexpr int kRectSlabs = 8;
+
 int rect_eval(int device, const int64_t nm[3], const double a[3], const double b[3],
               const double* coeffs, const double* y[3], const int64_t Mv[3], double* out,
               int on_device, cudaStream_t s) {
@@ -67,6 +72,8 @@ int rect_eval(int device, const int64_t nm[3], const double a[3], const double b
   struct Scratch {
     std::mutex mu;  // held for the whole call: one caller per device at a time
     DevBuf C, T1, T2, F, E[3], Y[3];
+    cudaStream_t copy = nullptr;  // D2H of result slabs (host outputs)
+    cudaEvent_t ev[kRectSlabs + 1] = {};
   };
   static std::mutex smu;
   static std::map<int, Scratch*> scratch;
@@ -131,14 +138,36 @@ int rect_eval(int device, const int64_t nm[3], const double a[3], const double b
     VFN_BLAS(cublasZgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)M2, (int)M1, (int)N1, al,
                                        T1.as<cuDoubleComplex>(), (int)M2, N1 * M2, e1, (int)N1, 0,
                                        be, T2.as<cuDoubleComplex>(), (int)M2, M1 * M2, (int)N0));
-    // pass 3, mode 1: F (M0 x M1M2) = E0 (M0 x N0) T2 (N0 x M1M2)
-    VFN_BLAS(cublasZgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)(M1 * M2), (int)M0, (int)N0, al,
-                         T2.as<cuDoubleComplex>(), (int)(M1 * M2), e0, (int)N0, be,
-                         reinterpret_cast<cuDoubleComplex*>(Fd), (int)(M1 * M2)));
-  }
-  if (!on_device && cudaMemcpyAsync(out, Fd, fb, cudaMemcpyDeviceToHost, s) != cudaSuccess) {
-    st = fail(VFN_ERR_CUDA, "result download failed");
-    goto done;
+    // pass 3, mode 1: F (M0 x M1M2) = E0 (M0 x N0) T2 (N0 x M1M2); rows
+    // [lo, lo + n) of F use rows [lo, lo + n) of E0
+    const int nslab = on_device ? 1 : (int)std::min<int64_t>(kRectSlabs, M0);
+    if (!on_device && !sc->copy) {
+      if (cudaStreamCreateWithFlags(&sc->copy, cudaStreamNonBlocking) != cudaSuccess) {
+        st = fail(VFN_ERR_CUDA, "copy stream creation failed");
+        goto done;
+      }
+      for (auto& e : sc->ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    }
+    for (int j = 0; j < nslab; ++j) {
+      const int64_t lo = M0 * j / nslab, n = M0 * (j + 1) / nslab - lo;
+      if (n == 0) continue;
+      VFN_BLAS(cublasZgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)(M1 * M2), (int)n, (int)N0, al,
+                           T2.as<cuDoubleComplex>(), (int)(M1 * M2), e0 + lo * N0, (int)N0, be,
+                           reinterpret_cast<cuDoubleComplex*>(Fd) + lo * M1 * M2, (int)(M1 * M2)));
+      if (!on_device) {
+        cudaEventRecord(sc->ev[j], s);
+        cudaStreamWaitEvent(sc->copy, sc->ev[j], 0);
+        if (cudaMemcpyAsync(out + 2 * lo * M1 * M2, Fd + lo * M1 * M2, sizeof(double2) * n * M1 * M2,
+                            cudaMemcpyDeviceToHost, sc->copy) != cudaSuccess) {
+          st = fail(VFN_ERR_CUDA, "result download failed");
+          goto done;
+        }
+      }
+    }
+    if (!on_device) {
+      cudaEventRecord(sc->ev[kRectSlabs], sc->copy);
+      cudaStreamWaitEvent(s, sc->ev[kRectSlabs], 0);
+    }
   }
   {
     cudaError_t e = cudaStreamSynchronize(s);

@@ -41,9 +41,13 @@ def basis_matrix(domain, n: int, axis: int, coords) -> np.ndarray:
     return np.exp(2j * np.pi * np.outer(y - a, k) / (b - a)) / np.sqrt(b - a)
 
 
-def eval_rectilinear(spec, coords):
+def eval_rectilinear(spec, coords, out=None):
     """Series values on the tensor grid coords[0] x coords[1] x coords[2];
-    complex (M1, M2, M3) (rectilinear.py:47-64)."""
+    complex (M1, M2, M3) (rectilinear.py:47-64).  ``out`` (extension, like
+    ``NufftPlan.evaluate``'s): a C-contiguous complex128 (M1, M2, M3) array on
+    the coefficients' side (numpy for host coefficients, a CUDA tensor for
+    device ones) that receives the values; pinned host memory makes the
+    result download overlap the last pass."""
     if len(coords) != 3:
         raise ValueError("need exactly three coordinate vectors")
     coeffs = spec.coeffs
@@ -61,11 +65,19 @@ def eval_rectilinear(spec, coords):
         dev = _device_of(coeffs)
         coeffs = coeffs.to(t.complex128).contiguous()
         ys = [t.as_tensor(y, device=coeffs.device) for y in ys]
-        out = t.empty(M, dtype=t.complex128, device=coeffs.device)
+        if out is None:
+            out = t.empty(M, dtype=t.complex128, device=coeffs.device)
+        elif not (_is_cuda_tensor(out) and out.device == coeffs.device and tuple(out.shape) == M
+                  and out.dtype == t.complex128 and out.is_contiguous()):
+            raise ValueError(f"out must be a contiguous complex128 CUDA tensor of shape {M} on {coeffs.device}")
     else:
         dev = _device_of(None)
         coeffs = np.ascontiguousarray(np.asarray(coeffs), dtype=np.complex128)
-        out = np.empty(M, dtype=np.complex128)
+        if out is None:
+            out = np.empty(M, dtype=np.complex128)
+        elif not (isinstance(out, np.ndarray) and out.shape == M and out.dtype == np.complex128
+                  and out.flags.c_contiguous):
+            raise ValueError(f"out must be a C-contiguous complex128 numpy array of shape {M}")
     if 0 in M:
         return out
     lib = _lib.load()

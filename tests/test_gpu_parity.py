@@ -262,6 +262,37 @@ def test_rectilinear_matches_reference(vfb):
         assert l2 < 1e-13 and linf < 1e-13, (i, l2, linf)
 
 
+def test_rectilinear_out_argument_and_slabs(vfb):
+    """eval_rectilinear(..., out=): device outputs are bitwise the device
+    result; host outputs (pass 3 in slabs with overlapped downloads, also
+    with fewer output rows than slabs) are bitwise identical for pageable and
+    pinned memory and agree with the device result to rounding (cuBLAS may
+    pick another kernel for a slab's GEMM shape)."""
+    import torch
+
+    g = golden("rect_cases.npz")
+    for i in range(int(g["ncases"])):
+        box = vfb.DomainBox(tuple(g[f"case{i}_a"]), tuple(g[f"case{i}_b"]))
+        coeffs = g[f"case{i}_coeffs"]
+        ys = [g[f"case{i}_y{d}"] for d in range(3)]
+        for y0 in (ys[0], ys[0][:3]):
+            axes = [y0, ys[1], ys[2]]
+            shape = (len(y0), len(ys[1]), len(ys[2]))
+            dev = vfb.eval_rectilinear(vfb.SpectralField(box, torch.as_tensor(coeffs, device="cuda")), axes)
+            o = torch.empty(shape, dtype=torch.complex128, device="cuda")
+            vfb.eval_rectilinear(vfb.SpectralField(box, torch.as_tensor(coeffs, device="cuda")), axes, out=o)
+            assert torch.equal(o, dev)
+            plain = vfb.eval_rectilinear(vfb.SpectralField(box, coeffs), axes)
+            pinned = torch.empty(shape, dtype=torch.complex128, pin_memory=True).numpy()
+            vfb.eval_rectilinear(vfb.SpectralField(box, coeffs), axes, out=pinned)
+            ref = dev.cpu().numpy()
+            assert np.array_equal(plain, pinned)
+            l2, linf = rel_err(plain, ref)
+            assert l2 < 1e-14 and linf < 1e-14, (i, l2, linf)
+    with pytest.raises(ValueError):
+        vfb.eval_rectilinear(vfb.SpectralField(box, coeffs), ys, out=np.empty((1, 1, 1), complex))
+
+
 def test_rectilinear_regular_grid_matches_fft(vfb, offset_box):
     spec = random_spectral(offset_box, (12, 12, 12), 43)
     axes = vfb.regular_grid(offset_box, spec.coeffs.shape)
