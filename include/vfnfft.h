@@ -42,7 +42,9 @@
  *   - every call returns a vfn_status; vfn_last_error() gives the message of
  *     the last failure on the calling thread.
  *   - Inputs are never modified; the plan owns its device grid; outputs are
- *     caller-owned.  A plan may be evaluated from one host thread at a time.
+ *     caller-owned.  Calls on one plan from several host threads are
+ *     serialised by the plan (the reference allows evaluating a shared plan
+ *     from several threads); distinct plans are independent.
  */
 #ifndef VFNFFT_H
 #define VFNFFT_H

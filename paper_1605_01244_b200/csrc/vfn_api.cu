@@ -282,6 +282,7 @@ int vfn_plan_info(const vfn_plan* p, int64_t n_out[3], double* beta_out) {
 
 int vfn_plan_geometry(const vfn_plan* p, int64_t M, int box_out[3], int tile_out[3]) {
   if (!p || !box_out || !tile_out) return fail(VFN_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> plan_lock(p->mu);
   // the geometry of the last evaluate/bin call, else the point-free rule for M
   const double cells = (double)p->n[0] * (double)p->n[1] * (double)p->n[2];
   BinGeom g = p->has_last_geom ? p->last_geom
@@ -295,12 +296,14 @@ int vfn_plan_geometry(const vfn_plan* p, int64_t M, int box_out[3], int tile_out
 
 int vfn_plan_set_box(vfn_plan* p, int bxy) {
   if (!p || bxy < 0 || bxy > 2) return fail(VFN_ERR_INVALID, "box must be 0 (auto), 1 or 2");
+  std::lock_guard<std::mutex> plan_lock(p->mu);
   p->box_mode = bxy;
   return VFN_OK;
 }
 
 int vfn_plan_set_graphs(vfn_plan* p, int enable) {
   if (!p) return fail(VFN_ERR_INVALID, "null plan");
+  std::lock_guard<std::mutex> plan_lock(p->mu);
   p->graphs_on = enable != 0;
   p->gseen.valid = false;
   return VFN_OK;
@@ -308,12 +311,14 @@ int vfn_plan_set_graphs(vfn_plan* p, int enable) {
 
 int vfn_plan_set_gather(vfn_plan* p, int variant) {
   if (!p || variant < 0 || variant > 2) return fail(VFN_ERR_INVALID, "bad gather variant");
+  std::lock_guard<std::mutex> plan_lock(p->mu);
   p->gather_variant = variant;
   return VFN_OK;
 }
 
 int vfn_plan_last_timing(const vfn_plan* p, float* gather_ms, float* total_ms) {
   if (!p) return fail(VFN_ERR_INVALID, "null plan");
+  std::lock_guard<std::mutex> plan_lock(p->mu);
   if (gather_ms) *gather_ms = p->last_gather_ms;
   if (total_ms) *total_ms = p->last_total_ms;
   return VFN_OK;
@@ -402,6 +407,7 @@ static int bin_points(vfn_plan* p, const double* points, int64_t M, int on_devic
 int vfn_plan_bin(vfn_plan* p, const double* points, int64_t M, uint32_t* keys, int32_t* perm,
                  int on_device, int64_t* first_bad_row, void* stream) {
   if (!p || (M > 0 && (!points || !keys || !perm))) return fail(VFN_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> plan_lock(p->mu);
   if (M < 0 || M > INT32_MAX) return fail(VFN_ERR_INVALID, "point count out of range");
   if (first_bad_row) *first_bad_row = -1;
   if (M == 0) return VFN_OK;
@@ -725,6 +731,7 @@ extern "C" {
 int vfn_plan_eval(vfn_plan* p, const double* points, int64_t M, double* out, int on_device,
                   int64_t* first_bad_row, void* stream) {
   if (!p || (M > 0 && (!points || !out))) return fail(VFN_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> plan_lock(p->mu);
   if (M < 0) return fail(VFN_ERR_INVALID, "point count out of range");
   if (first_bad_row) *first_bad_row = -1;
   if (M == 0) return VFN_OK;

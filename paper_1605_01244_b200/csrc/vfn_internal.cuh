@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <mutex>
 #include <cstdio>
 #include <string>
 
@@ -124,6 +125,11 @@ struct WindowPoly {
 }  // namespace vfn
 
 struct vfn_plan {
+  // Serialises every entry point that touches the plan's scratch or settings:
+  // the reference allows one plan to be evaluated from several threads on
+  // disjoint point subsets; calls here queue on this lock
+  // (each call synchronises its stream before returning).
+  mutable std::mutex mu;
   int device = 0;
   int64_t N[3] = {0, 0, 0};
   int64_t n[3] = {0, 0, 0};

@@ -498,6 +498,44 @@ def test_tensor_core_gather_other_cutoffs(vfb, offset_box, m):
         assert l2 < 1e-13 and linf < 1e-13
 
 
+def test_shared_plan_from_several_threads(vfb, offset_box):
+    """The reference allows one plan to be evaluated from several threads on
+    disjoint point subsets (ctypes releases the GIL): host
+    and CUDA-tensor inputs from 6 threads give the serial values bitwise."""
+    import threading
+
+    import torch
+
+    spec = random_spectral(offset_box, (16, 20, 24), 400)
+    rng = np.random.default_rng(401)
+    pts = rng.uniform(offset_box.a, offset_box.b, (600000, 3))
+    plan = vfb.NufftPlan(spec)
+    parts = np.array_split(np.arange(len(pts)), 12)
+    serial = [plan.evaluate(pts[ix]) for ix in parts]
+    got = [None] * len(parts)
+    errors = []
+
+    def work(k):
+        try:
+            for j in range(k, len(parts), 6):
+                if j % 2:
+                    with torch.cuda.stream(torch.cuda.Stream()):
+                        got[j] = plan.evaluate(torch.as_tensor(pts[parts[j]], device="cuda")).cpu().numpy()
+                else:
+                    got[j] = plan.evaluate(pts[parts[j]])
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(6)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+    for a, b in zip(got, serial):
+        assert np.array_equal(a, b)
+
+
 def test_cuda_graph_replay_matches_eager(vfb, offset_box):
     """Repeated small evaluates replay one CUDA graph (second call captures):
     values bitwise equal to the eager launches, new point values in the same
