@@ -304,6 +304,32 @@ def test_rectilinear_regular_grid_matches_fft(vfb, offset_box):
     assert np.abs(out - ref).max() <= 1e-12 * np.abs(ref).max()
 
 
+def test_acceptance_geometry_grid_and_points(vfb):
+    """The reference's acceptance criteria 1-3 restated (test_acceptance.py:27-85):
+    a 64^3 spectrum (real and imaginary parts N(0, 1/2), seed 2024) on the
+    box [-20, 60)^3.  The rectilinear path on the regular grid and the NUFFT
+    at every grid point must match the inverse FFT to 1e-11 absolute.  1000
+    random points must match the exact sum to 1e-11."""
+    box = vfb.DomainBox((-20.0,) * 3, (60.0,) * 3)
+    rng = np.random.default_rng(2024)
+    shape = (64, 64, 64)
+    coeffs = (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)) / np.sqrt(2.0)
+    spec = vfb.SpectralField(box, coeffs)
+    axes = vfb.regular_grid(box, shape)
+    scale = float(np.prod(np.sqrt(box.widths) / np.array(shape)))
+    ref = np.fft.ifftn(np.fft.ifftshift(coeffs)) / scale
+    rect = vfb.eval_rectilinear(spec, axes)
+    assert np.abs(rect - ref).max() <= 1e-11
+    grid_pts = np.stack(np.meshgrid(*axes, indexing="ij"), axis=-1).reshape(-1, 3)
+    plan = vfb.NufftPlan(spec)
+    at_grid = plan.evaluate(grid_pts).reshape(shape)
+    assert np.abs(at_grid - ref).max() <= 1e-11
+    pts = rng.uniform(-20.0, 60.0, (1000, 3))
+    direct = O.ndft(coeffs, box.a, box.b, pts)
+    assert np.abs(plan.evaluate(pts) - direct).max() <= 1e-11
+    assert np.abs(vfb.eval_direct(spec, pts) - direct).max() <= 1e-11
+
+
 # ---------------------------------------------------------------- full-size properties
 
 
