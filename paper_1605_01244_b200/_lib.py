@@ -13,7 +13,9 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libvfnfft.so")
+# VFN_LIB=checks loads the debug build with device-side bounds checks
+# (python paper_1605_01244_b200/build.py --checks)
+LIB_PATH = os.path.join(HERE, "libvfnfft_checks.so" if os.environ.get("VFN_LIB") == "checks" else "libvfnfft.so")
 
 VFN_OK = 0
 VFN_ERR_INVALID = -1

@@ -4,6 +4,25 @@
 
 #include "vfn_internal.cuh"
 
+// Device-side bounds checks of the debug build (build.py --checks defines
+// VFN_CHECKS; compute-sanitizer is unavailable on the GPU pool): a failed
+// check prints its location and traps, failing the call with a CUDA error.
+#ifdef VFN_CHECKS
+#include <cstdio>
+#define VFN_DCHECK(cond)                                                                   \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("VFN_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                           \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define VFN_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 namespace vfn {
 
 // zeta_d = mod((x - a) / (a - b), 1) - 1/2 with numpy's float remainder

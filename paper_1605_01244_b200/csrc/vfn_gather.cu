@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_gather_dmma(GatherArgs A) {
       for (int r = warp; r < XY; r += kWarps) {
         const double2* src = A.grid + ((ox + x) * A.P1 + (oy + y)) * A.P2 + oz;
         double2* dst = sG + (size_t)r * A.SZ;
+        VFN_DCHECK(x < A.X && y < A.Y && oy + y < A.P1 && oz + A.Z <= A.P2);
         for (int z = lane; z < A.Z; z += 32) cp_async16(dst + z, src + z);
         x += dx;
         y += dy;
@@ -166,6 +167,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_gather_dmma(GatherArgs A) {
       const int ci = cell[0] - (int)ox - X0;  // offsets of the point inside its box
       const int cj = cell[1] - (int)oy - Y0;
       const int ck = cell[2] - (int)oz - Z0;
+      VFN_DCHECK(!valid || (ci >= 0 && ci < bi && cj >= 0 && cj < bj && ck >= 0 && ck < bk));
       // A fragment: axis-3 weights of point g at box depth k = 4 kc + tig
       double a[KC];
 #pragma unroll
@@ -198,6 +200,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_gather_dmma(GatherArgs A) {
       for (int t = 0; t < NT; ++t) {
         const int rb = 8 * t + g;
         const double2* bp = gz + (rb < R ? ((X0 + rbx) * A.Y + (Y0 + rby)) * A.SZ : 0);
+        VFN_DCHECK(bp >= sG && bp + 4 * (KC - 1) < sG + (size_t)A.X * A.Y * A.SZ);
         double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
 #pragma unroll
         for (int kc = 0; kc < KC; ++kc) {

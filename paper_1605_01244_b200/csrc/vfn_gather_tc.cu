@@ -92,6 +92,8 @@ struct Args {
   double2* out;
   const double* poly;     // window polynomial table (W x (deg+1))
   int deg;
+  int64_t M;              // points (bounds checks of the VFN_CHECKS build)
+  int64_t nunits;         // unit-list capacity (bounds checks)
   TorusMap tm;
   BinGeom g;
 };
@@ -156,10 +158,12 @@ __device__ __forceinline__ void issue_tile(const CUtensorMap* map, const Args& A
 // One 8-row DMMA tile: C_re/im[p, n] for the lane's B row at `addr`.
 template <int KC>
 __device__ __forceinline__ void tile_mma(unsigned addr, const double (&a)[KC], double& cr0,
-                                         double& cr1, double& ci0, double& ci1) {
+                                         double& cr1, double& ci0, double& ci1, unsigned lo,
+                                         unsigned hi) {
   cr0 = cr1 = ci0 = ci1 = 0.0;
 #pragma unroll
   for (int kc = 0; kc < KC; ++kc) {
+    VFN_DCHECK(addr + kc * 64 >= lo && addr + kc * 64 + 16 <= hi);  // inside the staged tile
     const double2 v = lds128(addr + kc * 64);
     dmma(cr0, cr1, a[kc], v.x);
     dmma(ci0, ci1, a[kc], v.y);
@@ -179,8 +183,10 @@ __device__ __forceinline__ UnitPoints load_unit_points(const Args& A, int4 desc,
   up.prow = 0;
   up.uu[0] = up.uu[1] = up.uu[2] = 0.0;
   if (g < (desc.y & 15)) {
+    VFN_DCHECK(desc.x >= 0 && desc.x + g < A.M);
     // streamed once: evict-first, so the grid's tiles keep the L2
     up.prow = __ldcs(A.perm + desc.x + g);
+    VFN_DCHECK(up.prow >= 0 && up.prow < A.M);
 #pragma unroll
     for (int d = 0; d < 3; ++d) up.uu[d] = __ldcs(A.u + 3 * up.prow + d);
   }
@@ -273,10 +279,17 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
   } else {
     const double* wa = wA + g * kAS + kAO + kz + tig - ck;
 #pragma unroll
-    for (int kc = 0; kc < KC; ++kc) a[kc] = inbox ? wa[4 * kc] : 0.0;
+    for (int kc = 0; kc < KC; ++kc) {
+      VFN_DCHECK(kAO + kz + tig - ck + 4 * kc >= 0 && kAO + kz + tig - ck + 4 * kc < kAS);
+      a[kc] = inbox ? wa[4 * kc] : 0.0;
+    }
   }
   const double* wx = wX + g * kXS + kXO - ci;  // wx[x], x in [0, 16); zero off the stencil
   const double* wy = wY + g * kXS + kXO - cj;  // wy[y]
+  VFN_DCHECK(kXO - ci >= 0 && kXO - ci + XB <= kXS && kXO - cj >= 0 && kXO - cj + YB <= kXS);
+  // the unit's K window [kz, kz + 4 KC) of staged depths holds every point's
+  // stencil (staged depths ck .. ck + W - 1) and lies inside the staged tile
+  VFN_DCHECK(kz >= 0 && kz + 4 * KC <= kSZ && (!inbox || (ck >= kz && ck + C::W <= kz + 4 * KC)));
 
   const unsigned base = tile_s + (unsigned)((kz + tig) * 16 + (X0 * C::SY + Y0) * kLine);
   constexpr unsigned kX = C::SY * kLine;  // x stride
@@ -294,7 +307,7 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
 #pragma unroll
     for (int x = 0; x < XB; ++x) {
       double cr0, cr1, ci0_, ci1_;
-      tile_mma<KC>(ba + x * kX, a, cr0, cr1, ci0_, ci1_);
+      tile_mma<KC>(ba + x * kX, a, cr0, cr1, ci0_, ci1_, tile_s, tile_s + C::kTileBytes);
       const double w = wx[x];
       t0r = fma(w, cr0, t0r);
       t1r = fma(w, cr1, t1r);
@@ -313,7 +326,7 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
 #pragma unroll
     for (int p = 0; p < (XB + 1) / 2; ++p) {
       double cr0, cr1, ci0_, ci1_;
-      tile_mma<KC>(bb + min(2 * p + xb, XB - 1) * kX, a, cr0, cr1, ci0_, ci1_);
+      tile_mma<KC>(bb + min(2 * p + xb, XB - 1) * kX, a, cr0, cr1, ci0_, ci1_, tile_s, tile_s + C::kTileBytes);
       const double w = wx[2 * p + xc];
       t0r = fma(w, cr0, t0r);
       t1r = fma(w, cr1, t1r);
@@ -331,7 +344,7 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
 #pragma unroll
     for (int q = 0; q < (XB + 3) / 4; ++q) {
       double cr0, cr1, ci0_, ci1_;
-      tile_mma<KC>(bc + min(4 * q + (g >> 1), XB - 1) * kX, a, cr0, cr1, ci0_, ci1_);
+      tile_mma<KC>(bc + min(4 * q + (g >> 1), XB - 1) * kX, a, cr0, cr1, ci0_, ci1_, tile_s, tile_s + C::kTileBytes);
       const double w = wx[4 * q + tig];
       t0r = fma(w, cr0, t0r);
       t1r = fma(w, cr1, t1r);
@@ -349,7 +362,7 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
 #pragma unroll
     for (int q = 0; q < (XB + 7) / 8; ++q) {
       double cr0, cr1, ci0_, ci1_;
-      tile_mma<KC>(bd + min(8 * q + g, XB - 1) * kX, a, cr0, cr1, ci0_, ci1_);
+      tile_mma<KC>(bd + min(8 * q + g, XB - 1) * kX, a, cr0, cr1, ci0_, ci1_, tile_s, tile_s + C::kTileBytes);
       const double w0 = wx[8 * q + 2 * tig], w1 = wx[8 * q + 2 * tig + 1];
       tr = fma(w0, cr0, fma(w1, cr1, tr));
       ti = fma(w0, ci0_, fma(w1, ci1_, ti));
@@ -458,6 +471,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       if (u < walk.base + n) {
         kk = walk.k;
         it4 = walk.item;
+        VFN_DCHECK(walk.item.y + (u - walk.base) < walk.item.z && walk.item.z <= A.nunits);
         desc = __ldg(A.units + walk.item.y + (u - walk.base));
         return true;
       }
@@ -685,6 +699,8 @@ int launch_tc(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t*
   A.out = out;
   A.poly = p->poly.dev;
   A.deg = p->poly.deg;
+  A.M = M;
+  A.nunits = M + 1;
   A.tm = p->map;
   A.g = g;
   mark_event(p, 1, s);  // gather timing starts here (binning prep excluded)

@@ -109,6 +109,7 @@ __global__ void k_map_key(const double* __restrict__ pts, int64_t M, TorusMap tm
   int64_t tile_id = ((int64_t)t[0] * g.ntile[1] + t[1]) * g.ntile[2] + t[2];
   int box_id = (in[0] * g.nbox[1] + in[1]) * g.nbox[2] + in[2];
   int cell_id = (c[2] * g.box[0] + c[0]) * g.box[1] + c[1];
+  VFN_DCHECK(tile_id < g.ntiles && box_id < g.boxes_per_tile && cell_id < g.cells_per_box);
   keys[i] = (uint32_t)((tile_id * g.boxes_per_tile + box_id) * g.cells_per_box + cell_id);
   if (iota) iota[i] = (int32_t)i;
 }
@@ -329,6 +330,7 @@ __global__ void __launch_bounds__(128) k_gather_simple(const double* __restrict_
   }
   // padded index of grid cell (c - m + j) is c + j
   const double2* base = grid + ((int64_t)cell[0] * P1 + cell[1]) * P2 + cell[2];
+  VFN_DCHECK(cell[1] + W <= P1 && cell[2] + W <= P2 && cell[0] >= 0 && cell[1] >= 0 && cell[2] >= 0);
   double ar = 0.0, ai = 0.0;
   for (int a = 0; a < W; ++a) {
     double br = 0.0, bi = 0.0;
