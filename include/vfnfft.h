@@ -138,7 +138,12 @@ int vfn_plan_geometry(const vfn_plan* plan, int64_t M, int box_out[3], int tile_
 int vfn_plan_set_box(vfn_plan* plan, int bxy);
 
 /* Kernel selection for vfn_plan_eval (benchmarks / A-B tests):
- * 0 = automatic, 1 = simple thread-per-point gather, 2 = DMMA box gather. */
+ * 0 = automatic, 1 = simple thread-per-point gather, 2 = DMMA box gather,
+ * 3 = unbinned warp-per-point gather.  Automatic uses 3 for evaluates of at
+ * most VFN_WARP_MAX_M points (no binning: two launches) and the binned
+ * tensor-core gather above.  Values of the two paths agree to rounding
+ * (~1e-16 relative), not bitwise. */
+#define VFN_WARP_MAX_M 32768
 int vfn_plan_set_gather(vfn_plan* plan, int variant);
 /* CUDA graphs for small evaluates (M <= 2^19, device part): on by default;
  * a repeated call with the same buffers, M and geometry replays one graph

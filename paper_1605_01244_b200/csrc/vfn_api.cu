@@ -235,6 +235,20 @@ int vfn_plan_create(vfn_plan** out, int device, const int64_t nmodes[3], const d
     }
   }
   for (int i = 0; i < 4; ++i) cudaEventCreate(&p->ev[i]);
+  if (cudaHostAlloc(&p->bad_host, sizeof(int64_t), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(&p->bad_mapped, p->bad_host, 0) != cudaSuccess) {
+    cudaGetLastError();
+    if (p->bad_host) cudaFreeHost(p->bad_host);
+    p->bad_host = nullptr;  // pageable fallback (p->bad_fallback)
+    p->bad_mapped = nullptr;
+  }
+  // bad-row word of the warp path, kept at the 0x7f.. sentinel between calls
+  if (p->warp_bad.ensure(sizeof(int64_t)) != VFN_OK ||
+      cudaMemset(p->warp_bad.ptr, 0x7f, sizeof(int64_t)) != cudaSuccess) {
+    std::string msg = vfn_last_error();
+    vfn_plan_destroy(p);
+    return fail(VFN_ERR_CUDA, "plan scratch: " + msg);
+  }
   // coefficients to the device
   const size_t cbytes = sizeof(double2) * nmodes[0] * nmodes[1] * nmodes[2];
   DevBuf staging;
@@ -268,6 +282,7 @@ int vfn_plan_destroy(vfn_plan* p) {
   for (int i = 0; i < 2; ++i)
     if (p->graph_ev[i]) cudaEventDestroy(p->graph_ev[i]);
   if (p->graph_stream) cudaStreamDestroy(p->graph_stream);
+  if (p->bad_host) cudaFreeHost(p->bad_host);
   delete p;
   return VFN_OK;
 }
@@ -310,7 +325,7 @@ int vfn_plan_set_graphs(vfn_plan* p, int enable) {
 }
 
 int vfn_plan_set_gather(vfn_plan* p, int variant) {
-  if (!p || variant < 0 || variant > 2) return fail(VFN_ERR_INVALID, "bad gather variant");
+  if (!p || variant < 0 || variant > 3) return fail(VFN_ERR_INVALID, "bad gather variant");
   std::lock_guard<std::mutex> plan_lock(p->mu);
   p->gather_variant = variant;
   return VFN_OK;
@@ -319,6 +334,11 @@ int vfn_plan_set_gather(vfn_plan* p, int variant) {
 int vfn_plan_last_timing(const vfn_plan* p, float* gather_ms, float* total_ms) {
   if (!p) return fail(VFN_ERR_INVALID, "null plan");
   std::lock_guard<std::mutex> plan_lock(p->mu);
+  if (p->timing_pending) {  // events of the last call, complete since it synchronised
+    p->last_gather_ms = elapsed_ms(p->ev[1], p->ev[2]);
+    p->last_total_ms = elapsed_ms(p->ev[0], p->ev[3]);
+    p->timing_pending = false;
+  }
   if (gather_ms) *gather_ms = p->last_gather_ms;
   if (total_ms) *total_ms = p->last_total_ms;
   return VFN_OK;
@@ -493,6 +513,14 @@ int outside(int64_t bad, int64_t* first_bad_row) {
 // and unit offsets); larger calls run as consecutive batches with the first
 // batch's bin geometry, so every point's value is the one a single call
 // would give it (HBM holds ~3e9 points with their scratch on a B200).
+// Evaluates of at most this many points take the unbinned warp-per-point
+// gather (VFN_WARP_MAX_M in include/vfnfft.h; env VFN_WARP_MAX_M overrides).
+int64_t warp_max_m() {
+  int64_t v = VFN_WARP_MAX_M;
+  if (const char* e = std::getenv("VFN_WARP_MAX_M")) v = std::atoll(e);
+  return v;
+}
+
 int64_t max_batch() {
   int64_t b = (int64_t)1 << 30;
   if (const char* e = std::getenv("VFN_MAX_BATCH")) b = std::max<int64_t>(1 << 10, std::atoll(e));
@@ -525,8 +553,7 @@ int eval_device_batches(vfn_plan* p, const double* points, int64_t M, double* ou
   VFN_CUDA(cudaMemcpyAsync(bad.data(), bad_dev, sizeof(int64_t) * nb, cudaMemcpyDeviceToHost, s));
   VFN_CUDA(cudaEventRecord(p->ev[3], s));
   VFN_CUDA(cudaStreamSynchronize(s));
-  p->last_gather_ms = elapsed_ms(p->ev[1], p->ev[2]);
-  p->last_total_ms = elapsed_ms(p->ev[0], p->ev[3]);
+  p->timing_pending = true;  // elapsed times are read lazily (vfn_plan_last_timing)
   for (int64_t i = 0; i < nb; ++i)
     if (bad[i] != kBadSentinel) return outside(i * bsz + bad[i], first_bad_row);
   return VFN_OK;
@@ -717,8 +744,7 @@ int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* ou
   for (auto& x : ev) cudaEventDestroy(x);
   if (st != VFN_OK) return st;
   if (e != cudaSuccess) return fail(VFN_ERR_CUDA, std::string("pipelined evaluate: ") + cudaGetErrorString(e));
-  p->last_gather_ms = elapsed_ms(p->ev[1], p->ev[2]);
-  p->last_total_ms = elapsed_ms(p->ev[0], p->ev[3]);
+  p->timing_pending = true;  // elapsed times are read lazily (vfn_plan_last_timing)
   for (int64_t i = 0; i < nc; ++i)
     if (bad[i] != kBadSentinel) return outside(lo_of[i] + bad[i], first_bad_row);
   return VFN_OK;
@@ -750,17 +776,36 @@ int vfn_plan_eval(vfn_plan* p, const double* points, int64_t M, double* out, int
   }
   VFN_CHECK(p->misc.ensure(64));
   int64_t* bad_dev = p->misc.as<int64_t>();
-  bool graphed = false;
-  VFN_CHECK(eval_graphed(p, static_cast<const double*>(pdev), M, out_dev, bad_dev, s, &graphed));
-  if (!graphed) VFN_CHECK(eval_enqueue(p, static_cast<const double*>(pdev), M, out_dev, bad_dev, s, nullptr));
+  const bool warp_path = p->gather_variant == 3 || (p->gather_variant == 0 && M <= warp_max_m());
+  if (warp_path) {
+    // small evaluate: one unbinned warp-per-point kernel (vfn_kernels.cu K4
+    // v3); its bad-row word holds the sentinel between calls (set at plan
+    // creation, restored by store_word), so no memset per call
+    bad_dev = p->warp_bad.as<int64_t>();
+    mark_event(p, 1, s);
+    VFN_CHECK(gather_warp(p, static_cast<const double*>(pdev), M, out_dev, bad_dev, s));
+    mark_event(p, 2, s);
+  } else {
+    bool graphed = false;
+    VFN_CHECK(eval_graphed(p, static_cast<const double*>(pdev), M, out_dev, bad_dev, s, &graphed));
+    if (!graphed) VFN_CHECK(eval_enqueue(p, static_cast<const double*>(pdev), M, out_dev, bad_dev, s, nullptr));
+  }
   if (!on_device)
     VFN_CUDA(cudaMemcpyAsync(out, out_dev, sizeof(double2) * M, cudaMemcpyDeviceToHost, s));
-  int64_t bad = kBadSentinel;
-  VFN_CUDA(cudaMemcpyAsync(&bad, bad_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  // first bad row -> mapped pinned host word, stored by a one-thread kernel
+  // (a copy-engine D2H of 8 bytes adds ~10-20 us of latency to every call)
+  int64_t* bad_host = p->bad_host ? p->bad_host : &p->bad_fallback;
+  *bad_host = kBadSentinel;
+  if (p->bad_mapped) {
+    VFN_CHECK(store_word(bad_dev, p->bad_mapped, s, warp_path));
+  } else {
+    VFN_CUDA(cudaMemcpyAsync(bad_host, bad_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    if (warp_path) VFN_CUDA(cudaMemsetAsync(bad_dev, kBadByte, sizeof(int64_t), s));
+  }
   VFN_CUDA(cudaEventRecord(p->ev[3], s));
   VFN_CUDA(cudaStreamSynchronize(s));
-  p->last_gather_ms = elapsed_ms(p->ev[1], p->ev[2]);
-  p->last_total_ms = elapsed_ms(p->ev[0], p->ev[3]);
+  const int64_t bad = *bad_host;
+  p->timing_pending = true;  // elapsed times are read lazily (vfn_plan_last_timing)
   if (bad != kBadSentinel) return outside(bad, first_bad_row);
   return VFN_OK;
 }

@@ -153,9 +153,14 @@ struct vfn_plan {
   bool keep_fftbuf = false;
   // evaluate scratch (grow-only)
   vfn::DevBuf pts, out, uvals, keys, keys_sorted, idx, perm, sort_tmp, box_start, items, units, uscratch, misc;
+  vfn::DevBuf warp_bad;  // first-bad-row word of the warp-per-point path (never reallocated)
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t* bad_host = nullptr;  // mapped pinned word for the first-bad-row readback
+  int64_t* bad_mapped = nullptr;  // its device-side address
+  int64_t bad_fallback = 0;
   cudaStream_t copy_stream[2] = {nullptr, nullptr};  // H2D / D2H of the pipelined host path
-  float last_gather_ms = 0.f, last_total_ms = 0.f;
+  mutable float last_gather_ms = 0.f, last_total_ms = 0.f;
+  mutable bool timing_pending = false;  // ev[0..3] hold the last call's unread timing
   vfn::BinGeom last_geom;
   bool has_last_geom = false;
   int64_t iota_len = 0;  // idx[0..iota_len) holds 0, 1, 2, ... (the sort's values)
@@ -205,6 +210,13 @@ int sort_pairs(vfn_plan* p, const uint32_t* keys_in, uint32_t* keys_out, const i
 int launch_torus(const TorusMap& tm, const double* pts, int64_t M, double* zeta, cudaStream_t s);
 int gather_simple(vfn_plan* p, const double* pts_dev, int64_t M, const int32_t* perm,
                   double2* out_dev, cudaStream_t s);
+// warp-per-point gather of M unbinned points incl. the domain check (first
+// bad row atomicMin'd into bad_dev, which must hold the 0x7f.. sentinel)
+int gather_warp(vfn_plan* p, const double* pts_dev, int64_t M, double2* out_dev, int64_t* bad_dev,
+                cudaStream_t s);
+// *dst = *src by one device thread (dst: mapped host memory); reset: then
+// *src = the 0x7f.. bad-row sentinel
+int store_word(int64_t* src, int64_t* dst, cudaStream_t s, bool reset);
 int gather_boxes(vfn_plan* p, const double* pts_dev, int64_t M, const BinGeom& g,
                  const uint32_t* keys_sorted, const int32_t* perm, double2* out_dev,
                  cudaStream_t s, bool* used);

@@ -352,6 +352,107 @@ __global__ void __launch_bounds__(128) k_gather_simple(const double* __restrict_
   out[p] = make_double2(ar, ai);
 }
 
+// ------------------------------------------------------------------ K4 v3
+// Small evaluates (M <= VFN_WARP_MAX_M): no binning at all.  One warp per
+// point, in input order: the domain check and torus map (K0/K1), the 3 W
+// window weights (lanes j < W), the W x W products w1[a] w2[b] in a per-warp
+// table, then lanes = (row sub-index, c): each load instruction reads
+// 32 / W whole z-lines of the ghost-padded grid (coalesced), each lane sums
+// its column c over its rows and applies w3[c] once; a warp reduction gives
+// the value (nufft.py:244-272).  Two launches (memset + this) instead of the
+// ~25 of the binned path.
+template <int MC>
+__global__ void __launch_bounds__(256) k_gather_warp(const double* __restrict__ pts, int64_t M, TorusMap tm,
+                                                     const double* __restrict__ poly, int deg,
+                                                     const double2* __restrict__ grid, int64_t P1,
+                                                     int64_t P2, double2* __restrict__ out,
+                                                     unsigned long long* __restrict__ bad) {
+  constexpr int W = 2 * MC + 1;
+  constexpr int RPI = 32 / W;  // rows per load instruction
+  extern __shared__ double s_warp[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* w = s_warp + warp * (3 * W + W * W);  // w[d][j], then w12[a * W + b]
+  double* w12 = w + 3 * W;
+  const int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (p >= M) return;
+  int cell[3];
+  double dl[3];
+  bool ok = true;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double x = pts[3 * p + d];
+    ok = ok && inside(x, tm.a[d], tm.b[d]);
+    cell[d] = nearest_cell(x, tm.a[d], tm.amb[d], tm.nd[d], tm.n[d], dl[d]);
+  }
+  if (!ok && lane == 0) atomicMin(bad, (unsigned long long)p);
+  if (lane < W) {
+#pragma unroll
+    for (int d = 0; d < 3; ++d) w[d * W + lane] = window_poly(poly, deg, lane, dl[d]);
+  }
+  __syncwarp();
+  for (int r = lane; r < W * W; r += 32) w12[r] = w[r / W] * w[W + r % W];
+  __syncwarp();
+  const int c = lane % W, rs = lane / W;
+  double ar = 0.0, ai = 0.0;
+  if (rs < RPI) {
+    // padded index of grid cell (cell - m + j) is cell + j
+    const double2* base = grid + ((int64_t)cell[0] * P1 + cell[1]) * P2 + cell[2] + c;
+    VFN_DCHECK(cell[1] + W <= P1 && cell[2] + W <= P2);
+#pragma unroll 4
+    for (int r = rs; r < W * W; r += RPI) {
+      const int a = r / W, b = r - a * W;
+      const double2 v = __ldg(base + ((int64_t)a * P1 + b) * P2);
+      const double f = w12[r];
+      ar = fma(f, v.x, ar);
+      ai = fma(f, v.y, ai);
+    }
+    const double wc = w[2 * W + c];
+    ar *= wc;
+    ai *= wc;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ar += __shfl_xor_sync(0xffffffffu, ar, o);
+    ai += __shfl_xor_sync(0xffffffffu, ai, o);
+  }
+  if (lane == 0) out[p] = make_double2(ar, ai);
+}
+
+template <int MC>
+static void launch_warp(vfn_plan* pl, const double* pts, int64_t M, double2* out, unsigned long long* bad,
+                        cudaStream_t s) {
+  constexpr int W = 2 * MC + 1;
+  const int warps = 8;
+  const size_t smem = sizeof(double) * warps * (3 * W + W * W);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_gather_warp<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_gather_warp<MC><<<(unsigned)((M + warps - 1) / warps), warps * 32, smem, s>>>(
+      pts, M, pl->map, pl->poly.dev, pl->poly.deg, pl->grid, pl->P[1], pl->P[2], out, bad);
+}
+
+int gather_warp(vfn_plan* p, const double* pts, int64_t M, double2* out, int64_t* bad_dev, cudaStream_t s) {
+  if (M == 0) return VFN_OK;
+  auto* bad = reinterpret_cast<unsigned long long*>(bad_dev);
+  switch (p->m) {
+    case 1: launch_warp<1>(p, pts, M, out, bad, s); break;
+    case 2: launch_warp<2>(p, pts, M, out, bad, s); break;
+    case 3: launch_warp<3>(p, pts, M, out, bad, s); break;
+    case 4: launch_warp<4>(p, pts, M, out, bad, s); break;
+    case 5: launch_warp<5>(p, pts, M, out, bad, s); break;
+    case 6: launch_warp<6>(p, pts, M, out, bad, s); break;
+    case 7: launch_warp<7>(p, pts, M, out, bad, s); break;
+    case 8: launch_warp<8>(p, pts, M, out, bad, s); break;
+    case 9: launch_warp<9>(p, pts, M, out, bad, s); break;
+    case 10: launch_warp<10>(p, pts, M, out, bad, s); break;
+    case 11: launch_warp<11>(p, pts, M, out, bad, s); break;
+    case 12: launch_warp<12>(p, pts, M, out, bad, s); break;
+    case 13: launch_warp<13>(p, pts, M, out, bad, s); break;
+    default: return fail(VFN_ERR_INVALID, "cutoff must be in 1..13");
+  }
+  VFN_CUDA(cudaGetLastError());
+  return VFN_OK;
+}
+
 template <int MC>
 static void launch_simple(vfn_plan* pl, const double* pts, int64_t M, const int32_t* perm,
                           double2* out, cudaStream_t s) {

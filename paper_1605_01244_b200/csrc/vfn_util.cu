@@ -60,3 +60,22 @@ extern "C" int vfn_bench_fp64_peak(int device, double seconds, double* tflops, d
   if (sm_clock_mhz) *sm_clock_mhz = clk / 1e3;
   return VFN_OK;
 }
+
+namespace vfn {
+
+// *dst = *src by one device thread; dst is mapped pinned host memory, so the
+// host reads the word after the stream synchronises without a copy-engine D2H
+// (reset: src is restored to the 0x7f.. sentinel for the next call)
+__global__ void k_store_word(int64_t* __restrict__ src, volatile int64_t* dst, bool reset) {
+  *dst = *src;
+  if (reset) *src = 0x7f7f7f7f7f7f7f7fLL;
+  __threadfence_system();
+}
+
+int store_word(int64_t* src, int64_t* dst, cudaStream_t s, bool reset) {
+  k_store_word<<<1, 1, 0, s>>>(src, dst, reset);
+  VFN_CUDA(cudaGetLastError());
+  return VFN_OK;
+}
+
+}  // namespace vfn

@@ -225,6 +225,12 @@ def eval_direct(spec, points):
     return out
 
 
+# Evaluates of at most this many points run the unbinned warp-per-point
+# gather (one launch instead of ~25; include/vfnfft.h VFN_WARP_MAX_M).  Its
+# values agree with the binned gather's to rounding, not bitwise.
+WARP_MAX_M = 32768
+
+
 class NufftPlan:
     """Reusable evaluator for one SpectralField (nufft.py:190-272).
 
@@ -259,6 +265,7 @@ class NufftPlan:
         self._beta = _kb_beta(params.cutoff, params.oversampling)
         self._modes = shape
         self._handle = None
+        self._gather = 0
         on_dev = 1 if _is_cuda_tensor(coeffs) else 0
         if not on_dev:
             coeffs = np.ascontiguousarray(np.asarray(coeffs), dtype=np.complex128)
@@ -292,8 +299,11 @@ class NufftPlan:
         return out
 
     def set_gather(self, variant: int) -> None:
-        """0 = automatic, 1 = thread-per-point gather, 2 = DMMA box gather."""
+        """0 = automatic (the warp-per-point gather up to WARP_MAX_M points, the
+        binned tensor-core gather above), 1 = thread-per-point gather, 2 = DMMA
+        box gather, 3 = unbinned warp-per-point gather."""
         _lib.check(_lib.load().vfn_plan_set_gather(self._handle, int(variant)))
+        self._gather = int(variant)
 
     def set_graphs(self, enable: bool) -> None:
         """Replay small evaluates (M <= 2^19) as one CUDA graph when the call
@@ -360,6 +370,8 @@ class NufftPlan:
         (profiles/r01/launches_c5_v8.md lists them)."""
         if M == 0:
             return 0
+        if (self._gather == 0 and M <= WARP_MAX_M) or self._gather == 3:
+            return 2  # unbinned warp-per-point gather + the bad-row store
         box, tile = self.geometry(M)
         ntiles = 1
         for d in range(3):

@@ -66,3 +66,13 @@ def test_invalid_arguments_fail_without_a_gpu():
                              _lib.f64x3((1, 1, 1)), 1.5, 6, ctypes.c_void_p(1), 0, None)
     assert st == _lib.VFN_ERR_INVALID
     assert "even" in lib.vfn_last_error().decode()
+
+
+def test_warp_threshold_matches_header():
+    """The Python launch accounting uses the header's VFN_WARP_MAX_M."""
+    import re
+
+    from paper_1605_01244_b200 import nufft
+
+    hdr = open(os.path.join(REPO, "include", "vfnfft.h")).read()
+    assert int(re.search(r"#define VFN_WARP_MAX_M (\d+)", hdr).group(1)) == nufft.WARP_MAX_M

@@ -96,4 +96,9 @@ def test_random_configuration(vfb, seed):
     # a point's value does not depend on the other points of the call
     if bxy != 0 and len(pts) > 1:
         part = rng.choice(len(pts), max(1, len(pts) // 3), replace=False)
-        np.testing.assert_array_equal(plan.evaluate(pts[part]), out[part])
+        W = vfb.nufft.WARP_MAX_M
+        if (len(part) <= W) == (len(pts) <= W):  # same gather path: bitwise
+            np.testing.assert_array_equal(plan.evaluate(pts[part]), out[part])
+        else:  # warp-per-point vs binned: rounding
+            l2, linf = rel_err(plan.evaluate(pts[part]), out[part])
+            assert l2 < 1e-14 * amp and linf < 1e-14 * amp

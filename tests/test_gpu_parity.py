@@ -114,7 +114,7 @@ def test_evaluate_matches_reference(vfb, i):
         assert np.abs(out - c["direct"]).max() <= 1e-12 * mass
 
 
-@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("variant", [1, 2, 3])
 def test_gather_variants_agree(vfb, variant):
     c = CASES[0]
     _, plan = make_plan(vfb, c)
@@ -178,15 +178,28 @@ def test_plan_reuse_is_bitwise_stable(vfb, offset_box):
 
 
 def test_batch_composition_invariance(vfb, offset_box):
-    """A point's value does not depend on which other points share the call."""
+    """A point's value does not depend on which other points share the call,
+    on either gather (binned tensor-core: set_gather(2); warp per point: 3);
+    the automatic choice by M switches between them, whose values agree to
+    rounding."""
     spec = random_spectral(offset_box, (16, 16, 16), 90)
     rng = np.random.default_rng(91)
-    pts = rng.uniform(offset_box.a, offset_box.b, (30000, 3))
+    pts = rng.uniform(offset_box.a, offset_box.b, (50000, 3))
     plan = vfb.NufftPlan(spec)
-    full = plan.evaluate(pts)
-    np.testing.assert_array_equal(full[:777], plan.evaluate(pts[:777]))
+    plan.set_box(2)  # the automatic box width depends on M (density)
     sel = rng.permutation(len(pts))[:5000]
-    np.testing.assert_array_equal(full[sel], plan.evaluate(pts[sel]))
+    fulls = []
+    for variant in (2, 3):
+        plan.set_gather(variant)
+        full = plan.evaluate(pts)
+        np.testing.assert_array_equal(full[:777], plan.evaluate(pts[:777]))
+        np.testing.assert_array_equal(full[sel], plan.evaluate(pts[sel]))
+        fulls.append(full)
+    l2, linf = rel_err(fulls[1], fulls[0])
+    assert l2 < 1e-14 and linf < 1e-14, (l2, linf)
+    plan.set_gather(0)
+    np.testing.assert_array_equal(plan.evaluate(pts), fulls[0])          # 50000 > WARP_MAX_M
+    np.testing.assert_array_equal(plan.evaluate(pts[sel]), fulls[1][sel])  # 5000 <= WARP_MAX_M
 
 
 def test_torch_cuda_tensors_match_numpy(vfb, offset_box):
@@ -349,6 +362,12 @@ def test_config2_full_size(vfb):
     l2, linf = rel_err(out[sub], ref)
     assert l2 < TOL and linf < TOL
     assert l2 < 1e-13 and linf < 1e-13, (l2, linf)
+    # 20000 points take the warp-per-point gather: rounding-level agreement;
+    # on the binned gather with the full call's box width: bitwise
+    l2, linf = rel_err(plan.evaluate(pts[sub]), out[sub])
+    assert l2 < 1e-14 and linf < 1e-14, (l2, linf)
+    plan.set_gather(2)
+    plan.set_box(plan.geometry(len(pts))[0][0])
     np.testing.assert_array_equal(out[sub], plan.evaluate(pts[sub]))
 
 
@@ -562,6 +581,41 @@ def test_shared_plan_from_several_threads(vfb, offset_box):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("m", [1, 2, 4, 6, 9, 13])
+def test_warp_gather_small_evaluates(vfb, offset_box, m):
+    """The unbinned warp-per-point gather (automatic up to WARP_MAX_M points):
+    vs the oracle at every cutoff family (W = 3 .. 27 lanes per row), M = 1,
+    the threshold itself, outside / NaN rows reported with the reference's
+    text, device and host inputs bitwise equal."""
+    import torch
+
+    spec = random_spectral(offset_box, (10, 14, 12), 500 + m)
+    rng = np.random.default_rng(510 + m)
+    a, b = np.array(offset_box.a), np.array(offset_box.b)
+    plan = vfb.NufftPlan(spec, vfb.NufftParams(cutoff=m, eps=0.999))
+    grid, n, beta = O.oversampled_grid(spec.coeffs, offset_box.a, offset_box.b, 2.0, m)
+    for M in (1, 777, vfb.nufft.WARP_MAX_M):
+        pts = rng.uniform(a, b, (M, 3))
+        out = plan.evaluate(pts)
+        assert plan.launch_count(M) == 2
+        sub = np.arange(M) if M < 2000 else rng.choice(M, 2000, replace=False)
+        ref = O.gather_eval(grid, n, m, beta, pts[sub], offset_box.a, offset_box.b)
+        l2, linf = rel_err(out[sub], ref)
+        tol = 1e-13 if m >= 3 else 1e-11
+        assert l2 < tol and linf < tol, (m, M, l2, linf)
+        dev = plan.evaluate(torch.as_tensor(pts, device="cuda"))
+        np.testing.assert_array_equal(dev.cpu().numpy(), out)
+    pts = rng.uniform(a, b, (500, 3))
+    pts[[123, 400], 1] = [b[1] + 0.5, np.nan]
+    with pytest.raises(ValueError, match=r"\(row 123\) lies outside"):
+        plan.evaluate(pts)
+    pts[123, 1] = a[1]
+    with pytest.raises(ValueError, match=r"\(row 400\) lies outside"):
+        plan.evaluate(pts)
+    pts[400, 1] = a[1]
+    plan.evaluate(pts)  # the bad-row word was reset: a clean call passes
+
+
 def test_cuda_graph_replay_matches_eager(vfb, offset_box):
     """Repeated small evaluates replay one CUDA graph (second call captures):
     values bitwise equal to the eager launches, new point values in the same
@@ -575,6 +629,8 @@ def test_cuda_graph_replay_matches_eager(vfb, offset_box):
     graphed = vfb.NufftPlan(spec)
     eager = vfb.NufftPlan(spec)
     eager.set_graphs(False)
+    for plan in (graphed, eager):
+        plan.set_gather(2)  # the binned path (graphs); small M would take the warp path
     for i in range(7):
         p = batches[i % 3]
         np.testing.assert_array_equal(graphed.evaluate(p), eager.evaluate(p))
@@ -642,7 +698,7 @@ def test_tiny_and_anisotropic_grids(vfb, offset_box, shape, m):
     plan = vfb.NufftPlan(spec, vfb.NufftParams(cutoff=m, eps=0.999))
     grid, n, beta = O.oversampled_grid(spec.coeffs, offset_box.a, offset_box.b, 2.0, m)
     ref = O.gather_eval(grid, n, m, beta, pts, offset_box.a, offset_box.b)
-    for variant in (0, 1):
+    for variant in (0, 1, 3):
         plan.set_gather(variant)
         l2, linf = rel_err(plan.evaluate(pts), ref)
         assert l2 < 1e-12 and linf < 1e-12, (shape, m, variant, l2, linf)
