@@ -521,6 +521,14 @@ int64_t warp_max_m() {
   return v;
 }
 
+// Host-buffer evaluates of at least this many points run pipelined
+// (chunked H2D / evaluate / D2H); env VFN_PIPE_MIN overrides.
+int64_t pipe_min_m() {
+  int64_t v = (int64_t)1 << 23;
+  if (const char* e = std::getenv("VFN_PIPE_MIN")) v = std::max<int64_t>(2, std::atoll(e));
+  return v;
+}
+
 int64_t max_batch() {
   int64_t b = (int64_t)1 << 30;
   if (const char* e = std::getenv("VFN_MAX_BATCH")) b = std::max<int64_t>(1 << 10, std::atoll(e));
@@ -763,8 +771,7 @@ int vfn_plan_eval(vfn_plan* p, const double* points, int64_t M, double* out, int
   if (M == 0) return VFN_OK;
   DeviceGuard guard(p->device);
   cudaStream_t s = as_stream(stream);
-  if (!on_device && M >= ((int64_t)1 << 23))
-    return eval_host_pipelined(p, points, M, out, first_bad_row, s);
+  if (!on_device && M >= pipe_min_m()) return eval_host_pipelined(p, points, M, out, first_bad_row, s);
   if (M > max_batch()) return eval_device_batches(p, points, M, out, on_device, first_bad_row, s);
   VFN_CUDA(cudaEventRecord(p->ev[0], s));
   const void* pdev = nullptr;

@@ -346,6 +346,38 @@ def test_acceptance_geometry_grid_and_points(vfb):
 # ---------------------------------------------------------------- full-size properties
 
 
+def test_config5_full_size(vfb):
+    """BASELINE config 5 at full size on one GPU: N = 256^3 (decay 4096),
+    2^28 uniform points generated on the device.  A 6000-point subset is
+    checked against the oracle's gather on the same grid, and 2^20 of the
+    points re-evaluated alone on the binned gather with the full call's box
+    width are bitwise the full call's values."""
+    import torch
+
+    from paper_1605_01244_b200 import workloads
+
+    w = workloads.WORKLOADS["c5"]
+    coeffs = workloads.coefficients("c5")
+    a, b = w.box
+    plan = vfb.NufftPlan(vfb.SpectralField(vfb.DomainBox(a, b), torch.as_tensor(coeffs, device="cuda")))
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(2005)
+    pts = torch.rand((w.npoints, 3), dtype=torch.float64, device="cuda", generator=gen) - 0.5
+    out = plan.evaluate(pts)
+    sub = torch.as_tensor(np.random.default_rng(5).choice(w.npoints, 6000, replace=False), device="cuda")
+    psub = pts[sub].cpu().numpy()
+    ref = O.nufft_eval(coeffs, a, b, psub)
+    l2, linf = rel_err(out[sub].cpu().numpy(), ref)
+    assert l2 < 1e-13 and linf < 1e-13, (l2, linf)
+    box = plan.geometry(w.npoints)[0][0]
+    part = pts[: 1 << 20]
+    plan.set_gather(2)
+    plan.set_box(box)
+    assert torch.equal(plan.evaluate(part), out[: 1 << 20])
+    del pts, out, part
+    torch.cuda.empty_cache()
+
+
 def test_config2_full_size(vfb):
     """BASELINE config 2 (64^3 modes, 1e6 points): a 20k-point subset against
     the oracle, the whole batch for determinism and batch invariance."""
