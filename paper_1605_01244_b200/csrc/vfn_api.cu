@@ -156,6 +156,7 @@ int choose_geometry(vfn_plan* p, int64_t M, const double* pts_dev, cudaStream_t 
   }
   const double cells = (double)p->n[0] * (double)p->n[1] * (double)p->n[2];
   p->col_density = 8.0 * (double)M / cells;  // mean; the sample below sees clustering
+  p->col_density_M = M;
   if (bxy == 0) {
     bxy = M >= cells ? 1 : 2;
     if (pts_dev && tc_supported(p->m) && p->has_tmap && M >= (int64_t)1 << 20) {
@@ -467,6 +468,13 @@ int eval_enqueue(vfn_plan* p, const double* pts_dev, int64_t M, double2* out_dev
     g = *fixed;
     p->last_geom = g;
     p->has_last_geom = true;
+    // later chunks / batches of one call: same point distribution, so the
+    // column density (CTA size choice only; values do not depend on it)
+    // scales with the chunk's point count
+    if (p->col_density_M > 0) {
+      p->col_density *= (double)M / (double)p->col_density_M;
+      p->col_density_M = M;
+    }
   } else {
     VFN_CHECK(choose_geometry(p, M, pts_dev, s, &g));
   }

@@ -31,6 +31,7 @@
 #include <cuda.h>
 
 #include <climits>
+#include <cstdlib>
 
 #include <cub/device/device_scan.cuh>
 
@@ -42,7 +43,7 @@ namespace tc {
 
 constexpr int kUnitPts = 8;
 // warps per CTA: 16 (128 registers each) keep the FP64 pipe fullest on
-// dense tiles; sparse tiles (< ~8 points per 1x1x8 column, e.g. 1e6 points on
+// dense tiles; sparse tiles (< ~5 points per 1x1x8 column, e.g. 1e6 points on
 // 128^3) have too few units per staged tile for 16 warps and run 12
 constexpr int kWarpsDense = 16, kWarpsSparse = 12;
 constexpr int kSZ = 20;                   // staged z extent (TZ + 2m)
@@ -649,7 +650,10 @@ static int launch(vfn_plan* p, const tc::Args& A, cudaStream_t s) {
 
 template <int MC>
 static int launch_m(vfn_plan* p, const tc::Args& A, int bxy, cudaStream_t s) {
-  const bool sparse = p->col_density < 8.0;  // points per 1x1x8 column (choose_geometry)
+  // 12-warp CTAs below ~5 points per 1x1x8 column (config 2 at 3.8; a 0.12
+  // chunk of c5 at 1.9), 16 above (a 0.38 chunk of c5 at 6.1: 66.4 -> 62.7 ms)
+  bool sparse = p->col_density < 5.0;
+  if (const char* e = std::getenv("VFN_WARPS")) sparse = std::atoi(e) == tc::kWarpsSparse;  // experiments
   if (bxy == 1)
     return sparse ? launch<MC, 1, tc::kWarpsSparse>(p, A, s) : launch<MC, 1, tc::kWarpsDense>(p, A, s);
   return sparse ? launch<MC, 2, tc::kWarpsSparse>(p, A, s) : launch<MC, 2, tc::kWarpsDense>(p, A, s);
