@@ -306,6 +306,28 @@ def test_rectilinear_out_argument_and_slabs(vfb):
         vfb.eval_rectilinear(vfb.SpectralField(box, coeffs), ys, out=np.empty((1, 1, 1), complex))
 
 
+def test_rectilinear_axis_permutation_and_single_point(vfb, offset_box):
+    """Properties the reference tests for the rectilinear path
+    (test_rectilinear.py): permuting the axes of the coefficients, the box and
+    the coordinate lists permutes the output (rtol 1e-12); a 1x1x1 grid
+    equals the exact sum at that point (rel 1e-13)."""
+    rng = np.random.default_rng(600)
+    spec = random_spectral(offset_box, (6, 8, 10), 601)
+    a, b = np.array(offset_box.a), np.array(offset_box.b)
+    ys = [np.sort(rng.uniform(a[d], b[d], n)) for d, n in enumerate((5, 7, 9))]
+    out = vfb.eval_rectilinear(spec, ys)
+    perm = (2, 0, 1)
+    pbox = vfb.DomainBox(tuple(a[list(perm)]), tuple(b[list(perm)]))
+    pspec = vfb.SpectralField(pbox, np.ascontiguousarray(spec.coeffs.transpose(perm)))
+    pout = vfb.eval_rectilinear(pspec, [ys[d] for d in perm])
+    np.testing.assert_allclose(pout, out.transpose(perm), rtol=1e-12, atol=1e-12 * np.abs(out).max())
+    x = np.array([[ys[0][2], ys[1][3], ys[2][4]]])
+    one = vfb.eval_rectilinear(spec, [x[:, 0], x[:, 1], x[:, 2]])[0, 0, 0]
+    direct = O.ndft(spec.coeffs, offset_box.a, offset_box.b, x)[0]
+    assert abs(one - direct) <= 1e-13 * abs(direct)
+    assert abs(vfb.eval_direct(spec, x)[0] - direct) <= 1e-13 * abs(direct)
+
+
 def test_rectilinear_regular_grid_matches_fft(vfb, offset_box):
     spec = random_spectral(offset_box, (12, 12, 12), 43)
     axes = vfb.regular_grid(offset_box, spec.coeffs.shape)
