@@ -101,6 +101,10 @@ BinGeom make_geometry(const vfn_plan* p, int bxy) {
   }
   g.boxes_per_tile = g.nbox[0] * g.nbox[1] * g.nbox[2];
   g.cells_per_box = g.box[0] * g.box[1] * g.box[2];
+  for (int d = 0; d < 3; ++d) {
+    g.tile_inv[d] = (((uint64_t)1 << 32) + (uint64_t)g.tile[d] - 1) / (uint64_t)g.tile[d];
+    g.box_inv[d] = (((uint64_t)1 << 32) + (uint64_t)g.box[d] - 1) / (uint64_t)g.box[d];
+  }
   g.ntiles = (int64_t)g.ntile[0] * g.ntile[1] * g.ntile[2];
   g.nboxes = g.ntiles * g.boxes_per_tile;
   return g;

@@ -32,7 +32,10 @@ namespace vfn {
 // nufft.py:81-92 evaluated by numpy.
 __device__ __forceinline__ double torus_coord(double x, double a, double amb) {
   double t = __ddiv_rn(__dsub_rn(x, a), amb);
-  double r = fmod(t, 1.0);
+  // fmod(t, 1) exactly: t - trunc(t) is exact for every finite t (the
+  // fraction bits of t), NaN for +-inf like fmod; only the sign of an exact
+  // zero differs, and zero is normalised to +0 below
+  double r = __dsub_rn(t, trunc(t));
   if (r != 0.0) {
     if (r < 0.0) r = __dadd_rn(r, 1.0);
   } else {

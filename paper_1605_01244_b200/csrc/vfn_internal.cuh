@@ -112,6 +112,9 @@ struct BinGeom {
   int cells_per_box;  // key = (tile * boxes_per_tile + box) * cells_per_box + cell
   int64_t ntiles;
   int64_t nboxes;  // ntiles * boxes_per_tile
+  // ceil(2^32 / d) for d = tile[k], box[k]: floor(x / d) = (x * inv) >> 32
+  // exactly for x < 2^21 and d <= 64 (cell indices; see quot())
+  uint64_t tile_inv[3], box_inv[3];
 };
 
 // Window polynomial table: w_j(delta) = sum_d coef[j*(deg+1) + d] delta^d,

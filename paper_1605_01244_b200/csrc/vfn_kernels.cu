@@ -101,10 +101,12 @@ __global__ void k_map_key(const double* __restrict__ pts, int64_t M, TorusMap tm
   int t[3], in[3], c[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    t[d] = cell[d] / g.tile[d];
+    // exact quotients by multiply-shift (cells < 2^20, tile/box sizes <= 64)
+    t[d] = (int)(((uint64_t)cell[d] * g.tile_inv[d]) >> 32);
     const int r = cell[d] - t[d] * g.tile[d];
-    in[d] = r / g.box[d];
+    in[d] = (int)(((uint64_t)r * g.box_inv[d]) >> 32);
     c[d] = r - in[d] * g.box[d];
+    VFN_DCHECK(t[d] == cell[d] / g.tile[d] && in[d] == r / g.box[d]);
   }
   int64_t tile_id = ((int64_t)t[0] * g.ntile[1] + t[1]) * g.ntile[2] + t[2];
   int box_id = (in[0] * g.nbox[1] + in[1]) * g.nbox[2] + in[2];
