@@ -188,6 +188,7 @@ const char* vfn_last_error(void) { return last_error_cstr(); }
 int vfn_plan_create(vfn_plan** out, int device, const int64_t nmodes[3], const double a[3],
                     const double b[3], double sigma, int m, const double* coeffs,
                     int coeffs_on_device, void* stream) {
+  vfn::NvtxRange nvtx_range("vfn plan build");
   if (!out || !nmodes || !a || !b || !coeffs) return fail(VFN_ERR_INVALID, "null argument");
   *out = nullptr;
   if (m < 1 || m > 13) return fail(VFN_ERR_INVALID, "cutoff must be in 1..13");
@@ -431,6 +432,7 @@ static int bin_points(vfn_plan* p, const double* points, int64_t M, int on_devic
 
 int vfn_plan_bin(vfn_plan* p, const double* points, int64_t M, uint32_t* keys, int32_t* perm,
                  int on_device, int64_t* first_bad_row, void* stream) {
+  vfn::NvtxRange nvtx_range("vfn bin");
   if (!p || (M > 0 && (!points || !keys || !perm))) return fail(VFN_ERR_INVALID, "null argument");
   std::lock_guard<std::mutex> plan_lock(p->mu);
   if (M < 0 || M > INT32_MAX) return fail(VFN_ERR_INVALID, "point count out of range");
@@ -467,6 +469,7 @@ constexpr int64_t kBadSentinel = 0x7f7f7f7f7f7f7f7fLL;
 // then the gather.  bad_dev receives the first out-of-domain row (relative).
 int eval_enqueue(vfn_plan* p, const double* pts_dev, int64_t M, double2* out_dev, int64_t* bad_dev,
                  cudaStream_t s, const BinGeom* fixed) {
+  vfn::NvtxRange nvtx_range("vfn evaluate batch (bin + gather)");
   BinGeom g;
   if (fixed) {
     g = *fixed;
@@ -693,6 +696,7 @@ double host_column_density(const vfn_plan* p, const double* pts, int64_t M) {
 
 int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* out,
                         int64_t* first_bad_row, cudaStream_t s) {
+  vfn::NvtxRange nvtx_range("vfn evaluate pipelined (host buffers)");
   // Each chunk's gather re-reads every grid tile its points touch, so small
   // chunks cost tile traffic (c5, 2^28 points: 2 equal chunks 254 ms, 3 equal
   // 244 ms, 4 equal 270 ms, 8 equal 380 ms; unpipelined 347 ms).  From 2^26
@@ -809,6 +813,7 @@ extern "C" {
 
 int vfn_plan_eval(vfn_plan* p, const double* points, int64_t M, double* out, int on_device,
                   int64_t* first_bad_row, void* stream) {
+  vfn::NvtxRange nvtx_range("vfn evaluate");
   if (!p || (M > 0 && (!points || !out))) return fail(VFN_ERR_INVALID, "null argument");
   std::lock_guard<std::mutex> plan_lock(p->mu);
   if (M < 0) return fail(VFN_ERR_INVALID, "point count out of range");
@@ -866,6 +871,7 @@ int vfn_rect_eval(int device, const int64_t nmodes[3], const double a[3], const 
                   const double* coeffs, const double* y1, int64_t M1, const double* y2,
                   int64_t M2, const double* y3, int64_t M3, double* out, int on_device,
                   void* stream) {
+  vfn::NvtxRange nvtx_range("vfn rectilinear");
   if (!nmodes || !a || !b || !coeffs || !out) return fail(VFN_ERR_INVALID, "null argument");
   VFN_CHECK(check_box(a, b));
   for (int d = 0; d < 3; ++d)

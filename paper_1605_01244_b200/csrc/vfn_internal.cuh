@@ -3,6 +3,8 @@
 
 #include <cstdint>
 #include <mutex>
+
+#include <nvtx3/nvToolsExt.h>
 #include <cstdio>
 #include <string>
 
@@ -32,6 +34,15 @@ int fail(int code, const std::string& msg);
   } while (0)
 
 // Restores the caller's current device on scope exit.
+// NVTX range for the duration of a scope (visible in Nsight Systems /
+// Compute timelines; header-only NVTX3, a no-op without an attached tool)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {

@@ -223,6 +223,7 @@ static int grid_blocks(int64_t total) {
 }
 
 int build_grid(vfn_plan* p, const double* coeffs_dev, cudaStream_t s) {
+  vfn::NvtxRange nvtx_range("vfn grid: deconvolve + pad + FFT + halo");
   const int64_t N0 = p->N[0], N1 = p->N[1], N2 = p->N[2];
   const int64_t n0 = p->n[0], n1 = p->n[1], n2 = p->n[2];
   // sign(k)/phihat tables

@@ -235,6 +235,7 @@ TubeScratch* tube_scratch(int device) {
 int vfn_decompose(int device, const double* values, const int64_t shape[3], const double a[3],
                   const double b[3], const int mirror[3], double* coeffs_out, int on_device,
                   void* stream) {
+  vfn::NvtxRange nvtx_range("vfn decompose");
   if (!values || !shape || !a || !b || !mirror || !coeffs_out) return fail(VFN_ERR_INVALID, "null argument");
   for (int d = 0; d < 3; ++d)
     if (shape[d] <= 0 || !(a[d] < b[d])) return fail(VFN_ERR_INVALID, "bad shape or domain");
@@ -266,6 +267,7 @@ int vfn_tube_eval(vfn_tube** out, int device, const double* values, const int64_
                   const double a[3], const double b[3], const int mirror[3],
                   const double* thresholds, int nthr, int has_filter, double final_filter,
                   double sigma, int m, int64_t* count, int* no_seeds, void* stream) {
+  vfn::NvtxRange nvtx_range("vfn tube_eval");
   if (!out || !values || !shape || !a || !b || !mirror || !thresholds || !count || !no_seeds)
     return fail(VFN_ERR_INVALID, "null argument");
   if (nthr < 1) return fail(VFN_ERR_INVALID, "thresholds must be a nonempty sequence of positive values");
