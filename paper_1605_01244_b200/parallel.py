@@ -62,3 +62,18 @@ def evaluate_sharded(plan, points, rank: int, world: int, out=None):
     """Evaluate this rank's contiguous block of `points` (global array) with `plan`."""
     lo, hi = shard_range(points.shape[0], world, rank)
     return plan.evaluate(points[lo:hi], out=out)
+
+
+def eval_rectilinear_sharded(spec, coords, rank: int, world: int, evaluator=None):
+    """This rank's slab of a rectilinear evaluation: the
+    (replicated, broadcast) coefficients are contracted for the rank's
+    contiguous block of axis-1 coordinates only, so each rank produces
+    output rows [lo, hi) of the (M1, M2, M3) grid and no collective is
+    needed beyond the coefficient broadcast; `gather_results` on the
+    flattened slabs (or writing them in place) assembles the grid.  Values
+    agree with the unsharded call to rounding (the last pass's GEMM shape
+    changes with the slab).  `evaluator` defaults to `eval_rectilinear`."""
+    if evaluator is None:
+        from .rectilinear import eval_rectilinear as evaluator
+    lo, hi = shard_range(len(coords[0]), world, rank)
+    return evaluator(spec, [coords[0][lo:hi], coords[1], coords[2]])

@@ -328,6 +328,24 @@ def test_rectilinear_axis_permutation_and_single_point(vfb, offset_box):
     assert abs(vfb.eval_direct(spec, x)[0] - direct) <= 1e-13 * abs(direct)
 
 
+def test_rectilinear_slabs_per_rank(vfb, offset_box):
+    """parallel.eval_rectilinear_sharded: the axis-1 slabs of 1, 2, 3 and 5
+    ranks (evaluated here one after another on this GPU) concatenate to
+    the unsharded grid within 1e-14 (last-pass GEMM shapes differ)."""
+    from paper_1605_01244_b200.parallel import eval_rectilinear_sharded
+
+    rng = np.random.default_rng(700)
+    spec = random_spectral(offset_box, (12, 10, 8), 701)
+    a, b = np.array(offset_box.a), np.array(offset_box.b)
+    coords = [np.sort(rng.uniform(a[d], b[d], n)) for d, n in enumerate((37, 20, 16))]
+    full = vfb.eval_rectilinear(spec, coords)
+    for world in (1, 2, 3, 5):
+        slabs = [eval_rectilinear_sharded(spec, coords, r, world) for r in range(world)]
+        got = np.concatenate(slabs, axis=0)
+        l2, linf = rel_err(got, full)
+        assert got.shape == full.shape and l2 < 1e-14 and linf < 1e-14, (world, l2, linf)
+
+
 def test_rectilinear_regular_grid_matches_fft(vfb, offset_box):
     spec = random_spectral(offset_box, (12, 12, 12), 43)
     axes = vfb.regular_grid(offset_box, spec.coeffs.shape)
