@@ -99,6 +99,6 @@ def test_random_configuration(vfb, seed):
         W = vfb.nufft.WARP_MAX_M
         if (len(part) <= W) == (len(pts) <= W):  # same gather path: bitwise
             np.testing.assert_array_equal(plan.evaluate(pts[part]), out[part])
-        else:  # warp-per-point vs binned: rounding
+        else:  # warp-per-point vs binned: both within tol of the oracle
             l2, linf = rel_err(plan.evaluate(pts[part]), out[part])
-            assert l2 < 1e-14 * amp and linf < 1e-14 * amp
+            assert l2 < 2 * tol and linf < 2 * tol, (seed, l2, linf)
