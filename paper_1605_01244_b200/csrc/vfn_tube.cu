@@ -14,6 +14,8 @@
 #include <cmath>
 #include <map>
 #include <mutex>
+#include <cstring>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -449,9 +451,59 @@ int vfn_tube_copy(const vfn_tube* t, double* points, double* density, int64_t* l
   if (t->count == 0) return VFN_OK;
   if (!points || !density || !level) return fail(VFN_ERR_INVALID, "null argument");
   DeviceGuard guard(t->device);
-  VFN_CUDA(cudaMemcpy(points, t->points.ptr, sizeof(double) * 3 * t->count, cudaMemcpyDeviceToHost));
-  VFN_CUDA(cudaMemcpy(density, t->density.ptr, sizeof(double) * t->count, cudaMemcpyDeviceToHost));
-  VFN_CUDA(cudaMemcpy(level, t->level.ptr, sizeof(int64_t) * t->count, cudaMemcpyDeviceToHost));
+  const size_t nb[3] = {sizeof(double) * 3 * t->count, sizeof(double) * t->count, sizeof(int64_t) * t->count};
+  const void* src[3] = {t->points.ptr, t->density.ptr, t->level.ptr};
+  void* dst[3] = {points, density, level};
+  const size_t total = nb[0] + nb[1] + nb[2];
+  if (total < ((size_t)1 << 20)) {
+    for (int i = 0; i < 3; ++i) VFN_CUDA(cudaMemcpy(dst[i], src[i], nb[i], cudaMemcpyDeviceToHost));
+    return VFN_OK;
+  }
+  // Large clouds (the caller's arrays are fresh pageable numpy memory): D2H
+  // at pinned speed into a per-device grow-only staging buffer, then copy
+  // out with several host threads (the page faults of the fresh arrays
+  // dominate a single-threaded copy)
+  struct Stage {
+    std::mutex mu;
+    void* ptr = nullptr;
+    size_t bytes = 0;
+  };
+  static std::mutex smu;
+  static std::map<int, Stage*> stages;
+  Stage* st;
+  {
+    std::lock_guard<std::mutex> lock(smu);
+    Stage*& slot = stages[t->device];
+    if (!slot) slot = new Stage();
+    st = slot;
+  }
+  std::lock_guard<std::mutex> lock(st->mu);
+  if (st->bytes < total) {
+    if (st->ptr) cudaFreeHost(st->ptr);
+    st->ptr = nullptr;
+    st->bytes = 0;
+    if (cudaMallocHost(&st->ptr, total) != cudaSuccess) {
+      cudaGetLastError();
+      st->ptr = nullptr;
+      for (int i = 0; i < 3; ++i) VFN_CUDA(cudaMemcpy(dst[i], src[i], nb[i], cudaMemcpyDeviceToHost));
+      return VFN_OK;
+    }
+    st->bytes = total;
+  }
+  char* stg = static_cast<char*>(st->ptr);
+  size_t off[3] = {0, nb[0], nb[0] + nb[1]};
+  for (int i = 0; i < 3; ++i) VFN_CUDA(cudaMemcpyAsync(stg + off[i], src[i], nb[i], cudaMemcpyDeviceToHost, 0));
+  VFN_CUDA(cudaStreamSynchronize(0));
+  const int nt = (int)std::min<size_t>(8, std::max(1u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> th;
+  for (int k = 0; k < nt; ++k)
+    th.emplace_back([&, k] {
+      for (int i = 0; i < 3; ++i) {
+        const size_t lo = nb[i] * k / nt, hi = nb[i] * (k + 1) / nt;
+        std::memcpy(static_cast<char*>(dst[i]) + lo, stg + off[i] + lo, hi - lo);
+      }
+    });
+  for (auto& x : th) x.join();
   return VFN_OK;
 }
 
