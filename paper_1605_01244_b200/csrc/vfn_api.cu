@@ -43,15 +43,25 @@ int check_box(const double a[3], const double b[3]) {
 }
 
 int stage_in(DevBuf& buf, const void* src, size_t bytes, int on_device, const void** dev,
-             cudaStream_t s) {
+             cudaStream_t s, HostStager* stager = nullptr) {
   if (on_device) {
     *dev = src;
     return VFN_OK;
   }
   VFN_CHECK(buf.ensure(bytes));
-  VFN_CUDA(cudaMemcpyAsync(buf.ptr, src, bytes, cudaMemcpyHostToDevice, s));
+  if (stager)
+    VFN_CHECK(stage_h2d(stager, buf.ptr, src, bytes, s));
+  else
+    VFN_CUDA(cudaMemcpyAsync(buf.ptr, src, bytes, cudaMemcpyHostToDevice, s));
   *dev = buf.ptr;
   return VFN_OK;
+}
+
+// The plan's pinned stager when `host` is pageable and large enough to matter.
+HostStager* stager_for(vfn_plan* p, const void* host, size_t bytes) {
+  if (bytes < ((size_t)1 << 20) || !is_pageable(host)) return nullptr;
+  if (!p->stager) p->stager = stager_create();
+  return p->stager;
 }
 
 // The sort's value input is iota (0..M-1); it never changes, so it is kept
@@ -289,6 +299,7 @@ int vfn_plan_destroy(vfn_plan* p) {
     if (p->graph_ev[i]) cudaEventDestroy(p->graph_ev[i]);
   if (p->graph_stream) cudaStreamDestroy(p->graph_stream);
   if (p->bad_host) cudaFreeHost(p->bad_host);
+  stager_destroy(p->stager);
   delete p;
   return VFN_OK;
 }
@@ -767,13 +778,29 @@ int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* ou
   int st = VFN_OK;
   BinGeom g;
   bool have_g = false;
+  // pageable user buffers: chunk copies go through the plan's pinned stager
+  // (host threads copy one piece while the DMA engine moves the previous);
+  // chunk i-1's output is staged out while chunk i computes
+  HostStager* st_in = stager_for(p, points, sizeof(double) * 3 * M);
+  HostStager* st_out = stager_for(p, out, sizeof(double2) * M);
+  auto stage_out = [&](int64_t j) -> int {
+    const int64_t lo = lo_of[j], n = lo_of[j + 1] - lo;
+    cudaStreamWaitEvent(sout, e_comp(j), 0);
+    VFN_CHECK(stage_d2h(st_out, out + 2 * lo, p->out.as<double2>() + chunk * (j & 1), sizeof(double2) * n, sout));
+    cudaEventRecord(e_out(j), sout);
+    return VFN_OK;
+  };
   VFN_CUDA(cudaEventRecord(p->ev[0], s));
   for (int64_t i = 0; i < nc && st == VFN_OK; ++i) {
     const int64_t lo = lo_of[i], n = lo_of[i + 1] - lo;
     double* pbuf = p->pts.as<double>() + 3 * chunk * (i & 1);
     double2* obuf = p->out.as<double2>() + chunk * (i & 1);
     if (i >= 2) cudaStreamWaitEvent(sin, e_comp(i - 2), 0);
-    cudaMemcpyAsync(pbuf, points + 3 * lo, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, sin);
+    if (st_in)
+      st = stage_h2d(st_in, pbuf, points + 3 * lo, sizeof(double) * 3 * n, sin);
+    else
+      cudaMemcpyAsync(pbuf, points + 3 * lo, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, sin);
+    if (st != VFN_OK) break;
     cudaEventRecord(e_in(i), sin);
     cudaStreamWaitEvent(s, e_in(i), 0);
     if (i >= 2) cudaStreamWaitEvent(s, e_out(i - 2), 0);
@@ -785,10 +812,15 @@ int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* ou
       have_g = true;
     }
     cudaEventRecord(e_comp(i), s);
-    cudaStreamWaitEvent(sout, e_comp(i), 0);
-    cudaMemcpyAsync(out + 2 * lo, obuf, sizeof(double2) * n, cudaMemcpyDeviceToHost, sout);
-    cudaEventRecord(e_out(i), sout);
+    if (st_out) {
+      if (i >= 1) st = stage_out(i - 1);
+    } else {
+      cudaStreamWaitEvent(sout, e_comp(i), 0);
+      cudaMemcpyAsync(out + 2 * lo, obuf, sizeof(double2) * n, cudaMemcpyDeviceToHost, sout);
+      cudaEventRecord(e_out(i), sout);
+    }
   }
+  if (st == VFN_OK && st_out) st = stage_out(nc - 1);
   std::vector<int64_t> bad(nc, kBadSentinel);
   if (st == VFN_OK) {
     cudaStreamWaitEvent(s, e_out(nc - 1), 0);
@@ -825,7 +857,9 @@ int vfn_plan_eval(vfn_plan* p, const double* points, int64_t M, double* out, int
   if (M > max_batch()) return eval_device_batches(p, points, M, out, on_device, first_bad_row, s);
   VFN_CUDA(cudaEventRecord(p->ev[0], s));
   const void* pdev = nullptr;
-  VFN_CHECK(stage_in(p->pts, points, sizeof(double) * 3 * M, on_device, &pdev, s));
+  HostStager* st_in = on_device ? nullptr : stager_for(p, points, sizeof(double) * 3 * M);
+  HostStager* st_out = on_device ? nullptr : stager_for(p, out, sizeof(double2) * M);
+  VFN_CHECK(stage_in(p->pts, points, sizeof(double) * 3 * M, on_device, &pdev, s, st_in));
   double2* out_dev = reinterpret_cast<double2*>(out);
   if (!on_device) {
     VFN_CHECK(p->out.ensure(sizeof(double2) * M));
@@ -847,7 +881,9 @@ int vfn_plan_eval(vfn_plan* p, const double* points, int64_t M, double* out, int
     VFN_CHECK(eval_graphed(p, static_cast<const double*>(pdev), M, out_dev, bad_dev, s, &graphed));
     if (!graphed) VFN_CHECK(eval_enqueue(p, static_cast<const double*>(pdev), M, out_dev, bad_dev, s, nullptr));
   }
-  if (!on_device)
+  if (st_out)
+    VFN_CHECK(stage_d2h(st_out, out, out_dev, sizeof(double2) * M, s));
+  else if (!on_device)
     VFN_CUDA(cudaMemcpyAsync(out, out_dev, sizeof(double2) * M, cudaMemcpyDeviceToHost, s));
   // first bad row -> mapped pinned host word, stored by a one-thread kernel
   // (a copy-engine D2H of 8 bytes adds ~10-20 us of latency to every call)
