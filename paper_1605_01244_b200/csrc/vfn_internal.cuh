@@ -218,6 +218,9 @@ namespace vfn {
 bool is_pageable(const void* host_ptr);
 HostStager* stager_create();
 void stager_destroy(HostStager* st);
+// process-wide stager of a device for plan-less calls (rectilinear); callers
+// serialise on their own per-device locks
+HostStager* device_stager(int device);
 int stage_h2d(HostStager* st, void* dst_dev, const void* src_host, size_t bytes, cudaStream_t s);
 int stage_d2h(HostStager* st, void* dst_host, const void* src_dev, size_t bytes, cudaStream_t s);
 

@@ -95,7 +95,9 @@ int rect_eval(int device, const int64_t nm[3], const double a[3], const double b
   const double* yd[3];
   if (!on_device) {
     if ((st = C.ensure(cb)) != VFN_OK) goto done;
-    if (cudaMemcpyAsync(C.ptr, coeffs, cb, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+    if (cb >= ((size_t)1 << 20) && is_pageable(coeffs)) {
+      if ((st = stage_h2d(device_stager(device), C.ptr, coeffs, cb, s)) != VFN_OK) goto done;
+    } else if (cudaMemcpyAsync(C.ptr, coeffs, cb, cudaMemcpyHostToDevice, s) != cudaSuccess) {
       st = fail(VFN_ERR_CUDA, "coefficient upload failed");
       goto done;
     }
@@ -148,6 +150,10 @@ int rect_eval(int device, const int64_t nm[3], const double a[3], const double b
       }
       for (auto& e : sc->ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     }
+    // pageable host output (a fresh numpy array): every slab's GEMM is
+    // enqueued first, then the slabs are staged out through pinned pieces
+    // while the later GEMMs run
+    const bool staged = !on_device && fb >= ((size_t)1 << 20) && is_pageable(out);
     for (int j = 0; j < nslab; ++j) {
       const int64_t lo = M0 * j / nslab, n = M0 * (j + 1) / nslab - lo;
       if (n == 0) continue;
@@ -156,12 +162,23 @@ int rect_eval(int device, const int64_t nm[3], const double a[3], const double b
                            reinterpret_cast<cuDoubleComplex*>(Fd) + lo * M1 * M2, (int)(M1 * M2)));
       if (!on_device) {
         cudaEventRecord(sc->ev[j], s);
+        if (staged) continue;
         cudaStreamWaitEvent(sc->copy, sc->ev[j], 0);
         if (cudaMemcpyAsync(out + 2 * lo * M1 * M2, Fd + lo * M1 * M2, sizeof(double2) * n * M1 * M2,
                             cudaMemcpyDeviceToHost, sc->copy) != cudaSuccess) {
           st = fail(VFN_ERR_CUDA, "result download failed");
           goto done;
         }
+      }
+    }
+    if (staged) {
+      for (int j = 0; j < nslab; ++j) {
+        const int64_t lo = M0 * j / nslab, n = M0 * (j + 1) / nslab - lo;
+        if (n == 0) continue;
+        cudaStreamWaitEvent(sc->copy, sc->ev[j], 0);
+        if ((st = stage_d2h(device_stager(device), out + 2 * lo * M1 * M2, Fd + lo * M1 * M2,
+                            sizeof(double2) * n * M1 * M2, sc->copy)) != VFN_OK)
+          goto done;
       }
     }
     if (!on_device) {

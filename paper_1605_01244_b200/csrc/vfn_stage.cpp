@@ -6,6 +6,8 @@
 // while the DMA engine moves the previous one.
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -58,6 +60,15 @@ void stager_destroy(HostStager* st) {
     if (st->ev_out[i]) cudaEventDestroy(st->ev_out[i]);
   }
   delete st;
+}
+
+HostStager* device_stager(int device) {
+  static std::mutex mu;
+  static std::map<int, HostStager*> st;
+  std::lock_guard<std::mutex> lock(mu);
+  HostStager*& s = st[device];
+  if (!s) s = stager_create();
+  return s;
 }
 
 static void par_copy(char* dst, const char* src, size_t n, int threads) {
