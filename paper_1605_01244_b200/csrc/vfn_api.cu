@@ -269,7 +269,9 @@ int vfn_plan_create(vfn_plan** out, int device, const int64_t nmodes[3], const d
   const size_t cbytes = sizeof(double2) * nmodes[0] * nmodes[1] * nmodes[2];
   DevBuf staging;
   const void* cdev = nullptr;
-  int st = stage_in(staging, coeffs, cbytes, coeffs_on_device, &cdev, s);
+  HostStager* cst = (!coeffs_on_device && cbytes >= ((size_t)1 << 20) && is_pageable(coeffs))
+                        ? device_stager(device) : nullptr;
+  int st = stage_in(staging, coeffs, cbytes, coeffs_on_device, &cdev, s, cst);
   if (st == VFN_OK) st = build_grid(p, static_cast<const double*>(cdev), s);
   if (st == VFN_OK) st = make_grid_tmap(p);
   staging.release();
