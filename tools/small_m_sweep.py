@@ -1,8 +1,8 @@
 """Per-call time of small evaluates on the unbinned warp-per-point gather
 (variant 3) vs the binned tensor-core path (variant 2, CUDA-graph replay),
 device-resident points, c1's plan (32^3 modes, 64^3 grid) and c2's (64^3
-modes, 128^3 grid): where the automatic switch (VFN_WARP_MAX_M) belongs.
-Usage: python tools/small_m_sweep.py"""
+modes, 128^3 grid), optionally c3 / c5's: where the automatic switch
+(VFN_WARP_MAX_M) belongs.  Usage: python tools/small_m_sweep.py [c1 c2 c3 c5]"""
 import os
 import sys
 
@@ -13,14 +13,19 @@ import paper_1605_01244_b200 as vfb
 from paper_1605_01244_b200 import workloads
 
 dev = torch.device("cuda", 0)
-for name in ("c1", "c2"):
+SIZES = {"c1": (1000, 4000, 10000, 16384, 32768, 65536, 131072, 262144),
+         "c2": (1000, 4000, 10000, 16384, 32768, 65536, 131072, 262144),
+         "c3": (32768, 131072, 262144, 524288),
+         "c5": (32768, 131072, 524288, 2097152)}
+for name in sys.argv[1:] or ("c1", "c2"):
     w = workloads.WORKLOADS[name]
     spec = vfb.SpectralField(vfb.DomainBox(*w.box), torch.as_tensor(workloads.coefficients(name)).to(dev))
     plan = vfb.NufftPlan(spec)
     g = torch.Generator(device=dev)
     g.manual_seed(7)
-    for M in (1000, 4000, 10000, 16384, 32768, 65536, 131072, 262144):
-        pts = torch.rand((M, 3), dtype=torch.float64, device=dev, generator=g) - 0.5
+    lo, hi = (torch.tensor(v, dtype=torch.float64, device=dev) for v in w.box)
+    for M in SIZES[name]:
+        pts = lo + (hi - lo) * torch.rand((M, 3), dtype=torch.float64, device=dev, generator=g)
         out = torch.empty(M, dtype=torch.complex128, device=dev)
         row = []
         for variant in (3, 2):
