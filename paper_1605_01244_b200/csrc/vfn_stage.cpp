@@ -21,6 +21,7 @@ constexpr int kRing = 3;                     // pieces per direction
 }  // namespace
 
 struct HostStager {
+  std::mutex mu;  // one transfer at a time (device stagers are shared by plan builds and rectilinear calls)
   char* in[kRing] = {};
   char* out[kRing] = {};
   cudaEvent_t ev_in[kRing] = {}, ev_out[kRing] = {};
@@ -92,6 +93,7 @@ int stage_h2d(HostStager* st, void* dst_dev, const void* src_host, size_t bytes,
     VFN_CUDA(cudaMemcpyAsync(dst_dev, src_host, bytes, cudaMemcpyHostToDevice, s));
     return VFN_OK;
   }
+  std::lock_guard<std::mutex> lock(st->mu);
   const char* src = static_cast<const char*>(src_host);
   char* dst = static_cast<char*>(dst_dev);
   for (size_t off = 0, k = 0; off < bytes; off += kPiece, ++k) {
@@ -112,6 +114,7 @@ int stage_d2h(HostStager* st, void* dst_host, const void* src_dev, size_t bytes,
     VFN_CUDA(cudaStreamSynchronize(s));
     return VFN_OK;
   }
+  std::lock_guard<std::mutex> lock(st->mu);
   const char* src = static_cast<const char*>(src_dev);
   char* dst = static_cast<char*>(dst_host);
   const size_t np = (bytes + kPiece - 1) / kPiece;
