@@ -234,7 +234,7 @@ int fit_window_poly(int m, double beta, double* coef, int max_deg);
 
 // ---------------------------------------------------------------- launchers
 // process-wide cuBLAS handle of `device` (cublasHandle_t; vfn_rect.cu)
-void* blas_handle(int device);
+void* blas_handle(int device);  // per (host thread, device)
 // in-place unnormalised forward Z2Z 3D FFT through a cached cuFFT plan
 int fft_forward(const int64_t n[3], double2* data, cudaStream_t s);
 int build_grid(vfn_plan* p, const double* coeffs_dev, cudaStream_t s);

@@ -27,16 +27,23 @@ __global__ void k_basis(const double* __restrict__ y, int64_t M, int64_t N, doub
   E[e] = make_double2(c * r, s * r);
 }
 
+// One cuBLAS handle per (host thread, device): a handle carries its stream
+// (cublasSetStream), so rectilinear and direct calls running concurrently on
+// one device from different threads must not share it.
 cublasHandle_t handle_for(int device) {
-  static std::mutex mu;
-  static std::map<int, cublasHandle_t> handles;
-  std::lock_guard<std::mutex> lock(mu);
-  auto it = handles.find(device);
-  if (it != handles.end()) return it->second;
+  struct Handles {
+    std::map<int, cublasHandle_t> h;
+    ~Handles() {
+      for (auto& kv : h) cublasDestroy(kv.second);
+    }
+  };
+  thread_local Handles handles;
+  auto it = handles.h.find(device);
+  if (it != handles.h.end()) return it->second;
   cublasHandle_t h = nullptr;
   if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
   cublasSetMathMode(h, CUBLAS_DEFAULT_MATH);
-  handles[device] = h;
+  handles.h[device] = h;
   return h;
 }
 

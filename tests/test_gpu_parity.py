@@ -719,6 +719,38 @@ def test_warp_gather_small_evaluates(vfb, offset_box, m):
     plan.evaluate(pts)  # the bad-row word was reset: a clean call passes
 
 
+def test_rectilinear_and_direct_from_several_threads(vfb, offset_box):
+    """Rectilinear and direct evaluations (both cuBLAS) running concurrently
+    from different threads on one device give the serial values bitwise."""
+    import threading
+
+    rng = np.random.default_rng(900)
+    spec = random_spectral(offset_box, (16, 12, 10), 901)
+    a, b = np.array(offset_box.a), np.array(offset_box.b)
+    axes = [np.sort(rng.uniform(a[d], b[d], n)) for d, n in enumerate((64, 48, 40))]
+    pts = rng.uniform(a, b, (3000, 3))
+    rect_ref = vfb.eval_rectilinear(spec, axes)
+    direct_ref = vfb.eval_direct(spec, pts)
+    errors = []
+
+    def work(k):
+        try:
+            for _ in range(6):
+                if k % 2:
+                    assert np.array_equal(vfb.eval_rectilinear(spec, axes), rect_ref)
+                else:
+                    assert np.array_equal(vfb.eval_direct(spec, pts), direct_ref)
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+
+
 def test_cuda_graph_replay_matches_eager(vfb, offset_box):
     """Repeated small evaluates replay one CUDA graph (second call captures):
     values bitwise equal to the eager launches, new point values in the same
