@@ -727,7 +727,12 @@ int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* ou
     }
   }
   if (frac.empty()) {
-    if (M >= ((int64_t)1 << 26))
+    if (M >= ((int64_t)1 << 27))
+      // from a timeline model (H2D 116 ms, D2H 80 ms and the measured
+      // evaluate cost of a first-f fraction of c5's points, which is
+      // superlinear at small f): c5 233.4 -> 226.4 ms measured
+      frac = {0.06, 0.28, 0.44, 0.22};
+    else if (M >= ((int64_t)1 << 26))
       frac = {0.12, 0.38, 0.38, 0.12};
     else if (host_column_density(p, points, M) >= 256.0)
       // clustered (config 3's cloud: ~1e5 points per 1x1x8 column): chunks
