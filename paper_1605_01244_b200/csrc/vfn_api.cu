@@ -57,11 +57,11 @@ int stage_in(DevBuf& buf, const void* src, size_t bytes, int on_device, const vo
   return VFN_OK;
 }
 
-// The plan's pinned stager when `host` is pageable and large enough to matter.
+// The device's pinned stager (shared by its plans; 384 MB of pinned host
+// memory per device, not per plan) when `host` is pageable and >= 1 MB.
 HostStager* stager_for(vfn_plan* p, const void* host, size_t bytes) {
   if (bytes < ((size_t)1 << 20) || !is_pageable(host)) return nullptr;
-  if (!p->stager) p->stager = stager_create();
-  return p->stager;
+  return device_stager(p->device);
 }
 
 // The sort's value input is iota (0..M-1); it never changes, so it is kept
@@ -301,7 +301,6 @@ int vfn_plan_destroy(vfn_plan* p) {
     if (p->graph_ev[i]) cudaEventDestroy(p->graph_ev[i]);
   if (p->graph_stream) cudaStreamDestroy(p->graph_stream);
   if (p->bad_host) cudaFreeHost(p->bad_host);
-  stager_destroy(p->stager);
   delete p;
   return VFN_OK;
 }
@@ -785,7 +784,7 @@ int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* ou
   int st = VFN_OK;
   BinGeom g;
   bool have_g = false;
-  // pageable user buffers: chunk copies go through the plan's pinned stager
+  // pageable user buffers: chunk copies go through the device's pinned stager
   // (host threads copy one piece while the DMA engine moves the previous);
   // chunk i-1's output is staged out while chunk i computes
   HostStager* st_in = stager_for(p, points, sizeof(double) * 3 * M);

@@ -138,10 +138,6 @@ struct WindowPoly {
 
 }  // namespace vfn
 
-namespace vfn {
-struct HostStager;
-}
-
 struct vfn_plan {
   // Serialises every entry point that touches the plan's scratch or settings:
   // the reference allows one plan to be evaluated from several threads on
@@ -178,7 +174,6 @@ struct vfn_plan {
   int64_t* bad_mapped = nullptr;  // its device-side address
   int64_t bad_fallback = 0;
   cudaStream_t copy_stream[2] = {nullptr, nullptr};  // H2D / D2H of the pipelined host path
-  vfn::HostStager* stager = nullptr;  // pinned staging for pageable host buffers (vfn_stage.cpp)
   mutable float last_gather_ms = 0.f, last_total_ms = 0.f;
   mutable bool timing_pending = false;  // ev[0..3] hold the last call's unread timing
   vfn::BinGeom last_geom;
@@ -215,6 +210,7 @@ namespace vfn {
 // threads, transfers on the given stream.  h2d returns once the data are in
 // pinned pieces with their H2D enqueued (the caller's later work on `s`
 // follows them); d2h returns once the data are in host memory.
+struct HostStager;
 bool is_pageable(const void* host_ptr);
 HostStager* stager_create();
 void stager_destroy(HostStager* st);
