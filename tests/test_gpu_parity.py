@@ -751,6 +751,36 @@ def test_rectilinear_and_direct_from_several_threads(vfb, offset_box):
     assert not errors, errors
 
 
+def test_plans_release_device_memory(vfb, offset_box):
+    """Creating, using and dropping plans repeatedly returns the device memory
+    (grid, evaluate scratch, graphs); only process-wide caches (cuFFT plans,
+    the window fit) may stay."""
+    import gc
+
+    import torch
+
+    rng = np.random.default_rng(950)
+    pts = rng.uniform(offset_box.a, offset_box.b, (200000, 3))
+    spec = random_spectral(offset_box, (24, 20, 16), 951)
+
+    def cycle():
+        plan = vfb.NufftPlan(spec)
+        plan.evaluate(pts)
+        plan.evaluate(pts[:5000])
+        plan.evaluate(torch.as_tensor(pts, device="cuda"))
+        del plan
+        gc.collect()
+
+    cycle()  # warm the process-wide caches
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(12):
+        cycle()
+    torch.cuda.synchronize()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 < 64 << 20, (free0 - free1) / 2**20
+
+
 def test_cuda_graph_replay_matches_eager(vfb, offset_box):
     """Repeated small evaluates replay one CUDA graph (second call captures):
     values bitwise equal to the eager launches, new point values in the same
