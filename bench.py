@@ -335,6 +335,15 @@ def run_ours(args):
     barrier()
     clk = clocks.stop()
     step_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    if M < (1 << 20) and M > plan_warp_max():
+        # graph-replayed evaluates report the whole graph's time; the
+        # roofline needs the gather kernel alone: a few eager evaluates
+        plan.set_graphs(False)
+        gather_ms = []
+        for _ in range(3):
+            plan.evaluate(pts, out=out)
+            gather_ms.append(plan.last_timing()[0])
+        plan.set_graphs(True)
     g_ms = max_over_ranks(float(np.mean(gather_ms)))
 
     # ---- end to end through the public API: pinned host in, pinned host out
@@ -626,6 +635,12 @@ def run_tube(args):
                                    "density_rel_linf": float(np.abs(rd - host_cloud.density).max() / np.abs(rd).max())
                                    if same and len(rd) else None}
     print(json.dumps(result), flush=True)
+
+
+def plan_warp_max() -> int:
+    from paper_1605_01244_b200 import nufft
+
+    return nufft.WARP_MAX_M
 
 
 def launches_per_step(plan, M: int) -> int:

@@ -600,7 +600,7 @@ int eval_device_batches(vfn_plan* p, const double* points, int64_t M, double* ou
 // first call with a new key runs eagerly (and sizes every buffer), the second
 // captures eval_enqueue on the plan's own stream, later ones replay it.
 // Values are bitwise those of the eager path (same kernels, same order).
-constexpr int64_t kGraphMaxM = (int64_t)1 << 19;  // below the density-sampling size
+constexpr int64_t kGraphMaxM = ((int64_t)1 << 20) - 1;  // below the density-sampling size (2^20)
 
 bool same_key(const vfn_plan::GraphKey& a, const vfn_plan::GraphKey& b) {
   if (!a.valid || !b.valid) return false;

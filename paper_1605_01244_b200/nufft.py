@@ -306,7 +306,7 @@ class NufftPlan:
         self._gather = int(variant)
 
     def set_graphs(self, enable: bool) -> None:
-        """Replay small evaluates (M <= 2^19) as one CUDA graph when the call
+        """Replay binned evaluates below 2^20 points as one CUDA graph when the call
         repeats (same buffers, M, geometry); on by default, values identical."""
         _lib.check(_lib.load().vfn_plan_set_graphs(self._handle, int(bool(enable))))
 
