@@ -423,14 +423,21 @@ int vfn_tube_eval(vfn_tube** out, int device, const double* values, const int64_
   VFN_CHECK(iota.ensure(sizeof(int) * cur));
   VFN_CHECK(perm.ensure(sizeof(int) * cur));
   k_keys<<<nblk(cur), 256, 0, s>>>(idxA.as<longlong4>(), cur, L, keys.as<unsigned long long>(), iota.as<int>());
+  // only the bits the lattice keys can use (~31 for a 1152^3 lattice): half
+  // the radix passes of a full 64-bit sort
+  int key_bits = 1;
+  {
+    const double span = (double)L.size[0] * (double)L.size[1] * (double)L.size[2];
+    while (key_bits < 64 && std::ldexp(1.0, key_bits) < span) ++key_bits;
+  }
   size_t bytes = 0;
   VFN_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.as<unsigned long long>(),
                                            keys2.as<unsigned long long>(), iota.as<int>(),
-                                           perm.as<int>(), (int)cur, 0, 64, s));
+                                           perm.as<int>(), (int)cur, 0, key_bits, s));
   VFN_CHECK(tmp.ensure(bytes));
   VFN_CUDA(cub::DeviceRadixSort::SortPairs(tmp.ptr, bytes, keys.as<unsigned long long>(),
                                            keys2.as<unsigned long long>(), iota.as<int>(),
-                                           perm.as<int>(), (int)cur, 0, 64, s));
+                                           perm.as<int>(), (int)cur, 0, key_bits, s));
   VFN_CHECK(t->points.ensure(sizeof(double) * 3 * cur));
   VFN_CHECK(t->density.ensure(sizeof(double) * cur));
   VFN_CHECK(t->level.ensure(sizeof(int64_t) * cur));
