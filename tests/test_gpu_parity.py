@@ -781,6 +781,34 @@ def test_plans_release_device_memory(vfb, offset_box):
     assert free0 - free1 < 64 << 20, (free0 - free1) / 2**20
 
 
+@pytest.mark.parametrize("M", [300000, (1 << 23) + 5])
+def test_pageable_and_pinned_host_buffers(vfb, offset_box, M):
+    """Every mix of pageable (plain numpy, staged through pinned pieces) and
+    pinned host buffers, on the simple and the pipelined host path, gives the
+    device-resident values bitwise; an outside row is still reported."""
+    import torch
+
+    spec = random_spectral(offset_box, (16, 16, 16), 980)
+    rng = np.random.default_rng(981)
+    a, b = np.array(offset_box.a), np.array(offset_box.b)
+    pts = rng.uniform(a, b, (M, 3))
+    plan = vfb.NufftPlan(spec)
+    plan.set_box(2)
+    ref = plan.evaluate(torch.as_tensor(pts, device="cuda")).cpu().numpy()
+    pin_p = torch.empty((M, 3), dtype=torch.float64, pin_memory=True)
+    pin_p.copy_(torch.as_tensor(pts))
+    for src in (pts, pin_p.numpy()):
+        for pinned_out in (False, True):
+            out = (torch.empty(M, dtype=torch.complex128, pin_memory=True).numpy() if pinned_out
+                   else np.empty(M, dtype=np.complex128))
+            plan.evaluate(src, out=out)
+            assert np.array_equal(out, ref), (src is pts, pinned_out)
+    bad = pts.copy()
+    bad[M - 3] = np.nan
+    with pytest.raises(ValueError, match=rf"\(row {M - 3}\)"):
+        plan.evaluate(bad)
+
+
 def test_cuda_graph_replay_matches_eager(vfb, offset_box):
     """Repeated small evaluates replay one CUDA graph (second call captures):
     values bitwise equal to the eager launches, new point values in the same
