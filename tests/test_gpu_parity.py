@@ -914,3 +914,28 @@ def test_c_abi_from_plain_c(tmp_path):
     run = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert run.returncode == 0, run.stdout + run.stderr
     assert "first bad row 17" in run.stdout
+
+
+@pytest.mark.timeout(600)
+def test_bench_under_torchrun_two_ranks(vfb):
+    """bench.py's N > 1 path (torchrun, one JSON line from rank 0, max over
+    ranks, weak scaling) with two ranks sharing this GPU over gloo
+    (VFN_DIST_BACKEND=gloo; NCCL refuses two ranks on one device)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from conftest import REPO
+
+    env = dict(os.environ, VFN_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29573", os.path.join(REPO, "bench.py"),
+           "--gpus", "2", "--workload", "c1", "--steps", "3", "--warmup", "3"]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=540, cwd=REPO, env=env)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, res.stdout
+    out = json.loads(lines[0])
+    assert out["n_gpus"] == 2 and out["scaling"] == "weak" and out["config"]["points"] == 2 * 10000
+    assert out["value"] > 0 and out["e2e"]["matches_device_result_bitwise"] is True
