@@ -377,6 +377,29 @@ def test_rectilinear_slabs_per_rank(vfb, offset_box):
         assert got.shape == full.shape and l2 < 1e-14 and linf < 1e-14, (world, l2, linf)
 
 
+def test_rectilinear_unsorted_duplicate_and_edge_coordinates(vfb, offset_box):
+    """Coordinate vectors need not be sorted (rectilinear.py:47-64): shuffled
+    and repeated values and the left edge a (never b) on every axis, vs the
+    oracle; a repeated coordinate gives bitwise equal slices."""
+    rng = np.random.default_rng(990)
+    spec = random_spectral(offset_box, (10, 12, 8), 991)
+    a, b = np.array(offset_box.a), np.array(offset_box.b)
+    ys = []
+    for d, n in enumerate((9, 7, 11)):
+        y = rng.uniform(a[d], b[d], n)
+        y[1] = y[4]  # duplicate
+        y[2] = a[d]  # left edge
+        y[3] = np.nextafter(b[d], a[d])
+        ys.append(y)
+    out = vfb.eval_rectilinear(spec, ys)
+    ref = O.rectilinear(spec.coeffs, offset_box.a, offset_box.b, ys)
+    l2, linf = rel_err(out, ref)
+    assert l2 < 1e-13 and linf < 1e-13, (l2, linf)
+    assert np.array_equal(out[1], out[4]) and np.array_equal(out[:, 1], out[:, 4])
+    with pytest.raises(ValueError, match="right endpoint aliases the left"):
+        vfb.eval_rectilinear(spec, [np.append(ys[0], b[0]), ys[1], ys[2]])
+
+
 def test_rectilinear_regular_grid_matches_fft(vfb, offset_box):
     spec = random_spectral(offset_box, (12, 12, 12), 43)
     axes = vfb.regular_grid(offset_box, spec.coeffs.shape)
