@@ -21,6 +21,7 @@
  *   vfn_direct_eval   <- eval_direct               nufft.py:129-149 (exact NDFT)
  *   vfn_decompose     <- snapshot_spectral         gpe.py:110-113 (mirror_extend gpe.py:90-101
  *                        + decompose fourier.py:183-188)
+ *   vfn_synthesize    <- synthesize_regular        fourier.py:191-196
  *   vfn_tube_eval     <- tube_eval                 tube.py:58-127 (one reused plan)
  *
  * File formats feeding the path, native and multithreaded:
@@ -161,6 +162,14 @@ int vfn_plan_last_timing(const vfn_plan* plan, float* gather_ms, float* total_ms
 int vfn_decompose(int device, const double* values, const int64_t shape[3], const double a[3],
                   const double b[3], const int mirror[3], double* coeffs_out, int on_device,
                   void* stream);
+
+/* Inverse of vfn_decompose without mirroring: the samples of a centred
+ * coefficient array on its box's regular grid, ifftn(ifftshift(coeffs)) /
+ * prod_d(sqrt(b_d - a_d) / N_d)   <- synthesize_regular (fourier.py:191-196).
+ * coeffs / values_out: (N1, N2, N3) complex128, C-order; on_device as for
+ * vfn_plan_eval. */
+int vfn_synthesize(int device, const double* coeffs, const int64_t shape[3], const double a[3],
+                   const double b[3], double* values_out, int on_device, void* stream);
 
 /* Adaptive low-density point extraction (tube.py:58-127): seeds are the
  * samples with |v|^2 <= thresholds[0]; each later threshold selects the

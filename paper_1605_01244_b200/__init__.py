@@ -5,7 +5,7 @@ kernels through the C ABI in include/vfnfft.h (libvfnfft.so, built in-tree).
 """
 
 from . import formats, pipeline
-from .fourier import DomainBox, SpectralField, regular_grid
+from .fourier import DomainBox, PhysicalField, SpectralField, decompose, regular_grid, synthesize_regular
 from .nufft import (
     AccuracyWarning,
     NufftParams,
@@ -23,10 +23,12 @@ __all__ = [
     "DomainBox",
     "NufftParams",
     "NufftPlan",
+    "PhysicalField",
     "Snapshot",
     "SpectralField",
     "TubePointCloud",
     "computational_domain",
+    "decompose",
     "formats",
     "pipeline",
     "basis_matrix",
@@ -37,6 +39,7 @@ __all__ = [
     "regular_grid",
     "rescale_coeffs",
     "snapshot_spectral",
+    "synthesize_regular",
     "tube_eval",
 ]
 

@@ -83,6 +83,10 @@ SIGNATURES = {
         ctypes.c_int,
         [ctypes.c_int, _vp, _c_i64_3, _c_f64_3, _c_f64_3, ctypes.c_int * 3, _vp, ctypes.c_int, _vp],
     ),
+    "vfn_synthesize": (
+        ctypes.c_int,
+        [ctypes.c_int, _vp, _c_i64_3, _c_f64_3, _c_f64_3, _vp, ctypes.c_int, _vp],
+    ),
     "vfn_tube_eval": (
         ctypes.c_int,
         [ctypes.POINTER(_vp), ctypes.c_int, _vp, _c_i64_3, _c_f64_3, _c_f64_3, ctypes.c_int * 3,

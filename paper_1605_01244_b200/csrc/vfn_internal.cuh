@@ -233,6 +233,8 @@ int fit_window_poly(int m, double beta, double* coef, int max_deg);
 void* blas_handle(int device);  // per (host thread, device)
 // in-place unnormalised forward Z2Z 3D FFT through a cached cuFFT plan
 int fft_forward(const int64_t n[3], double2* data, cudaStream_t s);
+// in-place unnormalised inverse (e^{+2 pi i k l / n}) 3D Z2Z FFT
+int fft_inverse(const int64_t n[3], double2* data, cudaStream_t s);
 int build_grid(vfn_plan* p, const double* coeffs_dev, cudaStream_t s);
 int map_and_key(vfn_plan* p, const double* pts_dev, int64_t M, const BinGeom& g, uint32_t* keys,
                 int32_t* iota, double* u, int64_t* bad_dev, cudaStream_t s);

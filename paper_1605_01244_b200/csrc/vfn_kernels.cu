@@ -33,7 +33,14 @@ uint64_t g_fft_clock = 0;
 constexpr size_t kFftCacheMax = 6;
 }  // namespace
 
-int fft_forward(const int64_t n[3], double2* data, cudaStream_t s) {
+int fft_exec(const int64_t n[3], double2* data, cudaStream_t s, int direction);
+
+int fft_forward(const int64_t n[3], double2* data, cudaStream_t s) { return fft_exec(n, data, s, CUFFT_FORWARD); }
+
+int fft_inverse(const int64_t n[3], double2* data, cudaStream_t s) { return fft_exec(n, data, s, CUFFT_INVERSE); }
+
+// in-place unnormalised 3D Z2Z transform through the cached plan of its size
+int fft_exec(const int64_t n[3], double2* data, cudaStream_t s, int direction) {
   int dev = 0;
   VFN_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(g_fft_mu);
@@ -64,8 +71,8 @@ int fft_forward(const int64_t n[3], double2* data, cudaStream_t s) {
   cufftResult r = cufftSetStream(e.h, s);
   if (r == CUFFT_SUCCESS)
     r = cufftExecZ2Z(e.h, reinterpret_cast<cufftDoubleComplex*>(data), reinterpret_cast<cufftDoubleComplex*>(data),
-                     CUFFT_FORWARD);
-  if (r != CUFFT_SUCCESS) return fail(VFN_ERR_CUFFT, "cuFFT Z2Z forward failed (code " + std::to_string((int)r) + ")");
+                     direction);
+  if (r != CUFFT_SUCCESS) return fail(VFN_ERR_CUFFT, "cuFFT Z2Z failed (code " + std::to_string((int)r) + ")");
   VFN_CUDA(cudaEventRecord(e.done, s));
   return VFN_OK;
 }

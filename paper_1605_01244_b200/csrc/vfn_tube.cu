@@ -11,6 +11,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <cmath>
 #include <map>
 #include <mutex>
@@ -233,6 +234,54 @@ TubeScratch* tube_scratch(int device) {
   return t;
 }
 }  // namespace
+
+// synthesize_regular (fourier.py:191-196): values = ifftn(ifftshift(coeffs))
+// / scale, scale = prod_d sqrt(b_d - a_d) / N_d.  One kernel writes the
+// shifted, scaled coefficients (1 / (N scale): cuFFT's inverse is
+// unnormalised), then an in-place inverse FFT.
+__global__ void k_ishift_scale(const double2* __restrict__ c, int64_t N0, int64_t N1, int64_t N2, double f,
+                               double2* __restrict__ out) {
+  const int64_t total = N0 * N1 * N2;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i2 = e % N2, r = e / N2, i1 = r % N1, i0 = r / N1;
+    const int64_t j0 = (i0 + N0 / 2) % N0, j1 = (i1 + N1 / 2) % N1, j2 = (i2 + N2 / 2) % N2;
+    const double2 v = c[(j0 * N1 + j1) * N2 + j2];
+    out[e] = make_double2(v.x * f, v.y * f);
+  }
+}
+
+int vfn_synthesize(int device, const double* coeffs, const int64_t shape[3], const double a[3],
+                   const double b[3], double* values_out, int on_device, void* stream) {
+  vfn::NvtxRange nvtx_range("vfn synthesize");
+  if (!coeffs || !shape || !a || !b || !values_out) return fail(VFN_ERR_INVALID, "null argument");
+  for (int d = 0; d < 3; ++d)
+    if (shape[d] <= 0 || !(a[d] < b[d])) return fail(VFN_ERR_INVALID, "bad shape or domain");
+  DeviceGuard guard(device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t n = shape[0] * shape[1] * shape[2];
+  double scale = 1.0;
+  for (int d = 0; d < 3; ++d) scale *= std::sqrt(b[d] - a[d]) / (double)shape[d];
+  DevBuf cin, vout;
+  const double2* cdev = reinterpret_cast<const double2*>(coeffs);
+  double2* vdev = reinterpret_cast<double2*>(values_out);
+  if (!on_device) {
+    VFN_CHECK(cin.ensure(sizeof(double2) * n));
+    VFN_CUDA(cudaMemcpyAsync(cin.ptr, coeffs, sizeof(double2) * n, cudaMemcpyHostToDevice, s));
+    cdev = cin.as<double2>();
+    VFN_CHECK(vout.ensure(sizeof(double2) * n));
+    vdev = vout.as<double2>();
+  }
+  const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
+  k_ishift_scale<<<blocks, 256, 0, s>>>(cdev, shape[0], shape[1], shape[2], 1.0 / ((double)n * scale), vdev);
+  VFN_CUDA(cudaGetLastError());
+  VFN_CHECK(fft_inverse(shape, vdev, s));
+  if (!on_device)
+    VFN_CUDA(cudaMemcpy(values_out, vdev, sizeof(double2) * n, cudaMemcpyDeviceToHost));
+  else
+    VFN_CUDA(cudaStreamSynchronize(s));
+  return VFN_OK;
+}
 
 int vfn_decompose(int device, const double* values, const int64_t shape[3], const double a[3],
                   const double b[3], const int mirror[3], double* coeffs_out, int on_device,

@@ -13,7 +13,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["DomainBox", "SpectralField", "regular_grid"]
+__all__ = ["DomainBox", "PhysicalField", "SpectralField", "decompose", "regular_grid", "synthesize_regular"]
 
 
 @dataclass(frozen=True)
@@ -72,6 +72,21 @@ def _check_values(values):
 
 
 @dataclass(frozen=True)
+class PhysicalField:
+    """Complex samples on the regular grid of a DomainBox (fourier.py:128-145)."""
+
+    domain: DomainBox
+    values: np.ndarray
+
+    def __post_init__(self):
+        object.__setattr__(self, "values", _check_values(self.values))
+
+    @property
+    def step(self) -> np.ndarray:
+        return np.asarray(self.domain.widths) / np.array(tuple(self.values.shape))
+
+
+@dataclass(frozen=True)
 class SpectralField:
     """Centred-order Fourier coefficients on a DomainBox (fourier.py:147-164)."""
 
@@ -90,3 +105,40 @@ def regular_grid(domain, size) -> list:
     """x_d = a_d + j h_d, j = 0..N_d-1 (fourier.py:167-180)."""
     size = tuple(int(v) for v in size)
     return [np.linspace(domain.a[d], domain.b[d], size[d] + 1)[: size[d]] for d in range(3)]
+
+
+def _transform(fn_name, domain, arr, extra=()):
+    # shared plumbing of decompose / synthesize_regular: numpy in -> numpy out,
+    # CUDA torch tensors in -> CUDA tensors out (no host round trip)
+    from . import _lib
+    from .nufft import _device_of, _is_cuda_tensor, _stream_of, _torch
+
+    on_dev = 1 if _is_cuda_tensor(arr) else 0
+    shape = tuple(int(s) for s in arr.shape)
+    if on_dev:
+        t = _torch()
+        out = t.empty(shape, dtype=t.complex128, device=arr.device)
+    else:
+        out = np.empty(shape, dtype=np.complex128)
+    dev = _device_of(arr)
+    fn = getattr(_lib.load(), fn_name)
+    _lib.check(fn(dev, _lib.ptr(arr), _lib.i64x3(shape), _lib.f64x3(domain.a), _lib.f64x3(domain.b), *extra,
+                  _lib.ptr(out), on_dev, _stream_of(dev)))
+    return out
+
+
+def decompose(field) -> SpectralField:
+    """Grid samples to centred Fourier coefficients on the device
+    (fourier.py:183-188): fftshift(fftn(values)) * prod_d sqrt(w_d) / N_d."""
+    import ctypes
+
+    values = _check_values(field.values)
+    mirror = (ctypes.c_int * 3)(0, 0, 0)
+    return SpectralField(field.domain, _transform("vfn_decompose", field.domain, values, (mirror,)))
+
+
+def synthesize_regular(spec) -> PhysicalField:
+    """Inverse of decompose: the samples on the regular grid of spec.domain
+    (fourier.py:191-196), on the device."""
+    coeffs = _check_values(spec.coeffs)
+    return PhysicalField(spec.domain, _transform("vfn_synthesize", spec.domain, coeffs))
