@@ -5,7 +5,16 @@ kernels through the C ABI in include/vfnfft.h (libvfnfft.so, built in-tree).
 """
 
 from . import formats, pipeline
-from .fourier import DomainBox, PhysicalField, SpectralField, decompose, regular_grid, synthesize_regular
+from .fourier import (
+    DomainBox,
+    PhysicalField,
+    SpectralField,
+    decompose,
+    fft_workers,
+    regular_grid,
+    set_fft_workers,
+    synthesize_regular,
+)
 from .nufft import (
     AccuracyWarning,
     NufftParams,
@@ -35,9 +44,11 @@ __all__ = [
     "eval_direct",
     "eval_nufft",
     "eval_rectilinear",
+    "fft_workers",
     "map_to_torus",
     "regular_grid",
     "rescale_coeffs",
+    "set_fft_workers",
     "snapshot_spectral",
     "synthesize_regular",
     "tube_eval",

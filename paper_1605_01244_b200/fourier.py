@@ -13,7 +13,22 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["DomainBox", "PhysicalField", "SpectralField", "decompose", "regular_grid", "synthesize_regular"]
+__all__ = ["DomainBox", "PhysicalField", "SpectralField", "decompose", "fft_workers", "regular_grid",
+           "set_fft_workers", "synthesize_regular"]
+
+_fft_workers = -1
+
+
+def set_fft_workers(n: int | None) -> None:
+    """The reference's CPU FFT thread knob (fourier.py:47-54), kept for
+    compatibility: every transform here runs on the GPU (cuFFT), so the
+    value is only stored and reported back."""
+    global _fft_workers
+    _fft_workers = -1 if n is None else int(n)
+
+
+def fft_workers() -> int:
+    return _fft_workers
 
 
 @dataclass(frozen=True)
