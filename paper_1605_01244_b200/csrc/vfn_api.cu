@@ -137,7 +137,7 @@ __global__ void k_sample_columns(const double* __restrict__ pts, int64_t M, int 
 // estimated from the colliding pairs of a strided sample of S points.
 static int local_density(vfn_plan* p, const double* pts, int64_t M, cudaStream_t s, double* rho) {
   const int S = 16384;
-  DevBuf buf;
+  DevBuf& buf = p->sample;  // grow-only plan scratch: no cudaMalloc/cudaFree (a device sync) per call
   VFN_CHECK(buf.ensure(sizeof(uint32_t) * 2 * S));
   uint32_t* a = buf.as<uint32_t>();
   uint32_t* b = a + S;
@@ -158,7 +158,6 @@ static int local_density(vfn_plan* p, const double* pts, int64_t M, cudaStream_t
     pairs += L * (L - 1) / 2;
   }
   *rho = 2.0 * pairs * (double)(M - 1) / ((double)S * (S - 1));
-  buf.release();
   return VFN_OK;
 }
 
