@@ -994,3 +994,43 @@ def test_bench_under_torchrun_two_ranks(vfb):
     out = json.loads(lines[0])
     assert out["n_gpus"] == 2 and out["scaling"] == "weak" and out["config"]["points"] == 2 * 10000
     assert out["value"] > 0 and out["e2e"]["matches_device_result_bitwise"] is True
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+def test_first_bad_row_on_every_path(vfb, unit_box, variant):
+    """Non-finite and out-of-domain rows deep inside a large call: every gather
+    variant reports the FIRST bad row (reference nufft.py domain check), from
+    host and device inputs, and the plan keeps working afterwards.  The
+    CUDA-graph replay (variant 2 below 2^20 points) must report a row that was
+    written into the captured input buffer in place."""
+    import torch
+
+    spec = random_spectral(unit_box, (16, 16, 16), 131)
+    rng = np.random.default_rng(132)
+    M = 100000
+    pts = rng.uniform(0.0, 1.0, (M, 3))
+    plan = vfb.NufftPlan(spec)
+    plan.set_gather(variant)
+    good = plan.evaluate(pts)
+    bad = pts.copy()
+    bad[77777] = (0.5, np.inf, 0.5)
+    bad[88888] = (np.nan, 0.5, 0.5)
+    bad[99999] = (-1e-300, 0.5, 0.5)
+    for arr in (bad, torch.as_tensor(bad, device="cuda")):
+        with pytest.raises(ValueError, match=r"\(row 77777\)"):
+            plan.evaluate(arr)
+    only_last = pts.copy()
+    only_last[M - 1] = (0.5, 0.5, 1.0)
+    with pytest.raises(ValueError, match=rf"\(row {M - 1}\)"):
+        plan.evaluate(only_last)
+    np.testing.assert_array_equal(plan.evaluate(pts), good)
+    # same device buffer twice (graph capture + replay), then poisoned in place
+    t = torch.as_tensor(pts, device="cuda")
+    for _ in range(3):
+        np.testing.assert_array_equal(plan.evaluate(t).cpu().numpy(), good)
+    t[4242, 2] = float("nan")
+    with pytest.raises(ValueError, match=r"\(row 4242\)"):
+        plan.evaluate(t)
+    t[4242, 2] = 0.25
+    out = plan.evaluate(t).cpu().numpy()
+    np.testing.assert_array_equal(np.delete(out, 4242), np.delete(good, 4242))
