@@ -93,4 +93,22 @@ __device__ __forceinline__ double window_poly(const double* __restrict__ coef, i
   return acc;
 }
 
+// window_poly of tap j at three deltas in one pass: three independent Horner
+// chains per coefficient read (the same fma sequence per chain, so bitwise
+// equal to three window_poly calls).
+__device__ __forceinline__ void window_poly3(const double* __restrict__ coef, int deg, int j,
+                                             const double dl[3], double w[3]) {
+  const double* c = coef + j * (deg + 1);
+  double a0 = c[deg], a1 = a0, a2 = a0;
+  for (int i = deg - 1; i >= 0; --i) {
+    const double ci = c[i];
+    a0 = fma(a0, dl[0], ci);
+    a1 = fma(a1, dl[1], ci);
+    a2 = fma(a2, dl[2], ci);
+  }
+  w[0] = a0;
+  w[1] = a1;
+  w[2] = a2;
+}
+
 }  // namespace vfn

@@ -381,7 +381,12 @@ __global__ void __launch_bounds__(256) k_gather_warp(const double* __restrict__ 
   constexpr int RPI = 32 / W;  // rows per load instruction
   extern __shared__ double s_warp[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* w = s_warp + warp * (3 * W + W * W);  // w[d][j], then w12[a * W + b]
+  // window coefficients staged once per CTA: Horner straight from global
+  // memory is a chain of dependent L2 round trips (~25 us per call)
+  double* s_poly = s_warp;
+  for (int i = threadIdx.x; i < W * (deg + 1); i += blockDim.x) s_poly[i] = poly[i];
+  __syncthreads();
+  double* w = s_warp + W * (deg + 1) + warp * (3 * W + W * W);  // w[d][j], then w12[a * W + b]
   double* w12 = w + 3 * W;
   const int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (p >= M) return;
@@ -396,8 +401,10 @@ __global__ void __launch_bounds__(256) k_gather_warp(const double* __restrict__ 
   }
   if (!ok && lane == 0) atomicMin(bad, (unsigned long long)p);
   if (lane < W) {
+    double wl[3];
+    window_poly3(s_poly, deg, lane, dl, wl);
 #pragma unroll
-    for (int d = 0; d < 3; ++d) w[d * W + lane] = window_poly(poly, deg, lane, dl[d]);
+    for (int d = 0; d < 3; ++d) w[d * W + lane] = wl[d];
   }
   __syncwarp();
   for (int r = lane; r < W * W; r += 32) w12[r] = w[r / W] * w[W + r % W];
@@ -408,13 +415,21 @@ __global__ void __launch_bounds__(256) k_gather_warp(const double* __restrict__ 
     // padded index of grid cell (cell - m + j) is cell + j
     const double2* base = grid + ((int64_t)cell[0] * P1 + cell[1]) * P2 + cell[2] + c;
     VFN_DCHECK(cell[1] + W <= P1 && cell[2] + W <= P2);
+    // row r = a W + b sits at base + (a P1 + b) P2; walk it incrementally (a
+    // single warp's call is a serial instruction stream: no 64-bit index
+    // products per row)
+    int b = rs % W;
+    const double2* q = base + ((int64_t)(rs / W) * P1 + b) * P2;
+    const int64_t step = (int64_t)RPI * P2, wrap = ((int64_t)P1 - W) * P2;
 #pragma unroll 4
     for (int r = rs; r < W * W; r += RPI) {
-      const int a = r / W, b = r - a * W;
-      const double2 v = __ldg(base + ((int64_t)a * P1 + b) * P2);
+      const double2 v = __ldg(q);
       const double f = w12[r];
       ar = fma(f, v.x, ar);
       ai = fma(f, v.y, ai);
+      const int wraps = (b + RPI) / W;  // branch-free, so loads batch across rows
+      b += RPI - wraps * W;
+      q += step + wraps * wrap;
     }
     const double wc = w[2 * W + c];
     ar *= wc;
@@ -433,7 +448,7 @@ static void launch_warp(vfn_plan* pl, const double* pts, int64_t M, double2* out
                         cudaStream_t s) {
   constexpr int W = 2 * MC + 1;
   const int warps = 8;
-  const size_t smem = sizeof(double) * warps * (3 * W + W * W);
+  const size_t smem = sizeof(double) * (W * (pl->poly.deg + 1) + warps * (3 * W + W * W));
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_gather_warp<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_gather_warp<MC><<<(unsigned)((M + warps - 1) / warps), warps * 32, smem, s>>>(
