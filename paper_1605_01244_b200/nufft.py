@@ -132,7 +132,14 @@ def _is_cuda_tensor(x) -> bool:
 
 def _stream_of(device: int):
     t = _torch()
-    if t is None or not t.cuda.is_available():
+    if t is None:
+        return None
+    # the raw-handle getter costs ~0.1 us against ~2.5 us for
+    # is_available() + current_stream(); same stream
+    raw = getattr(t._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None and t.cuda.is_initialized():
+        return ctypes.c_void_p(raw(device))
+    if not t.cuda.is_available():
         return None
     return ctypes.c_void_p(t.cuda.current_stream(device).cuda_stream)
 

@@ -1034,3 +1034,27 @@ def test_first_bad_row_on_every_path(vfb, unit_box, variant):
     t[4242, 2] = 0.25
     out = plan.evaluate(t).cpu().numpy()
     np.testing.assert_array_equal(np.delete(out, 4242), np.delete(good, 4242))
+
+
+def test_evaluate_runs_on_the_callers_current_stream(vfb, unit_box):
+    """Calls enqueue on torch's current stream (the stream handle passed through
+    the C-ABI), so a caller's side stream orders them with its own work."""
+    import torch
+
+    from paper_1605_01244_b200 import nufft
+
+    spec = random_spectral(unit_box, (16, 16, 16), 141)
+    rng = np.random.default_rng(142)
+    plan = vfb.NufftPlan(spec)
+    for M in (3000, 60000):  # warp path and binned path
+        pts = torch.as_tensor(rng.uniform(0.0, 1.0, (M, 3)), device="cuda")
+        ref = plan.evaluate(pts).cpu().numpy()
+        side = torch.cuda.Stream()
+        with torch.cuda.stream(side):
+            assert nufft._stream_of(plan.device).value == side.cuda_stream
+            shifted = pts * 1.0  # produced on the side stream, consumed by the evaluate
+            out = plan.evaluate(shifted)
+            host = out.cpu().numpy()
+        # the legacy default stream is handle 0 (c_void_p(0).value is None)
+        assert (nufft._stream_of(plan.device).value or 0) == torch.cuda.current_stream().cuda_stream
+        np.testing.assert_array_equal(host, ref)

@@ -43,6 +43,10 @@ def main():
             "_points_arg": lambda: nufft._points_arg(pts),
             "torch.empty": lambda: torch.empty(M, dtype=torch.complex128, device="cuda"),
             "_stream_of": lambda: nufft._stream_of(plan.device),
+            "torch.cuda.is_available": lambda: torch.cuda.is_available(),
+            "current_stream(dev).cuda_stream": lambda: torch.cuda.current_stream(plan.device).cuda_stream,
+            "_C._cuda_getCurrentRawStream": lambda: torch._C._cuda_getCurrentRawStream(plan.device),
+            "_lib.load": lambda: _lib.load(),
         }
         x = torch.zeros(1, device="cuda")
         s = torch.cuda.current_stream()
