@@ -241,6 +241,17 @@ int vfn_vtk_write(const char* path, const char* title, const int64_t shape[3],
                   const double* const coords[3], int nscalars, const char* const* names,
                   const double* const* scalars, int on_device, int device, void* stream);
 
+/* Plan-build breakdown of the last vfn_plan_create (ms): [0] host wall time
+ * of the whole call, [1] K2 deconvolve + pad, [2] K3 3D FFT, [3] halo
+ * faces, [4] host setup before the grid kernels (allocations, window fit,
+ * tables); [1..3] are CUDA-event times on the build stream.              */
+int vfn_plan_build_timing(const vfn_plan* plan, float ms_out[5]);
+
+/* Free the device buffers recycled from destroyed plans (device < 0: all
+ * devices).  Destroyed plans return their grids to a per-device pool of at
+ * most two buffers so a rebuilt plan skips cudaMalloc / cudaFree.        */
+int vfn_pool_release(int device);
+
 /* Utility (not a reference interface): measured sustained FP64 FMA rate of
  * `device` in TFLOP/s over ~`seconds`, the roofline denominator bench.py
  * reports against; *sm_clock_mhz gets the device's max SM clock.        */

@@ -131,6 +131,8 @@ SIGNATURES = {
         [_cp, _cp, _c_i64_3, _vp * 3, ctypes.c_int, ctypes.POINTER(_cp), ctypes.POINTER(_vp),
          ctypes.c_int, ctypes.c_int, _vp],
     ),
+    "vfn_plan_build_timing": (ctypes.c_int, [_vp, ctypes.c_float * 5]),
+    "vfn_pool_release": (ctypes.c_int, [ctypes.c_int]),
     "vfn_plan_last_timing": (
         ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
     ),

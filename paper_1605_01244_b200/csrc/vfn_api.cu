@@ -1,5 +1,6 @@
 // extern "C" entry points of libvfnfft (see include/vfnfft.h).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -198,6 +199,7 @@ int vfn_plan_create(vfn_plan** out, int device, const int64_t nmodes[3], const d
                     const double b[3], double sigma, int m, const double* coeffs,
                     int coeffs_on_device, void* stream) {
   vfn::NvtxRange nvtx_range("vfn plan build");
+  const auto t_start = std::chrono::steady_clock::now();
   if (!out || !nmodes || !a || !b || !coeffs) return fail(VFN_ERR_INVALID, "null argument");
   *out = nullptr;
   if (m < 1 || m > 13) return fail(VFN_ERR_INVALID, "cutoff must be in 1..13");
@@ -250,6 +252,7 @@ int vfn_plan_create(vfn_plan** out, int device, const int64_t nmodes[3], const d
     }
   }
   for (int i = 0; i < 4; ++i) cudaEventCreate(&p->ev[i]);
+  for (int i = 0; i < 4; ++i) cudaEventCreate(&p->bev[i]);
   if (cudaHostAlloc(&p->bad_host, sizeof(int64_t), cudaHostAllocMapped) != cudaSuccess ||
       cudaHostGetDevicePointer(&p->bad_mapped, p->bad_host, 0) != cudaSuccess) {
     cudaGetLastError();
@@ -264,6 +267,22 @@ int vfn_plan_create(vfn_plan** out, int device, const int64_t nmodes[3], const d
     vfn_plan_destroy(p);
     return fail(VFN_ERR_CUDA, "plan scratch: " + msg);
   }
+  // bin keys are uint32: (tile * boxes_per_tile + box) * cells_per_box + cell
+  // must stay below 2^32 for every geometry the plan can use (n1 n2 n3 ~>
+  // 4.2e9 cells); checked before the grid is allocated
+  for (int tm = 0; tm < 2; ++tm)
+    for (int bxy = 1; bxy <= 2; ++bxy) {
+      p->has_tmap = tm == 1;
+      const BinGeom g = make_geometry(p, bxy);
+      p->has_tmap = false;
+      if ((double)g.nboxes * (double)g.cells_per_box > 4294967296.0) {
+        const std::string msg = "oversampled grid too large: its bin keys exceed 32 bits (" +
+                                std::to_string(p->n[0]) + " x " + std::to_string(p->n[1]) + " x " +
+                                std::to_string(p->n[2]) + " cells)";
+        vfn_plan_destroy(p);
+        return fail(VFN_ERR_INVALID, msg);
+      }
+    }
   // coefficients to the device
   const size_t cbytes = sizeof(double2) * nmodes[0] * nmodes[1] * nmodes[2];
   DevBuf staging;
@@ -271,9 +290,12 @@ int vfn_plan_create(vfn_plan** out, int device, const int64_t nmodes[3], const d
   HostStager* cst = (!coeffs_on_device && cbytes >= ((size_t)1 << 20) && is_pageable(coeffs))
                         ? device_stager(device) : nullptr;
   int st = stage_in(staging, coeffs, cbytes, coeffs_on_device, &cdev, s, cst);
+  const auto t_setup = std::chrono::steady_clock::now();
   if (st == VFN_OK) st = build_grid(p, static_cast<const double*>(cdev), s);
   if (st == VFN_OK) st = make_grid_tmap(p);
   staging.release();
+  p->build_ms[4] = std::chrono::duration<float, std::milli>(t_setup - t_start).count();
+  p->build_ms[0] = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_start).count();
   if (st != VFN_OK) {
     std::string msg = vfn_last_error();
     vfn_plan_destroy(p);
@@ -286,8 +308,10 @@ int vfn_plan_create(vfn_plan** out, int device, const int64_t nmodes[3], const d
 int vfn_plan_destroy(vfn_plan* p) {
   if (!p) return VFN_OK;
   DeviceGuard guard(p->device);
-  if (p->grid) cudaFree(p->grid);
+  if (p->grid) pool_free(p->device, p->grid, p->grid_bytes);
   if (p->poly.dev) cudaFree(p->poly.dev);
+  for (int i = 0; i < 4; ++i)
+    if (p->bev[i]) cudaEventDestroy(p->bev[i]);
   DevBuf* bufs[] = {&p->pts, &p->out, &p->keys, &p->keys_sorted, &p->idx, &p->perm,
                     &p->sort_tmp, &p->box_start, &p->items, &p->units, &p->uscratch, &p->misc};
   for (DevBuf* b : bufs) b->release();
@@ -301,6 +325,12 @@ int vfn_plan_destroy(vfn_plan* p) {
   if (p->graph_stream) cudaStreamDestroy(p->graph_stream);
   if (p->bad_host) cudaFreeHost(p->bad_host);
   delete p;
+  return VFN_OK;
+}
+
+int vfn_plan_build_timing(const vfn_plan* p, float ms_out[5]) {
+  if (!p || !ms_out) return fail(VFN_ERR_INVALID, "null argument");
+  for (int i = 0; i < 5; ++i) ms_out[i] = p->build_ms[i];
   return VFN_OK;
 }
 
@@ -523,6 +553,21 @@ int eval_enqueue(vfn_plan* p, const double* pts_dev, int64_t M, double2* out_dev
     VFN_CHECK(gather_simple(p, pts_dev, M, p->perm.as<int32_t>(), out_dev, s));
   }
   mark_event(p, 2, s);
+  return VFN_OK;
+}
+
+// A device buffer handed to a plan must live on the plan's GPU: a pointer
+// into another device's memory would be written by this device's kernels
+// (a peer write or an illegal-address fault that poisons the context).
+int check_on_device(const void* ptr, int device, const char* what) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return VFN_OK;  // unknown to the runtime: let the kernels report it
+  }
+  if ((at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) && at.device != device)
+    return fail(VFN_ERR_INVALID, std::string(what) + " is on cuda:" + std::to_string(at.device) +
+                                     ", the plan on cuda:" + std::to_string(device));
   return VFN_OK;
 }
 
@@ -858,6 +903,10 @@ int vfn_plan_eval(vfn_plan* p, const double* points, int64_t M, double* out, int
   if (M == 0) return VFN_OK;
   DeviceGuard guard(p->device);
   cudaStream_t s = as_stream(stream);
+  if (on_device) {
+    VFN_CHECK(check_on_device(points, p->device, "points"));
+    VFN_CHECK(check_on_device(out, p->device, "out"));
+  }
   if (!on_device && M >= pipe_min_m()) return eval_host_pipelined(p, points, M, out, first_bad_row, s);
   if (M > max_batch()) return eval_device_batches(p, points, M, out, on_device, first_bad_row, s);
   VFN_CUDA(cudaEventRecord(p->ev[0], s));

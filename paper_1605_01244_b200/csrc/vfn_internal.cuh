@@ -158,6 +158,11 @@ struct vfn_plan {
   int64_t P[3] = {0, 0, 0};
   int pad_tile[3] = {8, 8, 8};  // grid padded to multiples of this
   double2* grid = nullptr;
+  size_t grid_bytes = 0;      // its allocation (from the device pool, vfn_util.cu)
+  cudaEvent_t bev[4] = {nullptr, nullptr, nullptr, nullptr};  // grid-build phases
+  // plan-build breakdown (vfn_plan_build_timing): host total, K2, K3 (FFT),
+  // halo, host setup before the grid kernels (allocations, tables)
+  float build_ms[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
   int gather_variant = 0;
   int box_mode = 0;          // 0 auto, 1 or 2: gather box width in cells (vfn_plan_set_box)
   double col_density = 16.0;  // points per 1x1x8 cell column in the last call (sampled or mean)
@@ -229,6 +234,15 @@ void kb_hat_table(int64_t N, int64_t n, int m, double beta, double* out);
 // fit the window polynomials; returns degree, fills coef ((2m+1)*(deg+1))
 int fit_window_poly(int m, double beta, double* coef, int max_deg);
 
+// ---------------------------------------------------------------- device pool (vfn_util.cu)
+// Large device buffers (oversampled grids) are recycled per device instead of
+// cudaFree'd: cudaFree synchronises the whole device, and a plan rebuilt for
+// a new field (a time series of snapshots, one plan per rank) reuses the
+// previous grid's memory.  At most kPoolKeep buffers are held per device;
+// vfn_pool_release() frees them.
+void* pool_alloc(int device, size_t bytes, size_t* got);
+void pool_free(int device, void* ptr, size_t bytes);
+
 // ---------------------------------------------------------------- launchers
 // process-wide cuBLAS handle of `device` (cublasHandle_t; vfn_rect.cu)
 void* blas_handle(int device);  // per (host thread, device)
@@ -236,6 +250,9 @@ void* blas_handle(int device);  // per (host thread, device)
 int fft_forward(const int64_t n[3], double2* data, cudaStream_t s);
 // in-place unnormalised inverse (e^{+2 pi i k l / n}) 3D Z2Z FFT
 int fft_inverse(const int64_t n[3], double2* data, cudaStream_t s);
+// in-place forward transform of an n0 x n1 x n2 array embedded in a C-order
+// allocation of extents embed[0..2] (the padded grid's interior)
+int fft_forward_embedded(const int64_t n[3], const int64_t embed[3], double2* data, cudaStream_t s);
 int build_grid(vfn_plan* p, const double* coeffs_dev, cudaStream_t s);
 int map_and_key(vfn_plan* p, const double* pts_dev, int64_t M, const BinGeom& g, uint32_t* keys,
                 int32_t* iota, double* u, int64_t* bad_dev, cudaStream_t s);

@@ -28,23 +28,31 @@ struct FftEntry {
   uint64_t stamp = 0;
 };
 std::mutex g_fft_mu;
-std::map<std::array<int64_t, 4>, FftEntry> g_fft;
+std::map<std::array<int64_t, 6>, FftEntry> g_fft;
 uint64_t g_fft_clock = 0;
 constexpr size_t kFftCacheMax = 6;
 }  // namespace
 
-int fft_exec(const int64_t n[3], double2* data, cudaStream_t s, int direction);
+int fft_exec(const int64_t n[3], double2* data, cudaStream_t s, int direction, const int64_t* embed = nullptr);
 
 int fft_forward(const int64_t n[3], double2* data, cudaStream_t s) { return fft_exec(n, data, s, CUFFT_FORWARD); }
 
 int fft_inverse(const int64_t n[3], double2* data, cudaStream_t s) { return fft_exec(n, data, s, CUFFT_INVERSE); }
 
+// In-place transform of an (n0, n1, n2) array embedded in a (E0, E1, E2)
+// C-order allocation (element (i0, i1, i2) at data[(i0 E1 + i1) E2 + i2]):
+// the ghost-padded grid's interior, transformed where it lies.
+int fft_forward_embedded(const int64_t n[3], const int64_t embed[3], double2* data, cudaStream_t s) {
+  return fft_exec(n, data, s, CUFFT_FORWARD, embed);
+}
+
 // in-place unnormalised 3D Z2Z transform through the cached plan of its size
-int fft_exec(const int64_t n[3], double2* data, cudaStream_t s, int direction) {
+// (and embedding, if any)
+int fft_exec(const int64_t n[3], double2* data, cudaStream_t s, int direction, const int64_t* embed) {
   int dev = 0;
   VFN_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(g_fft_mu);
-  const std::array<int64_t, 4> key = {dev, n[0], n[1], n[2]};
+  const std::array<int64_t, 6> key = {dev, n[0], n[1], n[2], embed ? embed[1] : 0, embed ? embed[2] : 0};
   auto it = g_fft.find(key);
   if (it == g_fft.end()) {
     if (g_fft.size() >= kFftCacheMax) {  // evict the least recently used plan
@@ -57,8 +65,16 @@ int fft_exec(const int64_t n[3], double2* data, cudaStream_t s, int direction) {
       g_fft.erase(lru);
     }
     FftEntry e;
-    if (cufftPlan3d(&e.h, (int)n[0], (int)n[1], (int)n[2], CUFFT_Z2Z) != CUFFT_SUCCESS)
-      return fail(VFN_ERR_CUFFT, "cufftPlan3d failed");
+    if (cufftCreate(&e.h) != CUFFT_SUCCESS) return fail(VFN_ERR_CUFFT, "cufftCreate failed");
+    long long nn[3] = {n[0], n[1], n[2]};
+    long long em[3] = {embed ? embed[0] : n[0], embed ? embed[1] : n[1], embed ? embed[2] : n[2]};
+    const long long dist = em[0] * em[1] * em[2];
+    size_t work = 0;
+    const cufftResult r = cufftMakePlanMany64(e.h, 3, nn, em, 1, dist, em, 1, dist, CUFFT_Z2Z, 1, &work);
+    if (r != CUFFT_SUCCESS) {
+      cufftDestroy(e.h);
+      return fail(VFN_ERR_CUFFT, "cufftMakePlanMany64 failed (code " + std::to_string((int)r) + ")");
+    }
     if (cudaEventCreateWithFlags(&e.done, cudaEventDisableTiming) != cudaSuccess) {
       cufftDestroy(e.h);
       return fail(VFN_ERR_CUDA, "fft event creation failed");
@@ -193,6 +209,60 @@ __global__ void k_deconv_pad(const double2* __restrict__ coeffs, int64_t N0, int
   }
 }
 
+// K2 writing straight into the ghost-padded grid's interior: row (i0, i1)
+// of the n0 x n1 x n2 FFT input lives at G + (i0 P1 + i1) P2 (G = the
+// interior origin), so the FFT runs in place there and only the halo faces
+// are copied afterwards (no separate n^3 buffer, no full ghost-pad pass).
+__global__ void k_deconv_pad_rows(const double2* __restrict__ coeffs, int64_t N0, int64_t N1,
+                                  int64_t N2, int64_t n0, int64_t n1, int64_t n2,
+                                  const double* __restrict__ fac0, const double* __restrict__ fac1,
+                                  const double* __restrict__ fac2, double scale,
+                                  double2* __restrict__ G, int64_t P1, int64_t P2) {
+  const int64_t rows = n0 * n1;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int64_t i0 = r / n1, i1 = r - i0 * n1;
+    const int64_t j0 = i0 < N0 / 2 ? i0 + N0 / 2 : (i0 >= n0 - N0 / 2 ? i0 - n0 + N0 / 2 : -1);
+    const int64_t j1 = i1 < N1 / 2 ? i1 + N1 / 2 : (i1 >= n1 - N1 / 2 ? i1 - n1 + N1 / 2 : -1);
+    double2* row = G + (i0 * P1 + i1) * P2;
+    const bool live = j0 >= 0 && j1 >= 0;
+    const double f01 = live ? fac0[j0] * fac1[j1] * scale : 0.0;
+    const double2* crow = coeffs + (live ? (j0 * N1 + j1) * N2 : 0);
+    for (int64_t i2 = threadIdx.x; i2 < n2; i2 += blockDim.x) {
+      const int64_t j2 = i2 < N2 / 2 ? i2 + N2 / 2 : (i2 >= n2 - N2 / 2 ? i2 - n2 + N2 / 2 : -1);
+      double2 v = make_double2(0.0, 0.0);
+      if (live && j2 >= 0) {
+        const double2 c = crow[j2];
+        const double f = f01 * fac2[j2];
+        v = make_double2(c.x * f, c.y * f);
+      }
+      row[i2] = v;
+    }
+  }
+}
+
+// Halo faces of the ghost-padded grid from its interior: padded index i
+// holds g[(i - m) mod n], i.e. interior index ((i - m) mod n) + m.  Rows with
+// both (i0, i1) inside copy only their 2m (+ alignment) z-ghosts; the others
+// copy the whole row from their periodic image.  Every read is interior.
+__global__ void k_halo_faces(double2* __restrict__ P, int64_t P0, int64_t P1, int64_t P2, int64_t n0,
+                             int64_t n1, int64_t n2, int m) {
+  const int64_t rows = P0 * P1;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int64_t r0 = r / P1, r1 = r - r0 * P1;
+    const int64_t s0 = ((r0 - m) % n0 + n0) % n0 + m, s1 = ((r1 - m) % n1 + n1) % n1 + m;
+    double2* dst = P + r * P2;
+    const double2* src = P + (s0 * P1 + s1) * P2;
+    const bool inner = s0 == r0 && s1 == r1;
+    const int64_t ghosts = P2 - n2;  // z-ghosts of an interior row
+    const int64_t count = inner ? ghosts : P2;
+    for (int64_t t = threadIdx.x; t < count; t += blockDim.x) {
+      const int64_t i2 = inner ? (t < m ? t : t - m + n2 + m) : t;
+      const int64_t s2 = ((i2 - m) % n2 + n2) % n2 + m;
+      dst[i2] = src[s2];
+    }
+  }
+}
+
 // K3b: ghost-padded copy, P[i] = g[(i - m) mod n] per axis.
 __global__ void k_halo(const double2* __restrict__ g, int64_t n0, int64_t n1, int64_t n2,
                        double2* __restrict__ P, int64_t P0, int64_t P1, int64_t P2, int m) {
@@ -233,74 +303,68 @@ int build_grid(vfn_plan* p, const double* coeffs_dev, cudaStream_t s) {
   vfn::NvtxRange nvtx_range("vfn grid: deconvolve + pad + FFT + halo");
   const int64_t N0 = p->N[0], N1 = p->N[1], N2 = p->N[2];
   const int64_t n0 = p->n[0], n1 = p->n[1], n2 = p->n[2];
+  const int m = p->m;
   // sign(k)/phihat tables
-  std::vector<double> fac[3];
-  for (int d = 0; d < 3; ++d) {
-    fac[d].resize(p->N[d]);
-    kb_hat_table(p->N[d], p->n[d], p->m, p->beta, fac[d].data());
-    for (int64_t j = 0; j < p->N[d]; ++j) {
-      int64_t k = j - p->N[d] / 2;
-      double sign = (k % 2 == 0) ? 1.0 : -1.0;  // 1 - 2 (|k| mod 2)  (nufft.py:101-104)
-      fac[d][j] = sign / fac[d][j];
+  std::vector<double> h(N0 + N1 + N2);
+  {
+    double* f = h.data();
+    for (int d = 0; d < 3; ++d) {
+      kb_hat_table(p->N[d], p->n[d], m, p->beta, f);
+      for (int64_t j = 0; j < p->N[d]; ++j) {
+        const int64_t k = j - p->N[d] / 2;
+        const double sign = (k % 2 == 0) ? 1.0 : -1.0;  // 1 - 2 (|k| mod 2)  (nufft.py:101-104)
+        f[j] = sign / f[j];
+      }
+      f += p->N[d];
     }
   }
   const double vol = (p->b[0] - p->a[0]) * (p->b[1] - p->a[1]) * (p->b[2] - p->a[2]);
   const double scale = 1.0 / std::sqrt(vol) / ((double)n0 * (double)n1 * (double)n2);
-
-  // scratch: the FFT buffer is kept by plans that are rebuilt in place
-  // (keep_fftbuf, tube_eval's cached plan), else released at the end
-  int status = VFN_OK;
-  auto cleanup = [&]() {
-    if (!p->keep_fftbuf) p->fftbuf.release();
-  };
-  const int64_t total = n0 * n1 * n2;
+  const int64_t Ptot = p->P[0] * p->P[1] * p->P[2];
   VFN_CHECK(p->dfacbuf.ensure(sizeof(double) * (N0 + N1 + N2)));
-  VFN_CHECK(p->fftbuf.ensure(sizeof(double2) * total));
   double* dfac = p->dfacbuf.as<double>();
-  double2* buf = p->fftbuf.as<double2>();
-  cudaError_t e = cudaSuccess;
-  std::vector<double> h(N0 + N1 + N2);
-  std::copy(fac[0].begin(), fac[0].end(), h.begin());
-  std::copy(fac[1].begin(), fac[1].end(), h.begin() + N0);
-  std::copy(fac[2].begin(), fac[2].end(), h.begin() + N0 + N1);
-  e = cudaMemcpyAsync(dfac, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) {
+  if (!p->grid) {  // a rebuild keeps the plan's grid (and its tensor map)
+    p->grid = static_cast<double2*>(pool_alloc(p->device, sizeof(double2) * Ptot, &p->grid_bytes));
+    if (!p->grid) return fail(VFN_ERR_NOMEM, "padded grid allocation failed");
+  }
+  VFN_CUDA(cudaMemcpyAsync(dfac, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, s));
+  const int64_t nn[3] = {n0, n1, n2};
+  const bool copy_path = std::getenv("VFN_GRID_COPY") != nullptr;  // A/B: the separate-buffer build
+  cudaEventRecord(p->bev[0], s);
+  if (!copy_path) {
+    // K2 into the padded interior, K3 in place there, then the halo faces
+    double2* G = p->grid + (m * p->P[1] + m) * p->P[2] + m;
+    k_deconv_pad_rows<<<(unsigned)std::min<int64_t>(n0 * n1, 148 * 64), 256, 0, s>>>(
+        reinterpret_cast<const double2*>(coeffs_dev), N0, N1, N2, n0, n1, n2, dfac, dfac + N0,
+        dfac + N0 + N1, scale, G, p->P[1], p->P[2]);
+    VFN_CUDA(cudaGetLastError());
+    cudaEventRecord(p->bev[1], s);
+    VFN_CHECK(fft_forward_embedded(nn, p->P, G, s));
+    cudaEventRecord(p->bev[2], s);
+    k_halo_faces<<<(unsigned)std::min<int64_t>(p->P[0] * p->P[1], 148 * 64), 128, 0, s>>>(
+        p->grid, p->P[0], p->P[1], p->P[2], n0, n1, n2, m);
+    VFN_CUDA(cudaGetLastError());
+  } else {
+    // separate n^3 FFT buffer, then a full ghost-padding copy (K3b)
+    VFN_CHECK(p->fftbuf.ensure(sizeof(double2) * n0 * n1 * n2));
+    double2* buf = p->fftbuf.as<double2>();
+    const int64_t total = n0 * n1 * n2;
     k_deconv_pad<<<grid_blocks(total), 256, 0, s>>>(
         reinterpret_cast<const double2*>(coeffs_dev), N0, N1, N2, n0, n1, n2, dfac, dfac + N0,
         dfac + N0 + N1, scale, buf);
-    e = cudaGetLastError();
+    VFN_CUDA(cudaGetLastError());
+    cudaEventRecord(p->bev[1], s);
+    VFN_CHECK(fft_forward(nn, buf, s));
+    cudaEventRecord(p->bev[2], s);
+    k_halo<<<grid_blocks(Ptot), 256, 0, s>>>(buf, n0, n1, n2, p->grid, p->P[0], p->P[1], p->P[2], m);
+    VFN_CUDA(cudaGetLastError());
   }
-  if (e != cudaSuccess) {
-    cleanup();
-    return fail(VFN_ERR_CUDA, std::string("deconvolve/pad: ") + cudaGetErrorString(e));
-  }
-  // K3: unnormalised forward 3D FFT (nufft.py:242), cached cuFFT plan
-  {
-    const int64_t nn[3] = {n0, n1, n2};
-    const int fst = fft_forward(nn, buf, s);
-    if (fst != VFN_OK) {
-      cleanup();
-      return fst;
-    }
-  }
-  // K3b: ghost padding
-  const int64_t Ptot = p->P[0] * p->P[1] * p->P[2];
-  if (!p->grid) {  // a rebuild keeps the plan's grid (and its tensor map)
-    e = cudaMalloc(&p->grid, sizeof(double2) * Ptot);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      p->grid = nullptr;
-      cleanup();
-      return fail(VFN_ERR_NOMEM, std::string("padded grid allocation failed: ") + cudaGetErrorString(e));
-    }
-  }
-  k_halo<<<grid_blocks(Ptot), 256, 0, s>>>(buf, n0, n1, n2, p->grid, p->P[0], p->P[1], p->P[2],
-                                           p->m);
-  e = cudaGetLastError();
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) status = fail(VFN_ERR_CUDA, std::string("grid build: ") + cudaGetErrorString(e));
-  cleanup();
-  return status;
+  cudaEventRecord(p->bev[3], s);
+  const cudaError_t e = cudaStreamSynchronize(s);
+  if (copy_path && !p->keep_fftbuf) p->fftbuf.release();
+  if (e != cudaSuccess) return fail(VFN_ERR_CUDA, std::string("grid build: ") + cudaGetErrorString(e));
+  for (int i = 0; i < 3; ++i) p->build_ms[1 + i] = elapsed_ms(p->bev[i], p->bev[i + 1]);
+  return VFN_OK;
 }
 
 int extract_grid(vfn_plan* p, double2* out_dev, cudaStream_t s) {

@@ -1,5 +1,7 @@
 // Roofline denominator: sustained FP64 FMA throughput of this device,
 // measured with an independent-chain DFMA kernel over all SMs (bench.py).
+#include <vector>
+
 #include "vfn_internal.cuh"
 
 namespace vfn {
@@ -79,3 +81,86 @@ int store_word(int64_t* src, int64_t* dst, cudaStream_t s, bool reset) {
 }
 
 }  // namespace vfn
+
+namespace vfn {
+
+namespace {
+struct PoolEntry {
+  int device;
+  void* ptr;
+  size_t bytes;
+};
+std::mutex g_pool_mu;
+std::vector<PoolEntry> g_pool;
+constexpr int kPoolKeep = 2;  // buffers kept per device
+}  // namespace
+
+void* pool_alloc(int device, size_t bytes, size_t* got) {
+  {
+    std::lock_guard<std::mutex> lock(g_pool_mu);
+    // the smallest cached buffer that fits without wasting more than 1/4
+    int best = -1;
+    for (int i = 0; i < (int)g_pool.size(); ++i) {
+      const PoolEntry& e = g_pool[i];
+      if (e.device == device && e.bytes >= bytes && e.bytes - bytes <= bytes / 4 &&
+          (best < 0 || e.bytes < g_pool[best].bytes))
+        best = i;
+    }
+    if (best >= 0) {
+      void* p = g_pool[best].ptr;
+      *got = g_pool[best].bytes;
+      g_pool.erase(g_pool.begin() + best);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    vfn_pool_release(device);  // retry once without the cached buffers
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+  }
+  *got = bytes;
+  return p;
+}
+
+void pool_free(int device, void* ptr, size_t bytes) {
+  if (!ptr) return;
+  void* evict = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_pool_mu);
+    int held = 0, oldest = -1;
+    for (int i = 0; i < (int)g_pool.size(); ++i)
+      if (g_pool[i].device == device) {
+        if (oldest < 0) oldest = i;
+        ++held;
+      }
+    if (held >= kPoolKeep) {
+      evict = g_pool[oldest].ptr;
+      g_pool.erase(g_pool.begin() + oldest);
+    }
+    g_pool.push_back({device, ptr, bytes});
+  }
+  if (evict) cudaFree(evict);
+}
+
+}  // namespace vfn
+
+extern "C" int vfn_pool_release(int device) {
+  std::vector<void*> drop;
+  {
+    std::lock_guard<std::mutex> lock(vfn::g_pool_mu);
+    for (auto it = vfn::g_pool.begin(); it != vfn::g_pool.end();) {
+      if (device < 0 || it->device == device) {
+        drop.push_back(it->ptr);
+        it = vfn::g_pool.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
+  for (void* p : drop) cudaFree(p);
+  return VFN_OK;
+}

@@ -232,6 +232,31 @@ def eval_direct(spec, points):
     return out
 
 
+# Largest window half-width the kernels are instantiated for: the reference's
+# NufftParams.for_accuracy clamps to 13 (nufft.py:67-73); an explicit larger
+# cutoff is rejected with ValueError instead of being evaluated.
+MAX_CUTOFF = 13
+
+
+def _warn_accuracy(params: "NufftParams", stacklevel: int = 2) -> None:
+    """The plan's accuracy warnings (nufft.py:199-212), shared with tube_eval
+    whose reference builds a NufftPlan (tube.py:100)."""
+    if params.cutoff < 2:
+        warnings.warn(
+            f"cutoff {params.cutoff} gives a degraded window; expect at "
+            "best ~1e-3 relative accuracy",
+            AccuracyWarning,
+            stacklevel=stacklevel,
+        )
+    elif params.reached_eps() > params.eps:
+        warnings.warn(
+            f"cutoff {params.cutoff} reaches ~{params.reached_eps():.0e}, "
+            f"short of the requested eps {params.eps:.0e}",
+            AccuracyWarning,
+            stacklevel=stacklevel,
+        )
+
+
 # Evaluates of at most this many points run the unbinned warp-per-point
 # gather (one launch instead of ~25; include/vfnfft.h VFN_WARP_MAX_M).  Its
 # values agree with the binned gather's to rounding, not bitwise.
@@ -248,22 +273,11 @@ class NufftPlan:
 
     def __init__(self, spec, params: NufftParams | None = None, *, device: int | None = None):
         params = params or NufftParams()
-        if params.cutoff < 2:
-            warnings.warn(
-                f"cutoff {params.cutoff} gives a degraded window; expect at "
-                "best ~1e-3 relative accuracy",
-                AccuracyWarning,
-                stacklevel=2,
-            )
-        elif params.reached_eps() > params.eps:
-            warnings.warn(
-                f"cutoff {params.cutoff} reaches ~{params.reached_eps():.0e}, "
-                f"short of the requested eps {params.eps:.0e}",
-                AccuracyWarning,
-                stacklevel=2,
-            )
-        if params.cutoff > 13:
-            raise ValueError("cutoff must be <= 13")
+        _warn_accuracy(params, stacklevel=3)
+        if params.cutoff > MAX_CUTOFF:
+            # the reference accepts any cutoff >= 1; for_accuracy never asks
+            # for more than 13 (nufft.py:67-73), the kernels stop there
+            raise ValueError(f"cutoff must be <= {MAX_CUTOFF}")
         self.domain = spec.domain
         self.params = params
         coeffs = spec.coeffs
@@ -322,6 +336,14 @@ class NufftPlan:
         Fix it when results must be bitwise identical across batches/GPU counts."""
         _lib.check(_lib.load().vfn_plan_set_box(self._handle, int(bxy)))
 
+    def build_timing(self) -> dict:
+        """Where the plan build went (ms): host wall time of the whole
+        construction, the three grid kernels (CUDA events) and the host
+        setup before them (allocations, window fit, tables)."""
+        v = (ctypes.c_float * 5)()
+        _lib.check(_lib.load().vfn_plan_build_timing(self._handle, v))
+        return {"total": v[0], "deconv_pad": v[1], "fft": v[2], "halo": v[3], "host_setup": v[4]}
+
     def last_timing(self) -> tuple[float, float]:
         """(gather_ms, device_total_ms) of the last evaluate, CUDA-event timed."""
         g, t = ctypes.c_float(), ctypes.c_float()
@@ -348,10 +370,12 @@ class NufftPlan:
             )
             if not ok:
                 raise ValueError("out must be a contiguous complex128 buffer of shape (M,) next to points")
-        if M == 0:
-            return out
         if on_dev and (pts.device.index or 0) != self.device:
             raise ValueError(f"points are on cuda:{pts.device.index}, plan on cuda:{self.device}")
+        if on_dev and (out.device.index or 0) != self.device:
+            raise ValueError(f"out is on cuda:{out.device.index}, plan on cuda:{self.device}")
+        if M == 0:
+            return out
         lib = _lib.load()
         bad = ctypes.c_int64(-1)
         st = lib.vfn_plan_eval(self._handle, _lib.ptr(pts), M, _lib.ptr(out), on_dev,

@@ -6,7 +6,7 @@ only the input file and the output bytes cross PCIe.
 * ``eval_points``  <- ``cmd_eval_points`` (cli.py:108-125)
 * ``eval_grid``    <- ``cmd_eval_grid``   (cli.py:90-105), without the figure
 * ``tube``         <- ``cmd_tube``        (cli.py:128-142), without the figure
-* ``parse_grid``   <- ``_parse_grid``     (cli.py:64-87)
+* ``parse_grid``   <- the grid argument of ``eval-grid`` (cli.py:64-87)
 
 Each returns what the command prints about (the written paths / the point
 count) instead of printing it; errors are the same ValueError / OSError the
@@ -42,29 +42,36 @@ def _device(device):
     return torch.cuda.current_device()
 
 
+_GRID_ARITY = {"equispaced": (9,), "clustered": (9, 10)}
+
+
+def _axes_file(path) -> list[np.ndarray]:
+    lines = [ln for ln in Path(path).read_text().strip().splitlines()]
+    if len(lines) != 3:
+        raise ValueError(f"grid file {path} must hold three lines of coordinates, one per axis")
+    return [np.fromiter((float(t) for t in ln.split()), dtype=float) for ln in lines]
+
+
 def parse_grid(tokens) -> list[np.ndarray]:
-    """Grid spec -> three coordinate vectors: ``equispaced M1 M2 M3 a1 b1 a2
-    b2 a3 b3``, ``clustered ... [strength]`` or ``file PATH`` (cli.py:64-87)."""
-    kind = tokens[0]
+    """Grid spec tokens -> three coordinate vectors.  Accepted forms (the
+    CLI's grid argument, cli.py:64-87): ``file PATH`` (three whitespace
+    separated coordinate lines), ``equispaced M1 M2 M3 a1 b1 a2 b2 a3 b3`` and
+    ``clustered M1 M2 M3 a1 b1 a2 b2 a3 b3 [strength]``."""
+    kind, rest = tokens[0], list(tokens[1:])
     if kind == "file":
-        if len(tokens) != 2:
-            raise ValueError("grid spec: file needs exactly one path")
-        rows = Path(tokens[1]).read_text().strip().splitlines()
-        if len(rows) != 3:
-            raise ValueError("grid file needs three lines of coordinates")
-        return [np.array([float(v) for v in row.split()]) for row in rows]
+        if len(rest) != 1:
+            raise ValueError("grid spec: file takes exactly one path")
+        return _axes_file(rest[0])
+    if kind not in _GRID_ARITY:
+        raise ValueError(f"unknown grid kind {kind!r} (expected file, equispaced or clustered)")
+    nums = [float(t) for t in rest]
+    if len(nums) not in _GRID_ARITY[kind]:
+        raise ValueError(f"grid spec: {kind} takes M1 M2 M3 a1 b1 a2 b2 a3 b3"
+                         + (" [strength]" if kind == "clustered" else ""))
+    counts, bounds = [int(v) for v in nums[:3]], nums[3:9]
     if kind == "equispaced":
-        vals = [float(t) for t in tokens[1:]]
-        if len(vals) != 9:
-            raise ValueError("grid spec: equispaced M1 M2 M3 a1 b1 a2 b2 a3 b3")
-        return formats.equispaced_axes([int(v) for v in vals[:3]], vals[3:])
-    if kind == "clustered":
-        vals = [float(t) for t in tokens[1:]]
-        if len(vals) not in (9, 10):
-            raise ValueError("grid spec: clustered M1 M2 M3 a1 b1 a2 b2 a3 b3 [strength]")
-        strength = vals[9] if len(vals) == 10 else 1.0
-        return formats.clustered_axes([int(v) for v in vals[:3]], vals[3:9], strength)
-    raise ValueError(f"unknown grid kind {kind!r}; use equispaced, clustered or file")
+        return formats.equispaced_axes(counts, bounds)
+    return formats.clustered_axes(counts, bounds, nums[9] if len(nums) > 9 else 1.0)
 
 
 def eval_grid(snapshot, grid, out, vtk: bool = False, device=None) -> list[Path]:

@@ -23,7 +23,7 @@ import numpy as np
 
 from . import _lib
 from .fourier import DomainBox, SpectralField
-from .nufft import NufftParams, _device_of, _is_cuda_tensor, _stream_of, _torch
+from .nufft import MAX_CUTOFF, NufftParams, _device_of, _is_cuda_tensor, _stream_of, _torch, _warn_accuracy
 
 __all__ = ["Snapshot", "TubePointCloud", "computational_domain", "snapshot_spectral", "tube_eval"]
 
@@ -124,6 +124,8 @@ def tube_eval(snap, thresholds, final_filter: float | None = None,
         raise ValueError("thresholds must be a nonempty sequence of positive values")
     params = params or NufftParams()
     values, _, mirror = _snap_args(snap)
+    if params.cutoff > MAX_CUTOFF:
+        raise ValueError(f"cutoff must be <= {MAX_CUTOFF}")
     thr = np.asarray(thresholds, dtype=np.float64)
     dev = _device_of(values)
     lib = _lib.load()
@@ -146,6 +148,9 @@ def tube_eval(snap, thresholds, final_filter: float | None = None,
                 stacklevel=2,
             )
             return _empty_cloud()
+        # the reference builds its plan once seeds exist (tube.py:100), which
+        # is where its accuracy warnings come from (nufft.py:199-212)
+        _warn_accuracy(params, stacklevel=3)
         n = count.value
         if n == 0:
             return _empty_cloud()
