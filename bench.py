@@ -67,6 +67,9 @@ def parse():
     p.add_argument("--scaling", choices=["weak", "strong"], default="strong",
                    help="strong (default, BASELINE config 5): one point set split across the ranks; "
                         "weak: every rank evaluates its own full workload-sized point set")
+    p.add_argument("--shard-mode", choices=["keyrange", "block"], default="keyrange",
+                   help="strong scaling over N>1 ranks: keyrange (sample sort + all-to-all, default) or "
+                        "block (each rank gathers its own input-order block)")
     p.add_argument("--cutoff", type=int, default=6,
                    help="window half-width m (BASELINE's metric is quoted at the default 6)")
     return p.parse_args()
@@ -309,11 +312,16 @@ def run_ours(args):
     if args.gather:
         plan.set_gather(args.gather)
 
-    # this rank's block of points, resident in HBM: a whole workload-sized
-    # block per rank (weak) or a 1/world slice of one point set (strong)
+    # this rank's block of points, resident in HBM: a 1/world block of ONE
+    # point set (strong; the same global set at every world size) or a whole
+    # workload-sized set per rank (weak)
+    from paper_1605_01244_b200.parallel import ShardStats, evaluate_sharded
+
     lo, hi = shard_range(w.npoints, world, rank) if args.scaling == "strong" else (0, w.npoints)
     M = hi - lo
-    if name == "c5":
+    if args.scaling == "strong" or world == 1:
+        pts = workloads.device_points(name, lo, hi, dev)
+    elif name == "c5":
         gen = torch.Generator(device=dev)
         gen.manual_seed(2005 + 7919 * rank)
         pts = torch.rand((M, 3), dtype=torch.float64, device=dev, generator=gen) - 0.5
@@ -321,10 +329,19 @@ def run_ours(args):
         pts = torch.as_tensor(workloads.points(name)[lo:hi]).to(dev)
     out = torch.empty(M, dtype=torch.complex128, device=dev)
     stream = torch.cuda.current_stream(dev)
+    # strong scaling over several ranks: key-range sharding (sample sort +
+    # NCCL all-to-all of points and values, parallel.evaluate_sharded)
+    sharded = world > 1 and args.scaling == "strong"
+    stats = ShardStats() if sharded else None
+
+    def step(p, o):
+        if sharded:
+            return evaluate_sharded(plan, p, out=o, stats=stats, mode=args.shard_mode)
+        return plan.evaluate(p, out=o)
 
     # ---- device-resident timing
     for _ in range(args.warmup):
-        plan.evaluate(pts, out=out)
+        step(pts, out)
     torch.cuda.synchronize()
     clocks = ClockSampler(dev.index if dev.index is not None else 0)
     barrier()
@@ -334,14 +351,15 @@ def run_ours(args):
     gather_ms = []
     e0.record(stream)
     for _ in range(args.steps):
-        plan.evaluate(pts, out=out)
+        step(pts, out)
         gather_ms.append(plan.last_timing()[0])
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
     step_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
-    if M < (1 << 20) and M > plan_warp_max():
+    M_gather = stats.received if sharded else M  # points of this rank's gather launch
+    if M_gather < (1 << 20) and M_gather > plan_warp_max() and not sharded:
         # graph-replayed evaluates report the whole graph's time; the
         # roofline needs the gather kernel alone: a few eager evaluates
         plan.set_graphs(False)
@@ -350,7 +368,21 @@ def run_ours(args):
             plan.evaluate(pts, out=out)
             gather_ms.append(plan.last_timing()[0])
         plan.set_graphs(True)
-    g_ms = max_over_ranks(float(np.mean(gather_ms)))
+    g_mean = float(np.mean(gather_ms))
+    g_ms = max_over_ranks(g_mean)
+    shard_info = None
+    if sharded:
+        shard_info = {
+            "mode": args.shard_mode,
+            "partition_ms": max_over_ranks(stats.partition_ms),
+            "all_to_all_points_ms": max_over_ranks(stats.exchange_in_ms),
+            "evaluate_ms": max_over_ranks(stats.evaluate_ms),
+            "all_to_all_values_ms": max_over_ranks(stats.exchange_out_ms),
+            "decide_ms": max_over_ranks(stats.decide_ms),
+            "received_max": int(max_over_ranks(float(stats.received))),
+            "received_min": int(-max_over_ranks(-float(stats.received))),
+            "note": "last timed step, CUDA events on each rank, max over ranks",
+        }
 
     # ---- end to end through the public API: pinned host in, pinned host out
     # (pageable if the host cannot pin 40 B per point for every rank)
@@ -364,16 +396,38 @@ def run_ours(args):
         pinned = False
     pts_host.copy_(pts)
     pts_np, out_np = pts_host.numpy(), out_host.numpy()
-    plan.evaluate(pts_np, out=out_np)
+
+    def e2e_step():
+        if sharded:  # this rank's block: H2D, sharded evaluate, D2H
+            pts.copy_(pts_host, non_blocking=True)
+            r = evaluate_sharded(plan, pts, out=out, mode=args.shard_mode)
+            out_host.copy_(r, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+        else:
+            plan.evaluate(pts_np, out=out_np)  # returns after the D2H has landed
+
+    e2e_step()
     torch.cuda.synchronize()
     barrier()
     e2e_ms = []
     for _ in range(max(2, min(args.steps, 5))):
         t0 = time.perf_counter()
-        plan.evaluate(pts_np, out=out_np)  # returns after the D2H has landed
+        e2e_step()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    e2e_step = max_over_ranks(float(np.mean(e2e_ms)))
-    same = bool(np.array_equal(out_np, out.cpu().numpy()))
+    e2e_step_ms = max_over_ranks(float(np.mean(e2e_ms)))
+    dev_vals = out.cpu().numpy()
+    same = bool(np.array_equal(out_np, dev_vals)) if not sharded else None
+    sharded_equal = None
+    if sharded:
+        # bitwise against ONE unsharded evaluate of the whole set on this rank's plan
+        plan.set_gather(0)
+        plan.set_box(0)
+        whole = workloads.device_points(name, 0, w.npoints, dev)
+        ref = plan.evaluate(whole)[lo:hi].cpu().numpy()
+        del whole
+        sharded_equal = bool(np.array_equal(dev_vals, ref)) and bool(np.array_equal(out_np, ref))
+        sharded_equal = bool(max_over_ranks(0.0 if sharded_equal else 1.0) == 0.0)
+        same = sharded_equal
 
     # ---- roofline of the gather kernel (per rank, max-time rank)
     peak = None
@@ -389,7 +443,9 @@ def run_ours(args):
     if rank != 0:
         return
     fl = float(flop_per_point(CUTOFF))
-    achieved = fl * M / (g_ms * 1e-3) / 1e12
+    # the slowest rank's gather rate (its own launch's points and time)
+    achieved = -max_over_ranks(-(fl * M_gather / (g_mean * 1e-3) / 1e12)) if world > 1 else \
+        fl * M_gather / (g_ms * 1e-3) / 1e12
     result = {
         "metric": METRIC,
         "value": value,
@@ -405,11 +461,11 @@ def run_ours(args):
         "data": "synthetic, seeded (SURVEY 8d recipe); no dataset exists for this benchmark",
         "config": workload_config(name, world, args.scaling),
         "e2e": {
-            "value": total_points / (e2e_step * 1e-3),
+            "value": total_points / (e2e_step_ms * 1e-3),
             "unit": "points/s",
             "h2d_bytes_per_step": int(total_points * 24),
             "d2h_bytes_per_step": int(total_points * 16),
-            "ms_per_step": e2e_step,
+            "ms_per_step": e2e_step_ms,
             "matches_device_result_bitwise": same,
             "pinned_host_buffers": pinned,
         },
@@ -423,7 +479,7 @@ def run_ours(args):
             "frac": achieved / peak if peak else None,
             "traffic": None,
             "algorithmic": f"{int(fl)} flop/point = 2*((2m+1)^3+(2m+1)^2+(2m+1)) real FMA at m={CUTOFF}; "
-            f"{M} points per launch",
+            f"{M_gather} points per launch",
             "peak_source": "measured DFMA peak on this device (vfn_bench_fp64_peak, 0.5 s); "
             "MEASURED_PEAKS.json has no FP64 figure",
             "gather_ms": g_ms,
@@ -439,11 +495,14 @@ def run_ours(args):
     ng = 1
     for v in plan._n:
         ng *= v
-    result["roofline"]["algorithmic_bytes"] = 40 * M + 16 * ng  # points in/out + grid once
+    result["roofline"]["algorithmic_bytes"] = 40 * M_gather + 16 * ng  # points in/out + grid once
+    if shard_info is not None:
+        shard_info["sharded_equals_unsharded_bitwise"] = sharded_equal
+        result["sharding"] = shard_info
     if tr is not None and world == 1 and CUTOFF == 6:  # the committed capture is m = 6
         result["roofline"]["traffic"] = tr[0]
         result["roofline"]["traffic_source"] = tr[1]
-    result["gpu_launches"] = launches_per_step(plan, M) * args.steps
+    result["gpu_launches"] = (launches_per_step(plan, M_gather) + (5 if sharded else 0)) * args.steps
     if cpu is not None:
         sp = cpu["sample_points"]
         gpu_vals = plan.evaluate(sp)

@@ -140,7 +140,8 @@ int vfn_plan_set_box(vfn_plan* plan, int bxy);
 
 /* Kernel selection for vfn_plan_eval (benchmarks / A-B tests):
  * 0 = automatic, 1 = simple thread-per-point gather, 2 = DMMA box gather,
- * 3 = unbinned warp-per-point gather.  Automatic uses 3 for evaluates of at
+ * 3 = unbinned warp-per-point gather, 4 = binned with the automatic kernel
+ * (never the warp path; what vfn_plan_decide returns above VFN_WARP_MAX_M).  Automatic uses 3 for evaluates of at
  * most VFN_WARP_MAX_M points (no binning: two launches) and the binned
  * tensor-core gather above.  Values of the two paths agree to rounding
  * (~1e-16 relative), not bitwise. */
@@ -240,6 +241,42 @@ int vfn_field_write(const char* hdr_path, const char* psi_path, const char* rho_
 int vfn_vtk_write(const char* path, const char* title, const int64_t shape[3],
                   const double* const coords[3], int nscalars, const char* const* names,
                   const double* const* scalars, int on_device, int device, void* stream);
+
+/* ------------------------------------------------------------ multi-GPU
+ * One point set sharded by key range over the ranks of a job (
+ * "evaluation with a shared immutable plan is safe in parallel across
+ * disjoint point subsets", reference SPEC.md:258-259).  The collectives
+ * themselves run in the host layer (torch.distributed / NCCL,
+ * paper_1605_01244_b200/parallel.py); these are the device steps.
+ *
+ * Partition key of a point = (tile << 32) | (row0 + row): the row-major index
+ * of the gather tile holding its nearest oversampled cell, ties broken by
+ * global input row.  vfn_plan_part_keys writes the keys of rows 0, stride,
+ * 2 stride, ... (ceil(M / stride) keys, device memory) for the splitter
+ * sample.  vfn_plan_partition sends row i to destination
+ * d = #{splitters <= key_i} (nparts - 1 ascending device splitters),
+ * writing the points destination-major and in input order within a
+ * destination into `send` (device, M x 3), the send position of every row
+ * into pos (device int32), and the per-destination counts into counts
+ * (host, nparts).  Out-of-domain rows: VFN_ERR_OUTSIDE with the first
+ * (local) row.  vfn_gather_values puts returned values back in input
+ * order: out[i] = values[pos[i]] (device, complex128).                   */
+int vfn_plan_part_keys(vfn_plan* plan, const double* points, int64_t M, int64_t stride, int64_t row0,
+                       uint64_t* keys, void* stream);
+int vfn_plan_partition(vfn_plan* plan, const double* points, int64_t M, int64_t row0,
+                       const uint64_t* splitters, int nparts, double* send, int32_t* pos,
+                       int64_t* counts, int64_t* first_bad_row, void* stream);
+int vfn_gather_values(int device, const double* values, const int32_t* pos, int64_t M, double* out,
+                      void* stream);
+
+/* The gather decisions an evaluate of M points makes (gather variant 3 =
+ * warp per point or 4 = binned; box width 1 or 2), so that every rank of a
+ * sharded evaluate can pin the ones the unsharded call would take: values
+ * are then bitwise independent of the rank count.  From 2^20 points the
+ * box width depends on the points' local density: `sample` must hold the
+ * 16384 rows j * (M / 16384), j = 0..16383, of the whole set (device).   */
+int vfn_plan_decide(vfn_plan* plan, int64_t M, const double* sample, int nsample, int* variant_out,
+                    int* box_out, void* stream);
 
 /* Plan-build breakdown of the last vfn_plan_create (ms): [0] host wall time
  * of the whole call, [1] K2 deconvolve + pad, [2] K3 3D FFT, [3] halo

@@ -39,6 +39,8 @@ __all__ = [
     "bin_keys",
     "bin_permutation",
     "domain_violation",
+    "partition_keys",
+    "partition",
 ]
 
 
@@ -245,6 +247,33 @@ def bin_keys(points, a, b, n, box=(1, 1, 4), tile=(4, 4, 4)) -> np.ndarray:
 def bin_permutation(points, a, b, n, box=(1, 1, 4), tile=(4, 4, 4)) -> np.ndarray:
     """Stable argsort of bin_keys: sorted position -> input row."""
     return np.argsort(bin_keys(points, a, b, n, box, tile), kind="stable")
+
+
+def partition_keys(points, a, b, n, tile, row0: int = 0) -> np.ndarray:
+    """Key of the multi-GPU key-range partition (new): the
+    row-major index of the tile holding the nearest cell (same cell as the
+    reference gather, nufft.py:248-257) shifted left by 32, or'ed with the
+    global input row.  uint64 values < 2^63, returned as int64."""
+    _, l0 = nearest_cells(points, a, b, n)
+    cell = l0 % np.asarray(n)
+    tile = np.asarray(tile)
+    ntile = -(-np.asarray(n) // tile)
+    t = cell // tile
+    tile_id = (t[:, 0] * ntile[1] + t[:, 1]) * ntile[2] + t[:, 2]
+    return (tile_id.astype(np.int64) << 32) | (np.arange(len(points), dtype=np.int64) + row0)
+
+
+def partition(points, a, b, n, tile, splitters, row0: int = 0):
+    """Stable split by destination d = #{splitters <= key}: (send rows in
+    destination-major, input order within a destination; counts per
+    destination; pos = send position of every input row)."""
+    keys = partition_keys(points, a, b, n, tile, row0)
+    dest = np.searchsorted(np.asarray(splitters, dtype=np.int64), keys, side="right")
+    order = np.argsort(dest, kind="stable")
+    pos = np.empty(len(points), dtype=np.int64)
+    pos[order] = np.arange(len(points))
+    counts = np.bincount(dest, minlength=len(splitters) + 1)
+    return np.asarray(points)[order], counts, pos
 
 
 # ---------------------------------------------------------------------------

@@ -131,6 +131,19 @@ SIGNATURES = {
         [_cp, _cp, _c_i64_3, _vp * 3, ctypes.c_int, ctypes.POINTER(_cp), ctypes.POINTER(_vp),
          ctypes.c_int, ctypes.c_int, _vp],
     ),
+    "vfn_plan_part_keys": (
+        ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _vp, _vp]
+    ),
+    "vfn_plan_partition": (
+        ctypes.c_int,
+        [_vp, _vp, ctypes.c_int64, ctypes.c_int64, _vp, ctypes.c_int, _vp, _vp, _vp,
+         ctypes.POINTER(ctypes.c_int64), _vp],
+    ),
+    "vfn_gather_values": (ctypes.c_int, [ctypes.c_int, _vp, _vp, ctypes.c_int64, _vp, _vp]),
+    "vfn_plan_decide": (
+        ctypes.c_int,
+        [_vp, ctypes.c_int64, _vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), _vp],
+    ),
     "vfn_plan_build_timing": (ctypes.c_int, [_vp, ctypes.c_float * 5]),
     "vfn_pool_release": (ctypes.c_int, [ctypes.c_int]),
     "vfn_plan_last_timing": (

@@ -76,6 +76,14 @@ int32_t* iota_for(vfn_plan* p, int64_t M, bool* write) {
   return p->idx.as<int32_t>();
 }
 
+// Evaluates of at most this many points take the unbinned warp-per-point
+// gather (VFN_WARP_MAX_M in include/vfnfft.h; env VFN_WARP_MAX_M overrides).
+int64_t warp_max_m() {
+  int64_t v = VFN_WARP_MAX_M;
+  if (const char* e = std::getenv("VFN_WARP_MAX_M")) v = std::atoll(e);
+  return v;
+}
+
 int key_bits_for(int64_t nkeys) {
   int bits = 1;
   while (bits < 32 && ((int64_t)1 << bits) < nkeys) ++bits;
@@ -121,6 +129,9 @@ BinGeom make_geometry(const vfn_plan* p, int bxy) {
   return g;
 }
 
+constexpr int kDensitySample = 16384;            // sample rows of the density estimate
+constexpr int64_t kDensityMinM = (int64_t)1 << 20;  // evaluates from this size sample the density
+
 __global__ void k_sample_columns(const double* __restrict__ pts, int64_t M, int S, TorusMap tm,
                                  uint32_t* __restrict__ cols) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -135,14 +146,19 @@ __global__ void k_sample_columns(const double* __restrict__ pts, int64_t M, int 
 }
 
 // Expected number of OTHER points in a random point's 1 x 1 x 8 column,
-// estimated from the colliding pairs of a strided sample of S points.
-static int local_density(vfn_plan* p, const double* pts, int64_t M, cudaStream_t s, double* rho) {
-  const int S = 16384;
+// estimated from the colliding pairs of the strided sample rows j (M / S),
+// j < S, of the M points.  `pts` holds all M points, or (presampled) just the
+// S sample rows in order — the multi-GPU path assembles the same S rows from
+// every rank's block, so the estimate, and the box width chosen from it, do
+// not depend on the number of ranks.
+static int local_density(vfn_plan* p, const double* pts, int64_t M, cudaStream_t s, double* rho,
+                         bool presampled = false) {
+  const int S = kDensitySample;
   DevBuf& buf = p->sample;  // grow-only plan scratch: no cudaMalloc/cudaFree (a device sync) per call
   VFN_CHECK(buf.ensure(sizeof(uint32_t) * 2 * S));
   uint32_t* a = buf.as<uint32_t>();
   uint32_t* b = a + S;
-  k_sample_columns<<<(S + 255) / 256, 256, 0, s>>>(pts, M, S, p->map, a);
+  k_sample_columns<<<(S + 255) / 256, 256, 0, s>>>(pts, presampled ? S : M, S, p->map, a);
   VFN_CUDA(cudaGetLastError());
   size_t tmp = 0;
   VFN_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, a, b, S, 0, 32, s));
@@ -162,7 +178,9 @@ static int local_density(vfn_plan* p, const double* pts, int64_t M, cudaStream_t
   return VFN_OK;
 }
 
-int choose_geometry(vfn_plan* p, int64_t M, const double* pts_dev, cudaStream_t s, BinGeom* g) {
+// Box width for an evaluate of M points (sample: the points, or their
+// presampled density rows; see local_density).
+static int choose_bxy(vfn_plan* p, int64_t M, const double* sample, bool presampled, cudaStream_t s, int* out) {
   int bxy = p->box_mode;
   if (bxy == 0) {
     const char* fb = std::getenv("VFN_BOX_XY");  // experiment override
@@ -173,14 +191,21 @@ int choose_geometry(vfn_plan* p, int64_t M, const double* pts_dev, cudaStream_t 
   p->col_density_M = M;
   if (bxy == 0) {
     bxy = M >= cells ? 1 : 2;
-    if (pts_dev && tc_supported(p->m) && p->has_tmap && M >= (int64_t)1 << 20) {
+    if (sample && tc_supported(p->m) && p->has_tmap && M >= kDensityMinM) {
       // 1 x 1 columns once a column's box (TZ cells) holds >= ~32 points
       double rho = 0.0;
-      VFN_CHECK(local_density(p, pts_dev, M, s, &rho));
+      VFN_CHECK(local_density(p, sample, M, s, &rho, presampled));
       p->col_density = std::max(p->col_density, rho);
       bxy = rho * tc_tile_depth(p->m) / 8.0 >= 32.0 ? 1 : 2;
     }
   }
+  *out = bxy;
+  return VFN_OK;
+}
+
+int choose_geometry(vfn_plan* p, int64_t M, const double* pts_dev, cudaStream_t s, BinGeom* g) {
+  int bxy = 2;
+  VFN_CHECK(choose_bxy(p, M, pts_dev, false, s, &bxy));
   *g = make_geometry(p, bxy);
   p->last_geom = *g;
   p->has_last_geom = true;
@@ -356,6 +381,27 @@ int vfn_plan_geometry(const vfn_plan* p, int64_t M, int box_out[3], int tile_out
   return VFN_OK;
 }
 
+int vfn_plan_decide(vfn_plan* p, int64_t M, const double* sample, int nsample, int* variant_out,
+                    int* box_out, void* stream) {
+  if (!p || !variant_out || !box_out) return fail(VFN_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> plan_lock(p->mu);
+  DeviceGuard guard(p->device);
+  const double cells = (double)p->n[0] * (double)p->n[1] * (double)p->n[2];
+  const bool wants_sample = p->box_mode == 0 && !std::getenv("VFN_BOX_XY") && tc_supported(p->m) &&
+                            p->has_tmap && M >= kDensityMinM;
+  if (wants_sample && (!sample || nsample != kDensitySample))
+    return fail(VFN_ERR_INVALID, "decide: " + std::to_string(M) + " points need the " +
+                                     std::to_string(kDensitySample) + "-row density sample");
+  int v = p->gather_variant;
+  if (v == 0) v = M <= warp_max_m() ? 3 : 4;
+  int bxy = 2;
+  VFN_CHECK(choose_bxy(p, M, wants_sample ? sample : nullptr, true, reinterpret_cast<cudaStream_t>(stream), &bxy));
+  (void)cells;
+  *variant_out = v;
+  *box_out = bxy;
+  return VFN_OK;
+}
+
 int vfn_plan_set_box(vfn_plan* p, int bxy) {
   if (!p || bxy < 0 || bxy > 2) return fail(VFN_ERR_INVALID, "box must be 0 (auto), 1 or 2");
   std::lock_guard<std::mutex> plan_lock(p->mu);
@@ -372,7 +418,7 @@ int vfn_plan_set_graphs(vfn_plan* p, int enable) {
 }
 
 int vfn_plan_set_gather(vfn_plan* p, int variant) {
-  if (!p || variant < 0 || variant > 3) return fail(VFN_ERR_INVALID, "bad gather variant");
+  if (!p || variant < 0 || variant > 4) return fail(VFN_ERR_INVALID, "bad gather variant");
   std::lock_guard<std::mutex> plan_lock(p->mu);
   p->gather_variant = variant;
   return VFN_OK;
@@ -584,13 +630,6 @@ int outside(int64_t bad, int64_t* first_bad_row) {
 // and unit offsets); larger calls run as consecutive batches with the first
 // batch's bin geometry, so every point's value is the one a single call
 // would give it (HBM holds ~3e9 points with their scratch on a B200).
-// Evaluates of at most this many points take the unbinned warp-per-point
-// gather (VFN_WARP_MAX_M in include/vfnfft.h; env VFN_WARP_MAX_M overrides).
-int64_t warp_max_m() {
-  int64_t v = VFN_WARP_MAX_M;
-  if (const char* e = std::getenv("VFN_WARP_MAX_M")) v = std::atoll(e);
-  return v;
-}
 
 // Host-buffer evaluates of at least this many points run pipelined
 // (chunked H2D / evaluate / D2H); env VFN_PIPE_MIN overrides.

@@ -1,0 +1,247 @@
+// Multi-GPU key-range sharding of one point set (the reference
+// allows evaluating disjoint point subsets on a shared immutable plan,
+// SPEC.md:258-259).  Every rank holds a block of the input in input order;
+// the ranks agree on splitters of a partition key, each rank partitions its
+// block by destination (stable, so every destination receives its points in
+// input order), the points move with one all-to-all (torch.distributed in
+// parallel.py), every rank evaluates a spatially compact key range at full
+// point density, and the values return with a second all-to-all and are put
+// back in input order (vfn_gather_values).
+//
+// Partition key of a point: (tile << 32) | global row, where tile is the
+// row-major index of the gather tile of its nearest oversampled cell (the
+// tensor-core geometry's 4 x 4 x TZ tiles, independent of the box width) —
+// so a key range is a run of whole tiles (x-slabs for a uniform set), and
+// ties inside one tile (config 3's dense cloud) are split by row.
+#include <algorithm>
+#include <vector>
+
+#include <cub/device/device_scan.cuh>
+
+#include "vfn_device.cuh"
+
+namespace vfn {
+
+namespace {
+
+constexpr int kPartMax = 256;    // destinations
+constexpr int kPartThreads = 256;
+constexpr int kPartRounds = 16;  // points per thread per block
+constexpr int kPartChunk = kPartThreads * kPartRounds;
+
+struct TileMap {
+  TorusMap tm;
+  int tile[3];
+  int ntile[3];
+};
+
+__device__ __forceinline__ uint64_t tile_of(const double* __restrict__ pts, int64_t i, const TileMap& T,
+                                            bool& ok) {
+  int c[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double x = pts[3 * i + d];
+    ok = ok && inside(x, T.tm.a[d], T.tm.b[d]);
+    double delta;
+    c[d] = nearest_cell(x, T.tm.a[d], T.tm.amb[d], T.tm.nd[d], T.tm.n[d], delta) / T.tile[d];
+  }
+  return ((uint64_t)c[0] * T.ntile[1] + c[1]) * T.ntile[2] + c[2];
+}
+
+// destination = number of splitters <= key (splitters ascending)
+__device__ __forceinline__ int dest_of(uint64_t key, const uint64_t* s_split, int nsplit) {
+  int lo = 0, hi = nsplit;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (s_split[mid] <= key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_part_keys(const double* __restrict__ pts, int64_t M, int64_t stride, int64_t row0, TileMap T,
+                            uint64_t* __restrict__ keys, int64_t nkeys) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nkeys) return;
+  const int64_t i = j * stride;
+  bool ok = true;
+  const uint64_t t = tile_of(pts, i, T, ok);
+  keys[j] = (t << 32) | (uint64_t)(row0 + i);
+}
+
+// Pass 1: destination of every point (one byte), the per-(destination, block)
+// counts in destination-major order, and the first out-of-domain row.
+__global__ void __launch_bounds__(kPartThreads) k_part_count(const double* __restrict__ pts, int64_t M, int64_t row0,
+                                                             TileMap T, const uint64_t* __restrict__ split, int nsplit,
+                                                             uint8_t* __restrict__ dest, int32_t* __restrict__ counts,
+                                                             int nblocks, unsigned long long* __restrict__ bad) {
+  __shared__ uint64_t s_split[kPartMax];
+  __shared__ int s_cnt[kPartMax];
+  for (int i = threadIdx.x; i < nsplit; i += blockDim.x) s_split[i] = split[i];
+  for (int i = threadIdx.x; i <= nsplit; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kPartChunk;
+  for (int r = 0; r < kPartRounds; ++r) {
+    const int64_t i = base + r * kPartThreads + threadIdx.x;
+    if (i >= M) break;
+    bool ok = true;
+    const uint64_t t = tile_of(pts, i, T, ok);
+    if (!ok) atomicMin(bad, (unsigned long long)i);
+    const int d = dest_of((t << 32) | (uint64_t)(row0 + i), s_split, nsplit);
+    dest[i] = (uint8_t)d;
+    atomicAdd(&s_cnt[d], 1);
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d <= nsplit; d += blockDim.x) counts[(int64_t)d * nblocks + blockIdx.x] = s_cnt[d];
+}
+
+// Pass 2: stable scatter.  Block b owns points [b C, (b+1) C) in input order,
+// processed in rounds of 256; inside a round the order is warp-major, then
+// lane, so ranks come from __match_any_sync within a warp plus per-warp
+// per-destination prefix sums in shared memory.
+__global__ void __launch_bounds__(kPartThreads) k_part_scatter(const double* __restrict__ pts, int64_t M,
+                                                               const uint8_t* __restrict__ dest,
+                                                               const int32_t* __restrict__ offs, int nparts,
+                                                               int nblocks, double* __restrict__ send,
+                                                               int32_t* __restrict__ pos) {
+  constexpr int kW = kPartThreads / 32;
+  __shared__ int s_run[kPartMax];        // next position per destination
+  __shared__ int s_wc[kW][kPartMax];     // this round's count per warp and destination
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int d = threadIdx.x; d < nparts; d += blockDim.x) s_run[d] = offs[(int64_t)d * nblocks + blockIdx.x];
+  const int64_t base = (int64_t)blockIdx.x * kPartChunk;
+  for (int r = 0; r < kPartRounds; ++r) {
+    for (int k = threadIdx.x; k < kW * nparts; k += blockDim.x) s_wc[k / nparts][k % nparts] = 0;
+    __syncthreads();
+    const int64_t i = base + r * kPartThreads + threadIdx.x;
+    const bool live = i < M;
+    const int d = live ? dest[i] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    if (live && rank == 0) s_wc[warp][d] = __popc(peers);
+    __syncthreads();
+    if (live) {
+      int p = s_run[d] + rank;
+      for (int w = 0; w < warp; ++w) p += s_wc[w][d];
+      pos[i] = p;
+      const double x0 = pts[3 * i], x1 = pts[3 * i + 1], x2 = pts[3 * i + 2];
+      send[3 * (int64_t)p] = x0;
+      send[3 * (int64_t)p + 1] = x1;
+      send[3 * (int64_t)p + 2] = x2;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nparts; e += blockDim.x) {
+      int t = 0;
+      for (int w = 0; w < kW; ++w) t += s_wc[w][e];
+      s_run[e] += t;
+    }
+    __syncthreads();  // s_wc is zeroed by the next round
+  }
+}
+
+__global__ void k_part_totals(const int32_t* __restrict__ offs, int nparts, int nblocks, int64_t* __restrict__ out) {
+  const int d = threadIdx.x;
+  if (d <= nparts) out[d] = offs[(int64_t)d * nblocks];
+}
+
+__global__ void k_gather_values(const double2* __restrict__ vals, const int32_t* __restrict__ pos, int64_t M,
+                                double2* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < M) out[i] = vals[pos[i]];
+}
+
+TileMap tile_map(const vfn_plan* p) {
+  TileMap T;
+  T.tm = p->map;
+  const BinGeom g = make_geometry(p, 2);
+  for (int d = 0; d < 3; ++d) {
+    T.tile[d] = g.tile[d];
+    T.ntile[d] = g.ntile[d];
+  }
+  return T;
+}
+
+}  // namespace
+
+}  // namespace vfn
+
+using namespace vfn;
+
+extern "C" {
+
+int vfn_plan_part_keys(vfn_plan* p, const double* points, int64_t M, int64_t stride, int64_t row0,
+                       uint64_t* keys, void* stream) {
+  if (!p || (M > 0 && (!points || !keys)) || stride < 1) return fail(VFN_ERR_INVALID, "bad argument");
+  if (M <= 0) return VFN_OK;
+  std::lock_guard<std::mutex> plan_lock(p->mu);
+  DeviceGuard guard(p->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t n = (M + stride - 1) / stride;
+  k_part_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(points, M, stride, row0, tile_map(p), keys, n);
+  VFN_CUDA(cudaGetLastError());
+  return VFN_OK;
+}
+
+int vfn_plan_partition(vfn_plan* p, const double* points, int64_t M, int64_t row0, const uint64_t* splitters,
+                       int nparts, double* send, int32_t* pos, int64_t* counts, int64_t* first_bad_row,
+                       void* stream) {
+  vfn::NvtxRange nvtx_range("vfn partition by key range");
+  if (!p || !counts || (M > 0 && (!points || !send || !pos)) || (nparts > 1 && !splitters))
+    return fail(VFN_ERR_INVALID, "null argument");
+  if (nparts < 1 || nparts > kPartMax) return fail(VFN_ERR_INVALID, "destination count must be in 1..256");
+  if (M < 0 || M > INT32_MAX) return fail(VFN_ERR_INVALID, "point count out of range");
+  if (first_bad_row) *first_bad_row = -1;
+  for (int d = 0; d < nparts; ++d) counts[d] = 0;
+  if (M == 0) return VFN_OK;
+  std::lock_guard<std::mutex> plan_lock(p->mu);
+  DeviceGuard guard(p->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int nb = (int)((M + kPartChunk - 1) / kPartChunk);
+  const int64_t ncnt = (int64_t)nparts * nb + 1;
+  // scratch: dest bytes, counts, offsets, totals, bad word (plan's grow-only buffers)
+  VFN_CHECK(p->keys.ensure(M));  // dest (uint8)
+  VFN_CHECK(p->uscratch.ensure(sizeof(int32_t) * (2 * ncnt + 1) + sizeof(int64_t) * (nparts + 2)));
+  uint8_t* dest = p->keys.as<uint8_t>();
+  int32_t* cnt = p->uscratch.as<int32_t>();
+  int32_t* off = cnt + ncnt;
+  int64_t* tot = reinterpret_cast<int64_t*>(off + ncnt + (ncnt & 1));
+  int64_t* bad = tot + nparts + 1;
+  VFN_CUDA(cudaMemsetAsync(bad, 0x7f, sizeof(int64_t), s));
+  VFN_CUDA(cudaMemsetAsync(cnt + ncnt - 1, 0, sizeof(int32_t), s));
+  const TileMap T = tile_map(p);
+  k_part_count<<<nb, kPartThreads, 0, s>>>(points, M, row0, T, splitters, nparts - 1, dest, cnt, nb,
+                                           reinterpret_cast<unsigned long long*>(bad));
+  VFN_CUDA(cudaGetLastError());
+  size_t tmp = 0;
+  VFN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, off, (int)ncnt, s));
+  VFN_CHECK(p->sort_tmp.ensure(tmp));
+  VFN_CUDA(cub::DeviceScan::ExclusiveSum(p->sort_tmp.ptr, tmp, cnt, off, (int)ncnt, s));
+  k_part_scatter<<<nb, kPartThreads, 0, s>>>(points, M, dest, off, nparts, nb, send, pos);
+  VFN_CUDA(cudaGetLastError());
+  k_part_totals<<<1, 288, 0, s>>>(off, nparts, nb, tot);
+  VFN_CUDA(cudaGetLastError());
+  std::vector<int64_t> h(nparts + 2);
+  VFN_CUDA(cudaMemcpyAsync(h.data(), tot, sizeof(int64_t) * (nparts + 2), cudaMemcpyDeviceToHost, s));
+  VFN_CUDA(cudaStreamSynchronize(s));
+  const int64_t b = h[nparts + 1];
+  if (b != (int64_t)0x7f7f7f7f7f7f7f7fLL) {
+    if (first_bad_row) *first_bad_row = b;
+    return fail(VFN_ERR_OUTSIDE, "point (row " + std::to_string(b) + ") lies outside the domain");
+  }
+  for (int d = 0; d < nparts; ++d) counts[d] = h[d + 1] - h[d];
+  return VFN_OK;
+}
+
+int vfn_gather_values(int device, const double* values, const int32_t* pos, int64_t M, double* out,
+                      void* stream) {
+  if (M < 0 || (M > 0 && (!values || !pos || !out))) return fail(VFN_ERR_INVALID, "bad argument");
+  if (M == 0) return VFN_OK;
+  DeviceGuard guard(device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  k_gather_values<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(reinterpret_cast<const double2*>(values), pos, M,
+                                                              reinterpret_cast<double2*>(out));
+  VFN_CUDA(cudaGetLastError());
+  return VFN_OK;
+}
+
+}  // extern "C"

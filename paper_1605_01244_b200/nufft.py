@@ -287,6 +287,7 @@ class NufftPlan:
         self._modes = shape
         self._handle = None
         self._gather = 0
+        self._box = 0
         on_dev = 1 if _is_cuda_tensor(coeffs) else 0
         if not on_dev:
             coeffs = np.ascontiguousarray(np.asarray(coeffs), dtype=np.complex128)
@@ -322,7 +323,8 @@ class NufftPlan:
     def set_gather(self, variant: int) -> None:
         """0 = automatic (the warp-per-point gather up to WARP_MAX_M points, the
         binned tensor-core gather above), 1 = thread-per-point gather, 2 = DMMA
-        box gather, 3 = unbinned warp-per-point gather."""
+        box gather, 3 = unbinned warp-per-point gather, 4 = binned with the
+        automatic kernel at any M."""
         _lib.check(_lib.load().vfn_plan_set_gather(self._handle, int(variant)))
         self._gather = int(variant)
 
@@ -335,6 +337,69 @@ class NufftPlan:
         """Gather box width: 0 = automatic (by the points' local density), 1 or 2.
         Fix it when results must be bitwise identical across batches/GPU counts."""
         _lib.check(_lib.load().vfn_plan_set_box(self._handle, int(bxy)))
+        self._box = int(bxy)
+
+    # ---- multi-GPU steps (parallel.evaluate_sharded; include/vfnfft.h)
+
+    DENSITY_SAMPLE = 16384  # rows j * (M // 16384) decide the box width from 2^20 points
+
+    def decide(self, M: int, sample=None) -> tuple[int, int]:
+        """(gather variant, box width) an evaluate of M points takes: variant 3
+        (warp per point) or 4 (binned), box 1 or 2.  ``sample``: CUDA tensor of
+        the DENSITY_SAMPLE rows j * (M // DENSITY_SAMPLE) of the whole set
+        (needed from 2^20 points)."""
+        v, b = ctypes.c_int(), ctypes.c_int()
+        ptr = 0
+        ns = 0
+        if sample is not None:
+            sample = sample.to(_torch().float64).contiguous()
+            ptr, ns = _lib.ptr(sample), int(sample.shape[0])
+        _lib.check(_lib.load().vfn_plan_decide(self._handle, int(M), ptr, ns, ctypes.byref(v), ctypes.byref(b),
+                                               _stream_of(self.device)))
+        return v.value, b.value
+
+    def pin(self, variant: int, box: int) -> None:
+        """Fix the gather variant and box width (what ``decide`` returned)."""
+        self.set_gather(variant)
+        self.set_box(box)
+
+    def part_keys(self, points, stride: int = 1, row0: int = 0):
+        """Partition keys (tile << 32 | row0 + row) of rows 0, stride, ... of a
+        CUDA (M, 3) tensor, as a uint64 tensor (int64 storage)."""
+        t = _torch()
+        M = int(points.shape[0])
+        n = -(-M // stride) if M else 0
+        keys = t.empty(n, dtype=t.int64, device=points.device)
+        if n:
+            _lib.check(_lib.load().vfn_plan_part_keys(self._handle, _lib.ptr(points), M, int(stride), int(row0),
+                                                      _lib.ptr(keys), _stream_of(self.device)))
+        return keys
+
+    def partition(self, points, splitters, row0: int = 0, raise_outside: bool = True):
+        """Stable split of a CUDA (M, 3) tensor by key range: (send points,
+        per-destination counts (list), pos (int32 send position per row)), plus
+        the first out-of-domain local row (-1 if none) when not
+        ``raise_outside``.  ``splitters``: ascending int64 CUDA tensor of
+        nparts - 1 keys."""
+        t = _torch()
+        M = int(points.shape[0])
+        nparts = int(splitters.shape[0]) + 1
+        send = t.empty_like(points)
+        pos = t.empty(M, dtype=t.int32, device=points.device)
+        counts = (ctypes.c_int64 * nparts)()
+        bad = ctypes.c_int64(-1)
+        st = _lib.load().vfn_plan_partition(self._handle, _lib.ptr(points), M, int(row0),
+                                            _lib.ptr(splitters) if nparts > 1 else None, nparts,
+                                            _lib.ptr(send), _lib.ptr(pos), counts, ctypes.byref(bad),
+                                            _stream_of(self.device))
+        if st == _lib.VFN_ERR_OUTSIDE:
+            if raise_outside:
+                raise ValueError(_outside_message(points, bad.value, self.domain))
+            return send, [0] * nparts, pos, bad.value
+        _lib.check(st)
+        if raise_outside:
+            return send, list(counts), pos
+        return send, list(counts), pos, -1
 
     def build_timing(self) -> dict:
         """Where the plan build went (ms): host wall time of the whole
@@ -433,6 +498,19 @@ class NufftPlan:
             raise ValueError(_outside_message(pts, bad.value, self.domain))
         _lib.check(st)
         return keys, perm
+
+
+def gather_values(values, pos, out=None):
+    """out[i] = values[pos[i]] on the device (values back in input order
+    after a key-range exchange; include/vfnfft.h vfn_gather_values)."""
+    t = _torch()
+    M = int(pos.shape[0])
+    if out is None:
+        out = t.empty(M, dtype=t.complex128, device=pos.device)
+    dev = _device_of(pos)
+    _lib.check(_lib.load().vfn_gather_values(dev, _lib.ptr(values), _lib.ptr(pos), M, _lib.ptr(out),
+                                             _stream_of(dev)))
+    return out
 
 
 def eval_nufft(spec, points, params: NufftParams | None = None):

@@ -1,17 +1,41 @@
-"""Multi-GPU plumbing for the trafo: one process per GPU,
-torch.distributed for the control plane.
+"""Multi-GPU trafo: one process per GPU, torch.distributed (NCCL
+over NVLink/NVSwitch) for the collectives, the device steps in libvfnfft.
 
-* The coefficients (N1 N2 N3 complex128) are broadcast once per plan from
-  rank 0 over NCCL (NVLink/NVSwitch on an 8xB200 box) — the path's only
-  exchange step.  Every rank then builds its own replicated plan.
-* Points are partitioned into contiguous 1/P blocks in input order
-  (`shard_range`); each rank evaluates its block with no data-path
-  collective.  Results are bitwise independent of P because a point's value
-  depends only on the (identical) replicated grid and the point itself.
-* `gather_results` optionally assembles the full output on one rank.
+Plan build.  The coefficients (N1 N2 N3 complex128) are broadcast once from
+rank 0 (`broadcast_coefficients`); every rank builds the same replicated
+oversampled grid.
+
+Evaluate (`evaluate_sharded`).  Every rank holds a block of ONE point set in
+input order and gets the values of its own block back, in order.  The
+reference allows evaluating disjoint point subsets on a shared immutable
+plan; how the subsets are formed is this layer's choice:
+
+* ``mode="keyrange"`` (default): a distributed sample sort by the partition
+  key (tile of the nearest oversampled cell, then global row;
+  include/vfnfft.h vfn_plan_partition).  Splitters come from an all-gather
+  of key samples, the points move to the rank owning their key range with
+  one all-to-all, each rank evaluates a spatially compact range of whole
+  tiles at full point density, and the values come back with a second
+  all-to-all and are put back in input order on the device.  Input-order
+  blocks would instead leave every rank with a sparse sample of the whole
+  box: each grid tile staged for 1/P of its points (profiles/r01/
+  pcie_chunks.md: a 1/8 block costs 2.3x its share of the gather).
+* ``mode="block"``: each rank evaluates its own block (no exchange).
+
+Determinism.  Before evaluating, the ranks pin the gather decisions the
+unsharded call would take (`vfn_plan_decide`: warp-per-point vs binned
+from the global M, the box width from the density sample rows
+j * (M // 16384) of the whole set, assembled from the ranks' blocks).  A
+point's value then depends only on the point, the replicated grid and those
+pinned settings, so results are bitwise independent of the rank count P
+and of the mode, and equal to one `NufftPlan.evaluate` of the whole set.
+
+`gather_results` assembles per-rank outputs on one rank when wanted.
 """
 
 from __future__ import annotations
+
+from dataclasses import dataclass, field
 
 
 def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
@@ -58,10 +82,238 @@ def gather_results(local, total: int, dst: int = 0, group=None):
     return torch.view_as_complex(full) if local.is_complex() else full
 
 
-def evaluate_sharded(plan, points, rank: int, world: int, out=None):
-    """Evaluate this rank's contiguous block of `points` (global array) with `plan`."""
-    lo, hi = shard_range(points.shape[0], world, rank)
-    return plan.evaluate(points[lo:hi], out=out)
+# ---------------------------------------------------------------- collectives
+
+
+class _Comm:
+    """The few collectives the sharded evaluate needs, over a process group
+    (or a single process).  NCCL takes CUDA tensors directly; other backends
+    (gloo: CPU tests, ranks sharing one GPU) go through host copies."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist if dist.is_available() and dist.is_initialized() else None
+        self.group = group
+        self.world = self.dist.get_world_size(group) if self.dist else 1
+        self.rank = self.dist.get_rank(group) if self.dist else 0
+        self.nccl = bool(self.dist) and self.dist.get_backend(group) == "nccl"
+
+    def _io(self, t):
+        return t if self.nccl or not t.is_cuda else t.cpu()
+
+    def all_gather_ints(self, values: list[int]) -> list[list[int]]:
+        import torch
+
+        if self.world == 1:
+            return [list(values)]
+        dev = torch.device("cuda", torch.cuda.current_device()) if self.nccl else torch.device("cpu")
+        mine = torch.tensor(values, dtype=torch.int64, device=dev)
+        parts = [torch.empty_like(mine) for _ in range(self.world)]
+        self.dist.all_gather(parts, mine, group=self.group)
+        return [p.tolist() for p in parts]
+
+    def all_gather_rows(self, t, counts: list[int]):
+        """Concatenate every rank's (counts[r], ...) tensor in rank order."""
+        import torch
+
+        if self.world == 1:
+            return t
+        width = max(max(counts), 1)
+        src = self._io(t)
+        pad = torch.zeros((width,) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+        pad[: src.shape[0]] = src
+        parts = [torch.empty_like(pad) for _ in range(self.world)]
+        self.dist.all_gather(parts, pad, group=self.group)
+        out = torch.cat([p[:c] for p, c in zip(parts, counts)])
+        return out.to(t.device)
+
+    def all_reduce_min(self, v: int) -> int:
+        import torch
+
+        if self.world == 1:
+            return v
+        dev = torch.device("cuda", torch.cuda.current_device()) if self.nccl else torch.device("cpu")
+        x = torch.tensor([v], dtype=torch.int64, device=dev)
+        self.dist.all_reduce(x, op=self.dist.ReduceOp.MIN, group=self.group)
+        return int(x.item())
+
+    def all_reduce_sum(self, t):
+        if self.world == 1:
+            return t
+        x = self._io(t).clone()
+        self.dist.all_reduce(x, group=self.group)
+        return x.to(t.device)
+
+    def all_to_all(self, send, send_counts: list[int], recv_counts: list[int]):
+        """Rows of `send` (destination-major, send_counts[d] rows for rank d)
+        to their ranks; returns the received rows, source-major."""
+        import torch
+
+        if self.world == 1:
+            return send
+        src = self._io(send)
+        recv = torch.empty((sum(recv_counts),) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+        self.dist.all_to_all_single(recv, src, output_split_sizes=list(recv_counts),
+                                    input_split_sizes=list(send_counts), group=self.group)
+        return recv.to(send.device)
+
+
+# ---------------------------------------------------------------- sharded evaluate
+
+
+@dataclass
+class ShardStats:
+    """Where a sharded evaluate's time went on this rank (ms, CUDA events on
+    the current stream; host-side syncs of the exchange included)."""
+
+    decide_ms: float = 0.0
+    partition_ms: float = 0.0
+    exchange_in_ms: float = 0.0
+    evaluate_ms: float = 0.0
+    exchange_out_ms: float = 0.0
+    restore_ms: float = 0.0
+    sent: list = field(default_factory=list)
+    received: int = 0
+
+    @property
+    def exchange_ms(self) -> float:
+        return self.exchange_in_ms + self.exchange_out_ms
+
+
+def density_sample_rows(total: int, sample: int) -> tuple[int, int]:
+    """(stride, count) of the density sample rows j * stride, j < count."""
+    return max(1, total // sample), sample
+
+
+def splitters_from_samples(keys, world: int):
+    """world - 1 ascending splitters at the count quantiles of the sorted
+    key sample (int64 tensor): rank r owns keys in [s[r-1], s[r])."""
+    import torch
+
+    ks, _ = torch.sort(keys)
+    n = int(ks.shape[0])
+    if world <= 1 or n == 0:
+        return ks[:0]
+    idx = torch.tensor([(r * n) // world for r in range(1, world)], dtype=torch.int64, device=ks.device)
+    return ks[idx].contiguous()
+
+
+def _gather_values(values, pos):
+    if values.is_cuda:
+        from .nufft import gather_values
+
+        return gather_values(values, pos)
+    return values[pos.long()]  # host tensors: the CPU plumbing tests only
+
+
+class _Timer:
+    def __init__(self, enabled: bool):
+        import torch
+
+        self.on = enabled and torch.cuda.is_available() and torch.cuda.is_initialized()
+        self.marks = []
+        if self.on:
+            self.torch = torch
+
+    def mark(self):
+        if self.on:
+            e = self.torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.marks.append(e)
+
+    def spans(self, n: int) -> list[float]:
+        if not self.on or len(self.marks) < 2:
+            return [0.0] * n
+        self.torch.cuda.current_stream().synchronize()
+        return [a.elapsed_time(b) for a, b in zip(self.marks, self.marks[1:])]
+
+
+def evaluate_sharded(plan, points, group=None, mode: str = "keyrange", out=None, stats: ShardStats | None = None,
+                     samples_per_rank: int = 4096, comm=None):
+    """Values of this rank's block of one point set, in input order (see the
+    module docstring).  ``points``: this rank's (m, 3) block (a CUDA tensor
+    on the plan's device); the blocks of ranks 0..P-1 concatenated in rank
+    order are the whole set.  Every rank of ``group`` must call this.
+    ``comm`` replaces the torch.distributed group with an object offering
+    `_Comm`'s methods (tests run P ranks as threads of one process)."""
+    import torch
+
+    if mode not in ("keyrange", "block"):
+        raise ValueError("mode must be 'keyrange' or 'block'")
+    comm = comm if comm is not None else _Comm(group)
+    if points.dim() != 2 or points.shape[1] != 3:
+        raise ValueError(f"points must be an (M, 3) array, got shape {tuple(points.shape)}")
+    points = points.to(torch.float64).contiguous()
+    m = int(points.shape[0])
+    timer = _Timer(stats is not None)
+    timer.mark()
+    sizes = [c[0] for c in comm.all_gather_ints([m])]
+    total = sum(sizes)
+    row0 = sum(sizes[: comm.rank])
+
+    # the unsharded call's decisions, from the global M and global sample rows
+    sample = None
+    if total >= (1 << 20):
+        stride, cnt = density_sample_rows(total, plan.DENSITY_SAMPLE)
+        j0 = -(-row0 // stride)
+        j1 = min(cnt, -(-(row0 + m) // stride))
+        local = points[torch.arange(max(j0, 0), max(j1, j0), device=points.device) * stride - row0] \
+            if j1 > j0 else points[:0]
+        counts = [c[0] for c in comm.all_gather_ints([int(local.shape[0])])]
+        sample = comm.all_gather_rows(local, counts)
+    prev = (plan._gather, getattr(plan, "_box", 0))
+    variant, box = plan.decide(total, sample)
+    plan.pin(variant, box)
+    timer.mark()
+    try:
+        if mode == "block" or comm.world == 1 or variant == 3:
+            # the warp-per-point gather is point-local: no exchange needed
+            res = plan.evaluate(points, out=out)
+            timer.mark()
+            if stats is not None:
+                sp = timer.spans(2)
+                stats.decide_ms, stats.evaluate_ms = sp[0], sp[1]
+                stats.sent, stats.received = [m], m
+            return res
+        # splitters from an all-gather of key samples (same stride on every
+        # rank, so each rank's share of the sample follows its block size)
+        kstride = max(1, total // (samples_per_rank * comm.world))
+        keys = plan.part_keys(points, kstride, row0)
+        kcounts = [c[0] for c in comm.all_gather_ints([int(keys.shape[0])])]
+        split = splitters_from_samples(comm.all_gather_rows(keys, kcounts), comm.world)
+        send, send_counts, pos, bad = plan.partition(points, split, row0, raise_outside=False)
+        # an outside point anywhere fails every rank with the global first row
+        first = comm.all_reduce_min(row0 + bad if bad >= 0 else total)
+        if first < total:
+            mine = torch.zeros(3, dtype=torch.float64, device=points.device)
+            if row0 <= first < row0 + m:
+                mine = points[first - row0].clone()
+            bad_pt = comm.all_reduce_sum(mine).cpu().tolist()
+            raise ValueError(f"point {bad_pt} (row {first}) lies outside the domain "
+                             f"{list(plan.domain.a)} .. {list(plan.domain.b)}")
+        timer.mark()
+        recv_counts = [c[comm.rank] for c in comm.all_gather_ints(send_counts)]
+        recv = comm.all_to_all(send, send_counts, recv_counts)
+        timer.mark()
+        vals = plan.evaluate(recv)
+        timer.mark()
+        back = comm.all_to_all(torch.view_as_real(vals), recv_counts, send_counts)
+        timer.mark()
+        res = _gather_values(torch.view_as_complex(back.contiguous()), pos)
+        if out is not None:
+            out.copy_(res)
+            res = out
+        timer.mark()
+        if stats is not None:
+            sp = timer.spans(6)
+            (stats.decide_ms, stats.partition_ms, stats.exchange_in_ms, stats.evaluate_ms,
+             stats.exchange_out_ms, stats.restore_ms) = sp[:6]
+            stats.sent, stats.received = list(send_counts), int(sum(recv_counts))
+        return res
+    finally:
+        plan.set_gather(prev[0])
+        plan.set_box(prev[1])
 
 
 def eval_rectilinear_sharded(spec, coords, rank: int, world: int, evaluator=None):

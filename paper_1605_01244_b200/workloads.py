@@ -121,3 +121,28 @@ def rect_axes(count: int = 256):
     u = -1.0 + 2.0 * np.arange(count) / count
     x = 0.5 * np.tanh(3.0 * u) / np.tanh(3.0)
     return [x.copy(), x.copy(), x.copy()]
+
+
+DEVICE_CHUNK = 1 << 22  # generation unit of the device-side c5 set
+
+
+def device_points(name: str, lo: int, hi: int, device):
+    """Rows [lo, hi) of the workload's point set as a CUDA tensor.  c5's 2^28
+    uniform points are generated on the device in 2^22-point chunks, chunk k
+    from its own seed, so any rank's block of the ONE global set is the same
+    whatever the rank count (strong scaling shards one set)."""
+    import torch
+
+    w = WORKLOADS[name]
+    if name != "c5":
+        return torch.as_tensor(points(name)[lo:hi]).to(device)
+    out = torch.empty((hi - lo, 3), dtype=torch.float64, device=device)
+    gen = torch.Generator(device=device)
+    k0, k1 = lo // DEVICE_CHUNK, -(-hi // DEVICE_CHUNK)
+    for k in range(k0, k1):
+        c0, c1 = k * DEVICE_CHUNK, min((k + 1) * DEVICE_CHUNK, w.npoints)
+        gen.manual_seed(2005 + 7919 * k)
+        chunk = torch.rand((c1 - c0, 3), dtype=torch.float64, device=device, generator=gen) - 0.5
+        a, b = max(lo, c0), min(hi, c1)
+        out[a - lo:b - lo] = chunk[a - c0:b - c0]
+    return out

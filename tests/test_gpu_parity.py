@@ -974,8 +974,10 @@ def test_c_abi_from_plain_c(tmp_path):
 @pytest.mark.timeout(600)
 def test_bench_under_torchrun_two_ranks(vfb):
     """bench.py's N > 1 path (torchrun, one JSON line from rank 0, max over
-    ranks, weak scaling) with two ranks sharing this GPU over gloo
-    (VFN_DIST_BACKEND=gloo; NCCL refuses two ranks on one device)."""
+    ranks, strong scaling by key-range sharding: sample-sort splitters,
+    all-to-all of points and values) with two ranks sharing this GPU over
+    gloo (VFN_DIST_BACKEND=gloo; NCCL refuses two ranks on one device); the
+    sharded values equal one unsharded evaluate bitwise."""
     import json
     import os
     import subprocess
@@ -986,14 +988,17 @@ def test_bench_under_torchrun_two_ranks(vfb):
     env = dict(os.environ, VFN_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29573", os.path.join(REPO, "bench.py"),
-           "--gpus", "2", "--workload", "c1", "--steps", "3", "--warmup", "3"]
+           "--gpus", "2", "--workload", "c2", "--steps", "3", "--warmup", "3"]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=540, cwd=REPO, env=env)
     assert res.returncode == 0, res.stderr[-2000:]
     lines = [ln for ln in res.stdout.splitlines() if ln.strip().startswith("{")]
     assert len(lines) == 1, res.stdout
     out = json.loads(lines[0])
-    assert out["n_gpus"] == 2 and out["scaling"] == "weak" and out["config"]["points"] == 2 * 10000
+    assert out["n_gpus"] == 2 and out["scaling"] == "strong" and out["config"]["points"] == 10 ** 6
     assert out["value"] > 0 and out["e2e"]["matches_device_result_bitwise"] is True
+    sh = out["sharding"]
+    assert sh["sharded_equals_unsharded_bitwise"] is True and sh["mode"] == "keyrange"
+    assert 0.45e6 < sh["received_min"] <= sh["received_max"] < 0.55e6
 
 
 @pytest.mark.parametrize("variant", [0, 1, 2, 3])

@@ -1,0 +1,153 @@
+"""Key-range sharding of one point set over P ranks (
+paper_1605_01244_b200/parallel.py): the device partition vs the CPU
+restatement, and the sharded evaluate's bitwise P-invariance in the DEFAULT
+mode (no set_box / set_gather by the caller).  P ranks run as threads of
+this process (tests/simcomm.py), each with its own plan, as each GPU has its
+replicated plan; the torchrun test in test_gpu_parity.py runs the
+torch.distributed path."""
+
+import numpy as np
+import pytest
+
+from conftest import random_spectral
+from oracle import nfft_oracle as O
+from simcomm import run_ranks
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def vfb():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_1605_01244_b200 as pkg
+
+    return pkg
+
+
+def tile_of_plan(plan):
+    box, tile = plan.geometry(1 << 22)  # the tensor-core tile (independent of the box width)
+    return tile
+
+
+@pytest.mark.parametrize("nparts", [1, 2, 3, 8, 37])
+def test_partition_matches_cpu_restatement(vfb, offset_box, nparts):
+    import torch
+
+    spec = random_spectral(offset_box, (24, 20, 16), 1200 + nparts)
+    plan = vfb.NufftPlan(spec)
+    rng = np.random.default_rng(1210 + nparts)
+    pts = rng.uniform(offset_box.a, offset_box.b, (50000, 3))
+    pts[:300] = pts[0]  # a dense run inside one tile: ties split by row
+    row0 = 123456
+    dpts = torch.as_tensor(pts, device="cuda")
+    keys = plan.part_keys(dpts, 1, row0).cpu().numpy()
+    tile = tile_of_plan(plan)
+    ref_keys = O.partition_keys(pts, offset_box.a, offset_box.b, plan._n, tile, row0)
+    np.testing.assert_array_equal(keys, ref_keys)
+    np.testing.assert_array_equal(plan.part_keys(dpts, 7, row0).cpu().numpy(), ref_keys[::7])
+    split = np.sort(rng.choice(ref_keys, nparts - 1, replace=False)) if nparts > 1 else np.empty(0, np.int64)
+    split[: min(2, len(split))] = ref_keys[150]  # equal splitters: an empty destination
+    split = np.sort(split)
+    send, counts, pos = plan.partition(dpts, torch.as_tensor(split, device="cuda"), row0)
+    rsend, rcounts, rpos = O.partition(pts, offset_box.a, offset_box.b, plan._n, tile, split, row0)
+    assert counts == rcounts.tolist()
+    np.testing.assert_array_equal(pos.cpu().numpy(), rpos)
+    np.testing.assert_array_equal(send.cpu().numpy(), rsend)
+    vals = torch.as_tensor(rng.standard_normal(len(pts)) + 1j * rng.standard_normal(len(pts)), device="cuda")
+    back = vfb.nufft.gather_values(vals, pos).cpu().numpy()
+    np.testing.assert_array_equal(back, vals.cpu().numpy()[rpos])
+
+
+def test_partition_reports_outside_rows(vfb, unit_box):
+    import torch
+
+    plan = vfb.NufftPlan(random_spectral(unit_box, (8, 8, 8), 1220))
+    pts = np.random.default_rng(1221).uniform(0, 1, (9000, 3))
+    pts[[4097, 8000], 2] = [1.0, np.nan]
+    split = torch.tensor([1 << 40], dtype=torch.int64, device="cuda")
+    with pytest.raises(ValueError, match=r"\(row 4097\) lies outside"):
+        plan.partition(torch.as_tensor(pts, device="cuda"), split)
+
+
+def _sets(vfb):
+    from paper_1605_01244_b200 import workloads
+
+    rng = np.random.default_rng(1230)
+    uni = rng.uniform(-0.5, 0.5, (1 << 22, 3))
+    cloud = np.clip(rng.normal(0.0, 0.02, (1 << 22, 3)), -0.5, 0.4999)
+    return {"uniform": uni, "cloud": cloud}
+
+
+@pytest.mark.parametrize("kind", ["uniform", "cloud"])
+def test_sharded_default_mode_is_bitwise_P_invariant(vfb, kind):
+    """2^22 points as P = 1, 2, 4, 8 input-order blocks, default plan
+    settings: the key-range sharded evaluate (and the block mode) equals one
+    unsharded evaluate bitwise."""
+    import torch
+
+    from paper_1605_01244_b200.parallel import ShardStats, evaluate_sharded, shard_range
+
+    box = vfb.DomainBox((-0.5, -0.5, -0.5), (0.5, 0.5, 0.5))
+    spec = random_spectral(box, (64, 64, 64), 1240)
+    pts = _sets(vfb)[kind]
+    dpts = torch.as_tensor(pts, device="cuda")
+    ref = vfb.NufftPlan(spec).evaluate(dpts).cpu().numpy()
+    plans = [vfb.NufftPlan(spec) for _ in range(8)]
+    for P in (1, 2, 4, 8):
+        for mode in ("keyrange", "block"):
+            def rank(r, comm):
+                lo, hi = shard_range(len(pts), P, r)
+                st = ShardStats()
+                v = evaluate_sharded(plans[r], dpts[lo:hi], mode=mode, comm=comm, stats=st)
+                torch.cuda.synchronize()
+                return v.cpu().numpy(), st
+
+            res = run_ranks(P, rank)
+            got = np.concatenate([v for v, _ in res])
+            np.testing.assert_array_equal(got, ref, err_msg=f"{kind} P={P} {mode}")
+            if mode == "keyrange" and P > 1 and kind == "uniform":
+                recv = [st.received for _, st in res]
+                assert max(recv) <= 1.05 * len(pts) / P, recv  # balanced key ranges
+    for p in plans:  # the caller's settings are restored
+        assert p._gather == 0 and p._box == 0
+
+
+@pytest.mark.parametrize("M", [20000, 100000])
+def test_sharded_small_sets(vfb, offset_box, M):
+    """Below the warp-path threshold (point-local gather, no exchange) and a
+    binned set below the density-sampling size."""
+    import torch
+
+    from paper_1605_01244_b200.parallel import evaluate_sharded, shard_range
+
+    spec = random_spectral(offset_box, (20, 24, 16), 1250)
+    pts = np.random.default_rng(1251).uniform(offset_box.a, offset_box.b, (M, 3))
+    dpts = torch.as_tensor(pts, device="cuda")
+    ref = vfb.NufftPlan(spec).evaluate(dpts).cpu().numpy()
+    plans = [vfb.NufftPlan(spec) for _ in range(4)]
+    for P in (2, 3, 4):
+        res = run_ranks(P, lambda r, comm: evaluate_sharded(
+            plans[r], dpts[slice(*shard_range(M, P, r))], comm=comm).cpu().numpy())
+        np.testing.assert_array_equal(np.concatenate(res), ref)
+
+
+def test_sharded_outside_point_fails_every_rank(vfb, unit_box):
+    import torch
+
+    from paper_1605_01244_b200.parallel import evaluate_sharded, shard_range
+
+    spec = random_spectral(unit_box, (16, 16, 16), 1260)
+    pts = np.random.default_rng(1261).uniform(0, 1, (200000, 3))
+    pts[150001, 0] = 1.5
+    dpts = torch.as_tensor(pts, device="cuda")
+    plans = [vfb.NufftPlan(spec) for _ in range(3)]
+
+    def rank(r, comm):
+        with pytest.raises(ValueError, match=r"\(row 150001\) lies outside"):
+            evaluate_sharded(plans[r], dpts[slice(*shard_range(len(pts), 3, r))], comm=comm)
+        return True
+
+    assert all(run_ranks(3, rank))

@@ -127,3 +127,110 @@ def test_two_rank_rectilinear_slabs():
         assert p.exitcode == 0
     assert got.shape == ref.shape
     np.testing.assert_allclose(got, ref, rtol=1e-13, atol=1e-13 * np.abs(ref).max())
+
+
+class _OraclePlan:
+    """CPU stand-in for NufftPlan in the key-range plumbing test: the
+    partition keys, stable split and values come from the oracle (the device
+    steps are covered by tests/test_gpu_shard.py)."""
+
+    DENSITY_SAMPLE = 16384
+
+    def __init__(self, coeffs, a, b):
+        from oracle import nfft_oracle as O
+
+        self.O, self.coeffs, self.a, self.b = O, coeffs, a, b
+        self._n = tuple(2 * s for s in coeffs.shape)
+        self.tile = (4, 4, 8)
+        self._gather, self._box = 0, 0
+        self.evaluated = []
+
+        class D:
+            pass
+
+        self.domain = D()
+        self.domain.a, self.domain.b = a, b
+
+    def decide(self, M, sample=None):
+        return (3 if M <= 32768 else 4), 2
+
+    def pin(self, v, b):
+        self._gather, self._box = v, b
+
+    def set_gather(self, v):
+        self._gather = v
+
+    def set_box(self, b):
+        self._box = b
+
+    def part_keys(self, pts, stride=1, row0=0):
+        k = self.O.partition_keys(pts.numpy(), self.a, self.b, self._n, self.tile, row0)
+        return torch.as_tensor(k[::stride].copy())
+
+    def partition(self, pts, split, row0=0, raise_outside=True):
+        bad = self.O.domain_violation(pts.numpy(), self.a, self.b)
+        send, counts, pos = self.O.partition(pts.numpy(), self.a, self.b, self._n, self.tile,
+                                             split.numpy(), row0)
+        return torch.as_tensor(send), counts.tolist(), torch.as_tensor(pos.astype(np.int32)), bad
+
+    def evaluate(self, pts, out=None):
+        self.evaluated.append(int(pts.shape[0]))
+        return torch.as_tensor(self.O.nufft_eval(self.coeffs, self.a, self.b, pts.numpy()))
+
+
+def _keyrange_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1605_01244_b200.parallel import ShardStats, evaluate_sharded
+
+    a, b = (-1.5, 0.25, 2.0), (2.5, 1.25, 7.0)
+    coeffs = np.random.default_rng(7).standard_normal((8, 8, 8)) + 0j
+    pts = np.random.default_rng(8).uniform(a, b, (40000, 3))
+    lo, hi = shard_range(len(pts), world, rank)
+    plan = _OraclePlan(coeffs, a, b)
+    st = ShardStats()
+    got = evaluate_sharded(plan, torch.as_tensor(pts[lo:hi]), stats=st, samples_per_rank=512)
+    bad = pts.copy()
+    bad[30001, 1] = 9.0
+    blo, bhi = shard_range(len(bad), world, rank)
+    try:
+        evaluate_sharded(plan, torch.as_tensor(bad[blo:bhi]))
+        msg = None
+    except ValueError as e:
+        msg = str(e)
+    q.put((rank, got.numpy(), plan.evaluated, st.sent, msg))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_keyrange_exchange():
+    """The key-range sharded evaluate on 2 gloo ranks: sample-sort splitters,
+    all-to-all of points and values, values back in input order equal the
+    unsharded oracle bitwise; every rank evaluates only its key range; an
+    outside point fails both ranks with the global row."""
+    from oracle import nfft_oracle as O
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_keyrange_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=180) for _ in range(2)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    a, b = (-1.5, 0.25, 2.0), (2.5, 1.25, 7.0)
+    coeffs = np.random.default_rng(7).standard_normal((8, 8, 8)) + 0j
+    pts = np.random.default_rng(8).uniform(a, b, (40000, 3))
+    ref = O.nufft_eval(coeffs, a, b, pts)
+    np.testing.assert_array_equal(np.concatenate([r[1] for r in res]), ref)
+    # each rank evaluated one key range (x-slab of tiles), about half the points
+    for r in res:
+        assert abs(r[2][0] - 20000) < 2000, r[2]
+        assert sum(r[3]) == 20000
+    # rank 0 sent most of its points' second half elsewhere: a real exchange
+    assert res[0][3][1] > 5000 and res[1][3][0] > 5000
+    for r in res:
+        assert r[4] is not None and "(row 30001) lies outside" in r[4]
