@@ -440,12 +440,13 @@ def run_ours(args):
 
     total_points = w.npoints * (world if args.scaling == "weak" else 1)
     value = total_points / (step_ms * 1e-3)
-    if rank != 0:
-        return
     fl = float(flop_per_point(CUTOFF))
-    # the slowest rank's gather rate (its own launch's points and time)
+    # the slowest rank's gather rate (its own launch's points and time); a
+    # collective, so every rank computes it before rank 0 reports
     achieved = -max_over_ranks(-(fl * M_gather / (g_mean * 1e-3) / 1e12)) if world > 1 else \
         fl * M_gather / (g_ms * 1e-3) / 1e12
+    if rank != 0:
+        return
     result = {
         "metric": METRIC,
         "value": value,

@@ -200,11 +200,11 @@ int vfn_plan_partition(vfn_plan* p, const double* points, int64_t M, int64_t row
   const int64_t ncnt = (int64_t)nparts * nb + 1;
   // scratch: dest bytes, counts, offsets, totals, bad word (plan's grow-only buffers)
   VFN_CHECK(p->keys.ensure(M));  // dest (uint8)
-  VFN_CHECK(p->uscratch.ensure(sizeof(int32_t) * (2 * ncnt + 1) + sizeof(int64_t) * (nparts + 2)));
+  VFN_CHECK(p->uscratch.ensure(sizeof(int32_t) * 2 * ncnt + sizeof(int64_t) * (nparts + 2)));
   uint8_t* dest = p->keys.as<uint8_t>();
   int32_t* cnt = p->uscratch.as<int32_t>();
   int32_t* off = cnt + ncnt;
-  int64_t* tot = reinterpret_cast<int64_t*>(off + ncnt + (ncnt & 1));
+  int64_t* tot = reinterpret_cast<int64_t*>(off + ncnt);  // 8-byte aligned: 2 ncnt int32 before it
   int64_t* bad = tot + nparts + 1;
   VFN_CUDA(cudaMemsetAsync(bad, 0x7f, sizeof(int64_t), s));
   VFN_CUDA(cudaMemsetAsync(cnt + ncnt - 1, 0, sizeof(int32_t), s));

@@ -759,7 +759,10 @@ def test_warp_gather_small_evaluates(vfb, offset_box, m):
         sub = np.arange(M) if M < 2000 else rng.choice(M, 2000, replace=False)
         ref = O.gather_eval(grid, n, m, beta, pts[sub], offset_box.a, offset_box.b)
         l2, linf = rel_err(out[sub], ref)
-        tol = 1e-13 if m >= 3 else 1e-11
+        # relative to max|ref| of the sample (one value at M = 1); the widest
+        # windows deconvolve by the largest 1/phihat, so their grids carry
+        # a few ulps more FFT rounding
+        tol = (1e-13 if m <= 11 else 3e-13) if m >= 3 else 1e-11
         assert l2 < tol and linf < tol, (m, M, l2, linf)
         dev = plan.evaluate(torch.as_tensor(pts, device="cuda"))
         np.testing.assert_array_equal(dev.cpu().numpy(), out)
