@@ -615,10 +615,11 @@ def run_rect(args):
                 "h2d_bytes_per_step": int(coeffs.nbytes + 3 * 256 * 8), "d2h_bytes_per_step": int(npts * 16),
                 "ms_per_step": e2e_ms,
                 "matches_device_result_bitwise": bool(np.array_equal(host, out.cpu().numpy()))},
-        "roofline": {"bound": "tensor", "pipe": "FP64 (cuBLAS ZGEMM on DMMA)", "kernel": "3 ZGEMM passes (cuBLAS DMMA)", "achieved": achieved,
+        "roofline": {"bound": "tensor", "pipe": "FP64: DMMA (mma.sync m8n8k4 f64), peak = measured DFMA rate",
+                     "kernel": "3 separable passes, hand-written DMMA complex GEMM (vfn_zgemm.cu)", "achieved": achieved,
                      "peak": tf.value, "unit": "TFLOP/s", "frac": achieved / tf.value, "traffic": None,
                      "algorithmic": f"{cmacs} complex MACs = 8 flop each"},
-        "gpu_launches": 3 * args.steps,  # k_basis per axis; the ZGEMMs are cuBLAS's
+        "gpu_launches": (3 + 2 + 8) * args.steps,  # k_basis per axis, passes 1-2, pass 3 (8 slabs for host output)
         "clocks": clk,
     }
     if cpu is not None:

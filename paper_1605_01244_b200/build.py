@@ -1,7 +1,7 @@
 """Build libvfnfft.so in-tree with nvcc for sm_100a (no torch JIT cache).
 
 Every translation unit is compiled to an object in parallel, then linked
-(static cudart; cuFFT and cuBLAS from the CUDA toolkit via rpath)."""
+(static cudart; cuFFT from the CUDA toolkit via rpath)."""
 
 from __future__ import annotations
 
@@ -16,7 +16,7 @@ OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libvfnfft.so")
 LIB_CHECKS = os.path.join(HERE, "libvfnfft_checks.so")
 SOURCES = ["vfn_host.cpp", "vfn_stage.cpp", "vfn_kernels.cu", "vfn_gather.cu", "vfn_gather_tc.cu", "vfn_rect.cu",
-           "vfn_direct.cu", "vfn_util.cu", "vfn_tube.cu", "vfn_io.cpp", "vfn_io_kernels.cu", "vfn_shard.cu", "vfn_api.cu"]
+           "vfn_direct.cu", "vfn_util.cu", "vfn_tube.cu", "vfn_io.cpp", "vfn_io_kernels.cu", "vfn_shard.cu", "vfn_zgemm.cu", "vfn_api.cu"]
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -58,7 +58,7 @@ def build(verbose: bool = False, force: bool = False, checks: bool = False) -> s
     if failed:
         raise RuntimeError("nvcc build of libvfnfft.so failed")
     link = [NVCC, *ARCH, "-shared", "--cudart", "static", "-o", lib, *[o for o, _ in results],
-            "-L" + os.path.join(CUDA_HOME, "lib64"), "-lcufft", "-lcublas",
+            "-L" + os.path.join(CUDA_HOME, "lib64"), "-lcufft",
             "-Xlinker", "-rpath=" + os.path.join(CUDA_HOME, "lib64")]
     res = subprocess.run(link, capture_output=True, text=True)
     if verbose or res.returncode != 0:

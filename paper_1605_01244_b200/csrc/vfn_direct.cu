@@ -2,11 +2,11 @@
 // eval_direct, O(N1 N2 N3) complex MACs per point, as dense products on the
 // FP64 tensor cores.  Per chunk of P points:
 //   E_d[p, j] = exp(2 pi i k_j t_d(p)),  k_j = j - N_d/2,  t = (x - a)/(b - a)
-//   T[p, (k0, k1)] = sum_k2 E_2[p, k2] C[k0, k1, k2]          (cuBLAS ZGEMM)
+//   T[p, (k0, k1)] = sum_k2 E_2[p, k2] C[k0, k1, k2]          (DMMA ZGEMM, vfn_zgemm.cu)
 //   f[p] = norm * sum_k0 E_0[p, k0] sum_k1 E_1[p, k1] T[p, (k0, k1)]   (warp per point)
 // — the reference's separable basis (nufft.py:141-148) with the axis-3 sum
-// for all points of the chunk done as one ZGEMM.
-#include <cublas_v2.h>
+// for all points of the chunk done as one complex GEMM on the FP64 tensor
+// cores (hand-written, vfn_zgemm.cu).
 
 #include <algorithm>
 #include <map>
@@ -93,8 +93,6 @@ extern "C" int vfn_direct_eval(int device, const int64_t nm[3], const double a[3
   if (M == 0) return VFN_OK;
   DeviceGuard guard(device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  cublasHandle_t h = static_cast<cublasHandle_t>(blas_handle(device));
-  if (!h) return fail(VFN_ERR_CUBLAS, "cublasCreate failed");
   TorusMap tm;
   double vol = 1.0;
   for (int d = 0; d < 3; ++d) {
@@ -143,9 +141,7 @@ extern "C" int vfn_direct_eval(int device, const int64_t nm[3], const double a[3
   VFN_CHECK(T.ensure(sizeof(double2) * P * N01));
   const unsigned long long sentinel = ~0ull;
   VFN_CUDA(cudaMemcpyAsync(B.ptr, &sentinel, sizeof(sentinel), cudaMemcpyHostToDevice, s));
-  if (cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) return fail(VFN_ERR_CUBLAS, "cublasSetStream failed");
   const double norm = 1.0 / std::sqrt(vol);
-  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
   for (int64_t lo = 0; lo < M; lo += P) {
     const int64_t n = std::min(P, M - lo);
     double2* E0 = E.as<double2>();
@@ -155,12 +151,13 @@ extern "C" int vfn_direct_eval(int device, const int64_t nm[3], const double a[3
     k_direct_basis<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(pd + 3 * lo, n, lo, tm, N0, N1, N2, E0, E1, E2,
                                                                 B.as<unsigned long long>());
     VFN_CUDA(cudaGetLastError());
-    // column-major: T (N0N1 x n) = C^T (N0N1 x N2) * E2 (N2 x n); C is (N2 x N0N1) col-major
-    const cublasStatus_t r =
-        cublasZgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)N01, (int)n, N2, &one,
-                    reinterpret_cast<const cuDoubleComplex*>(cd), N2, reinterpret_cast<const cuDoubleComplex*>(E2),
-                    N2, &zero, T.as<cuDoubleComplex>(), (int)N01);
-    if (r != CUBLAS_STATUS_SUCCESS) return fail(VFN_ERR_CUBLAS, "cublasZgemm failed (" + std::to_string((int)r) + ")");
+    // T (n x N0N1) = E2 (n x N2) C^T, C read as (N0N1 x N2) row-major
+    ZGemm g;
+    g.M = n, g.N = N01, g.K = N2;
+    g.A = E2, g.lda = N2;
+    g.B = cd, g.ldb = N2, g.bt = true;
+    g.C = T.as<double2>(), g.ldc = N01;
+    VFN_CHECK(zgemm(g, s));
     k_direct_reduce<<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(T.as<double2>(), E0, E1, n, N0, N1, norm,
                                                                       od + lo);
     VFN_CUDA(cudaGetLastError());

@@ -243,9 +243,24 @@ int fit_window_poly(int m, double beta, double* coef, int max_deg);
 void* pool_alloc(int device, size_t bytes, size_t* got);
 void pool_free(int device, void* ptr, size_t bytes);
 
+// ---------------------------------------------------------------- complex GEMM (vfn_zgemm.cu)
+// C[b][m, n] = sum_k A[b][m, k] B[b][k, n], complex128 on the FP64 tensor
+// cores; A[m lda + k]; B[k ldb + n], or B[n ldb + k] with bt; C[m ldc + n];
+// batch b offsets the pointers by sA / sB / sC elements.
+struct ZGemm {
+  int64_t M = 0, N = 0, K = 0;
+  const double2* A = nullptr;
+  int64_t lda = 0, sA = 0;
+  const double2* B = nullptr;
+  int64_t ldb = 0, sB = 0;
+  bool bt = false;
+  double2* C = nullptr;
+  int64_t ldc = 0, sC = 0;
+  int batch = 1;
+};
+int zgemm(const ZGemm& g, cudaStream_t s);
+
 // ---------------------------------------------------------------- launchers
-// process-wide cuBLAS handle of `device` (cublasHandle_t; vfn_rect.cu)
-void* blas_handle(int device);  // per (host thread, device)
 // in-place unnormalised forward Z2Z 3D FFT through a cached cuFFT plan
 int fft_forward(const int64_t n[3], double2* data, cudaStream_t s);
 // in-place unnormalised inverse (e^{+2 pi i k l / n}) 3D Z2Z FFT

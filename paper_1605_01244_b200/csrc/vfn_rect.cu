@@ -1,9 +1,9 @@
 // K5: rectilinear tensor-grid evaluation (rectilinear.py:47-64) as three
 // exact separable 1D non-uniform passes.  Each pass contracts one mode with
 // its basis matrix E_d[m, k] = exp(2 pi i (y_m - a)(k - N/2)/(b - a))/sqrt(b - a)
-// (rectilinear.py:22-44), generated on the device; the contractions are plain
-// complex GEMMs (cuBLAS ZGEMM, FP64 tensor-core DMMA on sm_100a).
-#include <cublas_v2.h>
+// (rectilinear.py:22-44), generated on the device; the contractions are
+// complex GEMMs on the FP64 tensor cores (hand-written DMMA kernel,
+// vfn_zgemm.cu).
 
 #include <algorithm>
 #include <map>
@@ -27,37 +27,6 @@ __global__ void k_basis(const double* __restrict__ y, int64_t M, int64_t N, doub
   E[e] = make_double2(c * r, s * r);
 }
 
-// One cuBLAS handle per (host thread, device): a handle carries its stream
-// (cublasSetStream), so rectilinear and direct calls running concurrently on
-// one device from different threads must not share it.
-cublasHandle_t handle_for(int device) {
-  struct Handles {
-    std::map<int, cublasHandle_t> h;
-    ~Handles() {
-      for (auto& kv : h) cublasDestroy(kv.second);
-    }
-  };
-  thread_local Handles handles;
-  auto it = handles.h.find(device);
-  if (it != handles.h.end()) return it->second;
-  cublasHandle_t h = nullptr;
-  if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
-  cublasSetMathMode(h, CUBLAS_DEFAULT_MATH);
-  handles.h[device] = h;
-  return h;
-}
-
-void* blas_handle(int device) { return handle_for(device); }
-
-#define VFN_BLAS(expr)                                                                        \
-  do {                                                                                        \
-    cublasStatus_t _b = (expr);                                                               \
-    if (_b != CUBLAS_STATUS_SUCCESS) {                                                        \
-      st = fail(VFN_ERR_CUBLAS, std::string(#expr) + " failed (" + std::to_string((int)_b) + ")"); \
-      goto done;                                                                              \
-    }                                                                                         \
-  } while (0)
-
 // Host outputs: pass 3 runs in kRectSlabs slabs of output rows (m0), each
 // slab's D2H on a copy stream overlapping the next slab's GEMM.
 constexpr int kRectSlabs = 8;
@@ -65,8 +34,6 @@ constexpr int kRectSlabs = 8;
 int rect_eval(int device, const int64_t nm[3], const double a[3], const double b[3],
               const double* coeffs, const double* y[3], const int64_t Mv[3], double* out,
               int on_device, cudaStream_t s) {
-  cublasHandle_t h = handle_for(device);
-  if (!h) return fail(VFN_ERR_CUBLAS, "cublasCreate failed");
   const int64_t N0 = nm[0], N1 = nm[1], N2 = nm[2];
   const int64_t M0 = Mv[0], M1 = Mv[1], M2 = Mv[2];
   const size_t cb = sizeof(double2) * N0 * N1 * N2;
@@ -96,7 +63,6 @@ int rect_eval(int device, const int64_t nm[3], const double a[3], const double b
   DevBuf* E = sc->E;
   DevBuf* Y = sc->Y;
   int st = VFN_OK;
-  const double2 one = make_double2(1.0, 0.0), zero = make_double2(0.0, 0.0);
   const double2* Cd = reinterpret_cast<const double2*>(coeffs);
   double2* Fd = reinterpret_cast<double2*>(out);
   const double* yd[3];
@@ -132,21 +98,30 @@ int rect_eval(int device, const int64_t nm[3], const double a[3], const double b
   }
   if ((st = T1.ensure(t1b)) != VFN_OK) goto done;
   if ((st = T2.ensure(t2b)) != VFN_OK) goto done;
-  VFN_BLAS(cublasSetStream(h, s));
   {
-    auto* e0 = reinterpret_cast<const cuDoubleComplex*>(E[0].ptr);
-    auto* e1 = reinterpret_cast<const cuDoubleComplex*>(E[1].ptr);
-    auto* e2 = reinterpret_cast<const cuDoubleComplex*>(E[2].ptr);
-    auto* al = reinterpret_cast<const cuDoubleComplex*>(&one);
-    auto* be = reinterpret_cast<const cuDoubleComplex*>(&zero);
-    // pass 1, mode 3: T1 (N0N1 x M2) = C (N0N1 x N2) E2^T
-    VFN_BLAS(cublasZgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)M2, (int)(N0 * N1), (int)N2, al, e2,
-                         (int)N2, reinterpret_cast<const cuDoubleComplex*>(Cd), (int)N2, be,
-                         T1.as<cuDoubleComplex>(), (int)M2));
-    // pass 2, mode 2 (batched over n0): T2_n0 (M1 x M2) = E1 (M1 x N1) T1_n0 (N1 x M2)
-    VFN_BLAS(cublasZgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)M2, (int)M1, (int)N1, al,
-                                       T1.as<cuDoubleComplex>(), (int)M2, N1 * M2, e1, (int)N1, 0,
-                                       be, T2.as<cuDoubleComplex>(), (int)M2, M1 * M2, (int)N0));
+    const double2* e0 = E[0].as<double2>();
+    const double2* e1 = E[1].as<double2>();
+    const double2* e2 = E[2].as<double2>();
+    // pass 1, mode 3 (rectilinear.py:60): T1 (N0N1 x M2) = C (N0N1 x N2) E2^T
+    {
+      ZGemm g;
+      g.M = N0 * N1, g.N = M2, g.K = N2;
+      g.A = Cd, g.lda = N2;
+      g.B = e2, g.ldb = N2, g.bt = true;
+      g.C = T1.as<double2>(), g.ldc = M2;
+      if ((st = zgemm(g, s)) != VFN_OK) goto done;
+    }
+    // pass 2, mode 2 (rectilinear.py:62), batched over n0:
+    // T2_n0 (M1 x M2) = E1 (M1 x N1) T1_n0 (N1 x M2)
+    {
+      ZGemm g;
+      g.M = M1, g.N = M2, g.K = N1;
+      g.A = e1, g.lda = N1, g.sA = 0;
+      g.B = T1.as<double2>(), g.ldb = M2, g.sB = N1 * M2;
+      g.C = T2.as<double2>(), g.ldc = M2, g.sC = M1 * M2;
+      g.batch = (int)N0;
+      if ((st = zgemm(g, s)) != VFN_OK) goto done;
+    }
     // pass 3, mode 1: F (M0 x M1M2) = E0 (M0 x N0) T2 (N0 x M1M2); rows
     // [lo, lo + n) of F use rows [lo, lo + n) of E0
     const int nslab = on_device ? 1 : (int)std::min<int64_t>(kRectSlabs, M0);
@@ -164,9 +139,16 @@ int rect_eval(int device, const int64_t nm[3], const double a[3], const double b
     for (int j = 0; j < nslab; ++j) {
       const int64_t lo = M0 * j / nslab, n = M0 * (j + 1) / nslab - lo;
       if (n == 0) continue;
-      VFN_BLAS(cublasZgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)(M1 * M2), (int)n, (int)N0, al,
-                           T2.as<cuDoubleComplex>(), (int)(M1 * M2), e0 + lo * N0, (int)N0, be,
-                           reinterpret_cast<cuDoubleComplex*>(Fd) + lo * M1 * M2, (int)(M1 * M2)));
+      {
+        // pass 3, mode 1 (rectilinear.py:64): rows [lo, lo + n) of
+        // F (M0 x M1M2) = E0 (M0 x N0) T2 (N0 x M1M2)
+        ZGemm g;
+        g.M = n, g.N = M1 * M2, g.K = N0;
+        g.A = e0 + lo * N0, g.lda = N0;
+        g.B = T2.as<double2>(), g.ldb = M1 * M2;
+        g.C = Fd + lo * M1 * M2, g.ldc = M1 * M2;
+        if ((st = zgemm(g, s)) != VFN_OK) goto done;
+      }
       if (!on_device) {
         cudaEventRecord(sc->ev[j], s);
         if (staged) continue;
