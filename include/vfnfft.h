@@ -121,6 +121,17 @@ int vfn_rect_eval(int device, const int64_t nmodes[3], const double a[3], const 
                   int64_t M2, const double* y3, int64_t M3, double* out, int on_device,
                   void* stream);
 
+/* The same evaluation as three separable 1D type-2 NUFFT passes (SURVEY 8a
+ * R3): per axis, deconvolve + zero-pad to n = sigma N, FFT, and a (2m+1)-tap
+ * window gather at the axis' coordinates — the 3D trafo's algorithm in one
+ * dimension, each pass one fused kernel with the line staged in shared
+ * memory.  Accuracy ~10^-(2m+1) per pass (the plan's); needs sigma * N_d a
+ * power of two <= 4096 (VFN_ERR_INVALID otherwise: use vfn_rect_eval).   */
+int vfn_rect_eval_nufft(int device, const int64_t nmodes[3], const double a[3], const double b[3],
+                        const double* coeffs, const double* y1, int64_t M1, const double* y2, int64_t M2,
+                        const double* y3, int64_t M3, double sigma, int m, double* out, int on_device,
+                        void* stream);
+
 /* Exact series sum at M points, O(N1 N2 N3) per point (nufft.py:129-149).
  * Each N_d <= 1024.  Same point/domain conventions as vfn_plan_eval.   */
 int vfn_direct_eval(int device, const int64_t nmodes[3], const double a[3], const double b[3],

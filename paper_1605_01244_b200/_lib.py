@@ -64,6 +64,11 @@ SIGNATURES = {
         [ctypes.c_int, _c_i64_3, _c_f64_3, _c_f64_3, _vp, _vp, ctypes.c_int64, _vp,
          ctypes.c_int64, _vp, ctypes.c_int64, _vp, ctypes.c_int, _vp],
     ),
+    "vfn_rect_eval_nufft": (
+        ctypes.c_int,
+        [ctypes.c_int, _c_i64_3, _c_f64_3, _c_f64_3, _vp, _vp, ctypes.c_int64, _vp,
+         ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_double, ctypes.c_int, _vp, ctypes.c_int, _vp],
+    ),
     "vfn_direct_eval": (
         ctypes.c_int,
         [ctypes.c_int, _c_i64_3, _c_f64_3, _c_f64_3, _vp, _vp, ctypes.c_int64, _vp,

@@ -1014,4 +1014,24 @@ int vfn_rect_eval(int device, const int64_t nmodes[3], const double a[3], const 
   return rect_eval(device, nmodes, a, b, coeffs, y, Mv, out, on_device, as_stream(stream));
 }
 
+int vfn_rect_eval_nufft(int device, const int64_t nmodes[3], const double a[3], const double b[3],
+                        const double* coeffs, const double* y1, int64_t M1, const double* y2, int64_t M2,
+                        const double* y3, int64_t M3, double sigma, int m, double* out, int on_device,
+                        void* stream) {
+  vfn::NvtxRange nvtx_range("vfn rectilinear (NUFFT passes)");
+  if (!nmodes || !a || !b || !coeffs || !out) return fail(VFN_ERR_INVALID, "null argument");
+  VFN_CHECK(check_box(a, b));
+  for (int d = 0; d < 3; ++d)
+    if (nmodes[d] <= 0 || nmodes[d] % 2 != 0)
+      return fail(VFN_ERR_INVALID, "mode counts must be positive and even");
+  if (M1 < 0 || M2 < 0 || M3 < 0) return fail(VFN_ERR_INVALID, "negative coordinate count");
+  if (M1 > INT32_MAX || M2 > INT32_MAX || M3 > INT32_MAX) return fail(VFN_ERR_INVALID, "coordinate count too large");
+  if (m < 1) return fail(VFN_ERR_INVALID, "cutoff must be >= 1");
+  if (M1 * M2 * M3 == 0) return VFN_OK;
+  DeviceGuard guard(device);
+  const double* y[3] = {y1, y2, y3};
+  const int64_t Mv[3] = {M1, M2, M3};
+  return rect_eval(device, nmodes, a, b, coeffs, y, Mv, out, on_device, as_stream(stream), m, sigma);
+}
+
 }  // extern "C"

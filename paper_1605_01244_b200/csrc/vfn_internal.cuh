@@ -286,9 +286,12 @@ int store_word(int64_t* src, int64_t* dst, cudaStream_t s, bool reset);
 int gather_boxes(vfn_plan* p, const double* pts_dev, int64_t M, const BinGeom& g,
                  const uint32_t* keys_sorted, const int32_t* perm, double2* out_dev,
                  cudaStream_t s, bool* used);
+// exact passes (nufft_m == 0) or 1D-NUFFT passes with cutoff nufft_m
 int rect_eval(int device, const int64_t nmodes[3], const double a[3], const double b[3],
               const double* coeffs, const double* y[3], const int64_t Mv[3], double* out,
-              int on_device, cudaStream_t s);
+              int on_device, cudaStream_t s, int nufft_m = 0, double sigma = 2.0);
+int rect_nufft_device(int device, const int64_t nm[3], const double a[3], const double b[3], double sigma, int m,
+                      const double2* C, const double* y[3], const int64_t Mv[3], double2* F, cudaStream_t s);
 
 BinGeom make_geometry(const vfn_plan* p, int bxy);
 int choose_geometry(vfn_plan* p, int64_t M, const double* pts_dev, cudaStream_t s, BinGeom* g);

@@ -33,7 +33,7 @@ constexpr int kRectSlabs = 8;
 
 int rect_eval(int device, const int64_t nm[3], const double a[3], const double b[3],
               const double* coeffs, const double* y[3], const int64_t Mv[3], double* out,
-              int on_device, cudaStream_t s) {
+              int on_device, cudaStream_t s, int nufft_m, double sigma) {
   const int64_t N0 = nm[0], N1 = nm[1], N2 = nm[2];
   const int64_t M0 = Mv[0], M1 = Mv[1], M2 = Mv[2];
   const size_t cb = sizeof(double2) * N0 * N1 * N2;
@@ -89,12 +89,26 @@ int rect_eval(int device, const int64_t nm[3], const double a[3], const double b
       }
       yd[d] = Y[d].as<double>();
     }
+    if (nufft_m > 0) continue;  // NUFFT passes: no basis matrices
     if ((st = E[d].ensure(eb[d])) != VFN_OK) goto done;
     {
       int64_t tot = Mv[d] * nm[d];
       k_basis<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(yd[d], Mv[d], nm[d], a[d], b[d] - a[d],
                                                            E[d].as<double2>());
     }
+  }
+  if (nufft_m > 0) {
+    // separable 1D-NUFFT passes (vfn_rect_nufft.cu), then the whole result out
+    if ((st = rect_nufft_device(device, nm, a, b, sigma, nufft_m, Cd, yd, Mv, Fd, s)) != VFN_OK) goto done;
+    if (!on_device) {
+      if (fb >= ((size_t)1 << 20) && is_pageable(out)) {
+        if ((st = stage_d2h(device_stager(device), out, Fd, fb, s)) != VFN_OK) goto done;
+      } else if (cudaMemcpyAsync(out, Fd, fb, cudaMemcpyDeviceToHost, s) != cudaSuccess) {
+        st = fail(VFN_ERR_CUDA, "result download failed");
+        goto done;
+      }
+    }
+    goto finish;
   }
   if ((st = T1.ensure(t1b)) != VFN_OK) goto done;
   if ((st = T2.ensure(t2b)) != VFN_OK) goto done;
@@ -175,6 +189,7 @@ int rect_eval(int device, const int64_t nm[3], const double a[3], const double b
       cudaStreamWaitEvent(s, sc->ev[kRectSlabs], 0);
     }
   }
+finish:
   {
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) st = fail(VFN_ERR_CUDA, std::string("rectilinear: ") + cudaGetErrorString(e));

@@ -41,13 +41,20 @@ def basis_matrix(domain, n: int, axis: int, coords) -> np.ndarray:
     return np.exp(2j * np.pi * np.outer(y - a, k) / (b - a)) / np.sqrt(b - a)
 
 
-def eval_rectilinear(spec, coords, out=None):
+def eval_rectilinear(spec, coords, out=None, *, mode: str = "exact", params=None):
     """Series values on the tensor grid coords[0] x coords[1] x coords[2];
     complex (M1, M2, M3) (rectilinear.py:47-64).  ``out`` (extension, like
     ``NufftPlan.evaluate``'s): a C-contiguous complex128 (M1, M2, M3) array on
     the coefficients' side (numpy for host coefficients, a CUDA tensor for
     device ones) that receives the values; pinned host memory makes the
-    result download overlap the last pass."""
+    result download overlap the last pass.
+
+    ``mode`` (extension): "exact" (default; the reference's dense separable
+    contractions, to rounding) or "nufft" (three 1D type-2 NUFFT passes with
+    ``params`` — NufftParams, default sigma 2, m 6 — accurate to the plan's
+    ~10^-(2m+1); needs sigma * N a power of two <= 4096 per axis)."""
+    if mode not in ("exact", "nufft"):
+        raise ValueError("mode must be 'exact' or 'nufft'")
     if len(coords) != 3:
         raise ValueError("need exactly three coordinate vectors")
     coeffs = spec.coeffs
@@ -81,6 +88,17 @@ def eval_rectilinear(spec, coords, out=None):
     if 0 in M:
         return out
     lib = _lib.load()
+    if mode == "nufft":
+        from .nufft import NufftParams
+
+        params = params or NufftParams()
+        _lib.check(
+            lib.vfn_rect_eval_nufft(dev, _lib.i64x3(shape), _lib.f64x3(spec.domain.a),
+                                    _lib.f64x3(spec.domain.b), _lib.ptr(coeffs), _lib.ptr(ys[0]), M[0],
+                                    _lib.ptr(ys[1]), M[1], _lib.ptr(ys[2]), M[2], float(params.oversampling),
+                                    int(params.cutoff), _lib.ptr(out), on_dev, _stream_of(dev))
+        )
+        return out
     _lib.check(
         lib.vfn_rect_eval(dev, _lib.i64x3(shape), _lib.f64x3(spec.domain.a),
                           _lib.f64x3(spec.domain.b), _lib.ptr(coeffs), _lib.ptr(ys[0]), M[0],

@@ -1,0 +1,89 @@
+"""Rectilinear evaluation on the device: the exact passes
+(hand-written DMMA complex GEMM) and the separable 1D-NUFFT pass mode, vs
+the CPU restatement of rectilinear.py:47-64 (oracle) and the NDFT."""
+
+import numpy as np
+import pytest
+
+from conftest import random_spectral, rel_err
+from oracle import nfft_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def vfb():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_1605_01244_b200 as pkg
+
+    return pkg
+
+
+@pytest.mark.parametrize("shape,M,m,tol", [
+    ((16, 16, 16), (20, 17, 9), 6, 1e-12),
+    ((32, 8, 64), (33, 40, 7), 6, 1e-12),
+    ((8, 8, 8), (5, 300, 3), 7, 1e-12),
+    ((16, 32, 16), (64, 64, 64), 4, 1e-8),
+    ((2, 4, 2), (3, 5, 4), 6, 1e-12),
+])
+def test_nufft_passes_match_exact(vfb, offset_box, shape, M, m, tol):
+    spec = random_spectral(offset_box, shape, 1300 + sum(M))
+    rng = np.random.default_rng(1310 + m)
+    coords = [np.sort(rng.uniform(offset_box.a[d], offset_box.b[d], M[d])) for d in range(3)]
+    coords[1][0] = offset_box.a[1]  # the left endpoint
+    ref = O.rectilinear(spec.coeffs, offset_box.a, offset_box.b, coords)
+    got = vfb.eval_rectilinear(spec, coords, mode="nufft", params=vfb.NufftParams(cutoff=m))
+    l2, linf = rel_err(got, ref)
+    assert l2 < tol and linf < tol, (l2, linf)
+    exact = vfb.eval_rectilinear(spec, coords)
+    l2, linf = rel_err(exact, ref)
+    assert l2 < 1e-13 and linf < 1e-13, (l2, linf)
+
+
+def test_nufft_passes_config4_full(vfb):
+    """Config 4 (128^3 -> 256^3 tanh-clustered grid) in NUFFT mode vs the
+    exact device passes (themselves <= 1e-13 vs the oracle in
+    test_gpu_parity.test_config4_rectilinear_full_size), device-resident."""
+    import torch
+
+    from paper_1605_01244_b200 import workloads
+
+    w = workloads.WORKLOADS["c4"]
+    spec = vfb.SpectralField(vfb.DomainBox(*w.box), torch.as_tensor(workloads.coefficients("c4"), device="cuda"))
+    axes = workloads.rect_axes(256)
+    exact = vfb.eval_rectilinear(spec, axes).cpu().numpy()
+    fast = vfb.eval_rectilinear(spec, axes, mode="nufft").cpu().numpy()
+    l2, linf = rel_err(fast, exact)
+    assert l2 < 1e-12 and linf < 1e-12, (l2, linf)
+    # host coefficients and output: same bits as the device call
+    host = vfb.eval_rectilinear(vfb.SpectralField(spec.domain, workloads.coefficients("c4")), axes, mode="nufft")
+    np.testing.assert_array_equal(host, fast)
+
+
+def test_nufft_passes_reject_unsupported_sizes(vfb, unit_box):
+    spec = random_spectral(unit_box, (12, 16, 16), 1320)  # sigma N = 24: not a power of two
+    coords = [np.linspace(0, 0.9, 5)] * 3
+    with pytest.raises(ValueError, match="power of two"):
+        vfb.eval_rectilinear(spec, coords, mode="nufft")
+    with pytest.raises(ValueError, match="mode"):
+        vfb.eval_rectilinear(spec, coords, mode="fast")
+    got = vfb.eval_rectilinear(spec, coords)  # the exact mode covers it
+    ref = O.rectilinear(spec.coeffs, unit_box.a, unit_box.b, coords)
+    assert rel_err(got, ref)[1] < 1e-13
+
+
+@pytest.mark.parametrize("M,K", [(1, 1), (7, 3), (65, 130), (200, 33)])
+def test_exact_passes_ragged_gemm_shapes(vfb, offset_box, M, K):
+    """Tile edges of the DMMA complex GEMM (64 x 64 x 16 tiles): mode counts
+    and coordinate counts that are not tile multiples."""
+    shape = (2 * K, 2 * ((K + 1) // 2 + 1), 2)
+    spec = random_spectral(offset_box, shape, 1330 + M + K)
+    rng = np.random.default_rng(1331 + M)
+    coords = [rng.uniform(offset_box.a[d], offset_box.b[d], max(1, M - d)) for d in range(3)]
+    ref = O.rectilinear(spec.coeffs, offset_box.a, offset_box.b, coords)
+    got = vfb.eval_rectilinear(spec, coords)
+    l2, linf = rel_err(got, ref)
+    assert l2 < 1e-13 and linf < 1e-13, (l2, linf)
