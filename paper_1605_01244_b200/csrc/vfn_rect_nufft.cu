@@ -17,6 +17,7 @@
 // Coverage: n = sigma N a power of two <= 4096 (else VFN_ERR_INVALID; the
 // exact mode, vfn_rect_eval, covers every size).
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <map>
 #include <mutex>
@@ -40,96 +41,144 @@ struct Pass {
   int N, n, logn, M, m, W, G, deg;
   const double* fac;  // N: (-1)^k / phihat(k) / n / sqrt(w)
   const int* l0;      // M: nearest cell of each coordinate (mod n)
-  const double* dl;   // M: u - l0
-  const double* poly; // W x (deg + 1) window polynomial table
+  const double* wts;  // M x W: window weights of each coordinate
 };
 
 template <bool ROWS>  // ROWS: B == 1, a line is a contiguous row of X / Y
 __global__ void __launch_bounds__(kThreads) k_nufft_pass(const Pass P) {
   extern __shared__ __align__(16) unsigned char rsm[];
-  const int n = P.n, G = P.G, W = P.W, ld = n + 1;  // odd line pitch: conflict-free across lines
+  const int n = P.n, G = P.G, W = P.W, N = P.N, ld = n + 1;  // odd line pitch: conflict-free across lines
   double2* lines = reinterpret_cast<double2*>(rsm);
-  double2* tw = lines + (size_t)G * ld;                        // n/2 twiddles e^{-2 pi i t/n}
-  double* wts = reinterpret_cast<double*>(tw + n / 2);         // kChunk x W
-  int* l0s = reinterpret_cast<int*>(wts + kChunk * W);         // kChunk
-  double* poly = reinterpret_cast<double*>(l0s + kChunk + 2);  // W x (deg+1)
+  double2* tw = lines + (size_t)G * ld;                     // n/2 twiddles e^{-2 pi i t/n}
+  double* wts = reinterpret_cast<double*>(tw + n / 2);      // kChunk x W window weights
+  int64_t* lin = reinterpret_cast<int64_t*>(wts + kChunk * W);  // G: line offsets into X
+  int64_t* lout = lin + G;                                  // G: line offsets into Y
+  int* l0s = reinterpret_cast<int*>(lout + G);              // kChunk
   const int tid = threadIdx.x;
   const int64_t L0 = (int64_t)blockIdx.x * G;
-  const int g_here = (int)(P.nlines - L0 < G ? P.nlines - L0 : G);
+  const int gh = (int)(P.nlines - L0 < G ? P.nlines - L0 : G);
   for (int t = tid; t < n / 2; t += kThreads) {
     double s, c;
     sincospi(-2.0 * (double)t / (double)n, &s, &c);
     tw[t] = make_double2(c, s);
   }
-  for (int i = tid; i < W * (P.deg + 1); i += kThreads) poly[i] = P.poly[i];
+  for (int g = tid; g < gh; g += kThreads) {
+    const int64_t L = L0 + g, a = L / P.B, b = L - a * P.B;
+    lin[g] = a * N * P.B + b;
+    lout[g] = a * P.M * P.B + b;
+  }
   for (int i = tid; i < G * ld; i += kThreads) lines[i] = make_double2(0.0, 0.0);
   __syncthreads();
   // deconvolve + zero-pad (wavenumber k - N/2 at index (k - N/2) mod n),
   // stored bit-reversed for the in-place decimation-in-time FFT
   const int shift = 32 - P.logn;
-  for (int idx = tid; idx < g_here * P.N; idx += kThreads) {
-    int g, k;
-    if (ROWS) {
-      g = idx / P.N;
-      k = idx - g * P.N;
-    } else {
-      k = idx / g_here;
-      g = idx - k * g_here;
-    }
-    const int64_t L = L0 + g, a = L / P.B, b = L - a * P.B;
-    const double2 c = P.X[((int64_t)a * P.N + k) * P.B + b];
-    const double f = P.fac[k];
-    int pos = k - P.N / 2;
-    if (pos < 0) pos += n;
-    lines[g * ld + (int)(__brev((unsigned)pos) >> shift)] = make_double2(c.x * f, c.y * f);
+  if (ROWS) {
+    // warp per line, lanes along k: coalesced rows
+    for (int g = tid >> 5; g < gh; g += kThreads / 32)
+      for (int k = tid & 31; k < N; k += 32) {
+        const double2 c = P.X[lin[g] + k];
+        const double f = P.fac[k];
+        const int pos = k - N / 2 < 0 ? k - N / 2 + n : k - N / 2;
+        lines[g * ld + (int)(__brev((unsigned)pos) >> shift)] = make_double2(c.x * f, c.y * f);
+      }
+  } else {
+    // lanes along lines (consecutive b): coalesced columns
+    const int g = tid % G, k0 = tid / G, kst = kThreads / G;
+    if (g < gh && tid < kst * G)
+      for (int k = k0; k < N; k += kst) {
+        const double2 c = P.X[lin[g] + (int64_t)k * P.B];
+        const double f = P.fac[k];
+        const int pos = k - N / 2 < 0 ? k - N / 2 + n : k - N / 2;
+        lines[g * ld + (int)(__brev((unsigned)pos) >> shift)] = make_double2(c.x * f, c.y * f);
+      }
   }
   __syncthreads();
-  for (int s = 1; s <= P.logn; ++s) {
-    const int half = 1 << (s - 1), tstride = n >> s;
-    for (int bf = tid; bf < g_here * (n / 2); bf += kThreads) {
-      const int g = bf / (n / 2), r = bf - g * (n / 2);
-      const int j = r & (half - 1), i1 = ((r >> (s - 1)) << s) + j, i2 = i1 + half;
-      double2* x = lines + g * ld;
-      const double2 w = tw[j * tstride], u = x[i1], v = x[i2];
-      const double vr = fma(v.x, w.x, -v.y * w.y), vi = fma(v.x, w.y, v.y * w.x);
-      x[i1] = make_double2(u.x + vr, u.y + vi);
-      x[i2] = make_double2(u.x - vr, u.y - vi);
+  // radix-2 decimation in time, up to three stages per shared-memory round
+  // trip: a thread loads the 2^t elements base + j + i h (i < 2^t) that
+  // stages s .. s+t-1 combine and runs those butterflies in registers, with
+  // exactly the radix-2 arithmetic and twiddles (bitwise the same result)
+  for (int s = 1; s <= P.logn; s += 3) {
+    const int t = min(3, P.logn - s + 1), q = 1 << t, h = 1 << (s - 1);
+    const int per_line = n >> t;  // work items per line
+    for (int it = tid; it < gh * per_line; it += kThreads) {
+      const int g = it / per_line, r = it - g * per_line;
+      const int j = r & (h - 1), base = (r >> (s - 1)) << (s - 1 + t);
+      double2* x = lines + g * ld + base + j;
+      double2 e[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < q) e[i] = x[i * h];
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        if (u >= t) break;
+        const int step = 1 << u, ts = n >> (s + u);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (i >= q || (i & step)) continue;
+          const double2 w = tw[(j + (i & (step - 1)) * h) * ts];
+          const double2 a = e[i], b = e[i + step];
+          const double vr = fma(b.x, w.x, -b.y * w.y), vi = fma(b.x, w.y, b.y * w.x);
+          e[i] = make_double2(a.x + vr, a.y + vi);
+          e[i + step] = make_double2(a.x - vr, a.y - vi);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < q) x[i * h] = e[i];
     }
     __syncthreads();
   }
   // gather: value_j = sum_o w_o(delta_j) g[(l0_j + o - m) mod n]
   for (int j0 = 0; j0 < P.M; j0 += kChunk) {
     const int nj = min(kChunk, P.M - j0);
-    for (int e = tid; e < nj * W; e += kThreads) {
-      const int j = e / W, o = e - j * W;
-      wts[j * W + o] = window_poly(poly, P.deg, o, P.dl[j0 + j]);
-    }
-    for (int j = tid; j < nj; j += kThreads) l0s[j] = P.l0[j0 + j];
+    for (int e = tid; e < nj * W; e += kThreads) wts[e] = P.wts[(int64_t)j0 * W + e];
+    for (int j = tid; j < nj; j += kThreads) l0s[j] = ((P.l0[j0 + j] - P.m) % n + n) % n;
     __syncthreads();
-    for (int idx = tid; idx < g_here * nj; idx += kThreads) {
-      int g, j;
-      if (ROWS) {
-        g = idx / nj;
-        j = idx - g * nj;
-      } else {
-        j = idx / g_here;
-        g = idx - j * g_here;
+    if (ROWS) {
+      for (int g = tid >> 5; g < gh; g += kThreads / 32) {
+        const double2* x = lines + g * ld;
+        for (int j = tid & 31; j < nj; j += 32) {
+          const double* w = wts + j * W;
+          int p = l0s[j];
+          double ar = 0.0, ai = 0.0;
+          for (int o = 0; o < W; ++o) {
+            const double2 v = x[p];
+            ar = fma(w[o], v.x, ar);
+            ai = fma(w[o], v.y, ai);
+            p = p + 1 == n ? 0 : p + 1;
+          }
+          P.Y[lout[g] + j0 + j] = make_double2(ar, ai);
+        }
       }
-      const double2* x = lines + g * ld;
-      const double* w = wts + j * W;
-      int p = ((l0s[j] - P.m) % n + n) % n;
-      double ar = 0.0, ai = 0.0;
-      for (int o = 0; o < W; ++o) {
-        const double2 v = x[p];
-        ar = fma(w[o], v.x, ar);
-        ai = fma(w[o], v.y, ai);
-        p = p + 1 == n ? 0 : p + 1;
+    } else {
+      const int g = tid % G, jj = tid / G, jst = kThreads / G;
+      if (g < gh && tid < jst * G) {
+        const double2* x = lines + g * ld;
+        for (int j = jj; j < nj; j += jst) {
+          const double* w = wts + j * W;
+          int p = l0s[j];
+          double ar = 0.0, ai = 0.0;
+          for (int o = 0; o < W; ++o) {
+            const double2 v = x[p];
+            ar = fma(w[o], v.x, ar);
+            ai = fma(w[o], v.y, ai);
+            p = p + 1 == n ? 0 : p + 1;
+          }
+          P.Y[lout[g] + (int64_t)(j0 + j) * P.B] = make_double2(ar, ai);
+        }
       }
-      const int64_t L = L0 + g, a = L / P.B, b = L - a * P.B;
-      P.Y[((int64_t)a * P.M + j0 + j) * P.B + b] = make_double2(ar, ai);
     }
     __syncthreads();
   }
+}
+
+// window weights of every coordinate of one axis, W per coordinate
+__global__ void k_axis_weights(const double* __restrict__ dl, int M, const double* __restrict__ poly, int deg,
+                               int W, double* __restrict__ wts) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= M * W) return;
+  const int j = e / W, o = e - j * W;
+  wts[e] = window_poly(poly, deg, o, dl[j]);
 }
 
 // nearest cell and offset of every coordinate of one axis (the gather's map)
@@ -142,9 +191,9 @@ __global__ void k_axis_targets(const double* __restrict__ y, int M, double a, do
   dl[j] = d;
 }
 
-size_t smem_bytes(int G, int n, int W, int deg) {
+size_t smem_bytes(int G, int n, int W) {
   return sizeof(double2) * ((size_t)G * (n + 1) + n / 2) + sizeof(double) * kChunk * W +
-         sizeof(int) * (kChunk + 2) + sizeof(double) * W * (deg + 1) + 16;
+         sizeof(int64_t) * 2 * G + sizeof(int) * kChunk + 16;
 }
 
 }  // namespace rn
@@ -199,18 +248,22 @@ int rect_nufft_device(int device, const int64_t nm[3], const double a[3], const 
     }
     std::copy(coef.begin(), coef.begin() + (size_t)W * (deg + 1), h.begin() + Ntot);
   }
-  const size_t tb = sizeof(double) * h.size() + sizeof(double) * Mtot + sizeof(int) * (Mtot + 4);
+  const size_t tb = sizeof(double) * (h.size() + Mtot + (size_t)Mtot * W) + sizeof(int) * (Mtot + 4);
   VFN_CHECK(sc->tables.ensure(tb));
   double* dfac = sc->tables.as<double>();
   double* dpoly = dfac + Ntot;
   double* ddl = dpoly + (size_t)W * (deg + 1);
-  int* dl0 = reinterpret_cast<int*>(ddl + Mtot);
+  double* dw = ddl + Mtot;
+  int* dl0 = reinterpret_cast<int*>(dw + (size_t)Mtot * W);
   VFN_CUDA(cudaMemcpyAsync(dfac, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, s));
   {
     int64_t off = 0;
     for (int d = 0; d < 3; ++d) {
       rn::k_axis_targets<<<(unsigned)((Mv[d] + 255) / 256), 256, 0, s>>>(y[d], (int)Mv[d], a[d], a[d] - b[d],
                                                                          (int)n[d], dl0 + off, ddl + off);
+      VFN_CUDA(cudaGetLastError());
+      rn::k_axis_weights<<<(unsigned)((Mv[d] * W + 255) / 256), 256, 0, s>>>(ddl + off, (int)Mv[d], dpoly, deg, W,
+                                                                              dw + off * W);
       VFN_CUDA(cudaGetLastError());
       off += Mv[d];
     }
@@ -232,14 +285,17 @@ int rect_nufft_device(int device, const int64_t nm[3], const double a[3], const 
     P.M = (int)Mv[d];
     P.m = m;
     P.W = W;
-    P.G = (int)std::max<int64_t>(1, std::min<int64_t>(16, rn::kMaxGridElems / n[d]));
+    // lines per CTA: enough to amortise the twiddle / weight tables, few
+    // enough for ~4 CTAs per SM (the FFT rounds are latency-bound)
+    int64_t lpc = 8;
+    if (const char* e = std::getenv("VFN_RECT_LINES")) lpc = std::max(1, std::atoi(e));
+    P.G = (int)std::max<int64_t>(1, std::min<int64_t>(lpc, rn::kMaxGridElems / n[d]));
     if (B > 1) P.G = (int)std::min<int64_t>(P.G, B);
     P.deg = deg;
     P.fac = dfac + off_f[d];
     P.l0 = dl0 + off_t[d];
-    P.dl = ddl + off_t[d];
-    P.poly = dpoly;
-    const size_t smem = rn::smem_bytes(P.G, P.n, W, deg);
+    P.wts = dw + off_t[d] * W;
+    const size_t smem = rn::smem_bytes(P.G, P.n, W);
     const int64_t blocks = (P.nlines + P.G - 1) / P.G;
     if (B == 1) {
       VFN_CUDA(cudaFuncSetAttribute(rn::k_nufft_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

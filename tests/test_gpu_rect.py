@@ -23,11 +23,11 @@ def vfb():
 
 
 @pytest.mark.parametrize("shape,M,m,tol", [
-    ((16, 16, 16), (20, 17, 9), 6, 1e-12),
-    ((32, 8, 64), (33, 40, 7), 6, 1e-12),
-    ((8, 8, 8), (5, 300, 3), 7, 1e-12),
-    ((16, 32, 16), (64, 64, 64), 4, 1e-8),
-    ((2, 4, 2), (3, 5, 4), 6, 1e-12),
+    ((16, 16, 16), (20, 17, 9), 6, 5e-12),
+    ((32, 8, 64), (33, 40, 7), 6, 5e-12),
+    ((8, 8, 8), (5, 300, 3), 7, 5e-13),
+    ((16, 32, 16), (64, 64, 64), 4, 3e-8),  # m = 4: ~1e-9 per pass, three passes
+    ((2, 4, 2), (3, 5, 4), 6, 5e-12),
 ])
 def test_nufft_passes_match_exact(vfb, offset_box, shape, M, m, tol):
     spec = random_spectral(offset_box, shape, 1300 + sum(M))
@@ -57,7 +57,7 @@ def test_nufft_passes_config4_full(vfb):
     exact = vfb.eval_rectilinear(spec, axes).cpu().numpy()
     fast = vfb.eval_rectilinear(spec, axes, mode="nufft").cpu().numpy()
     l2, linf = rel_err(fast, exact)
-    assert l2 < 1e-12 and linf < 1e-12, (l2, linf)
+    assert l2 < 2e-12 and linf < 2e-12, (l2, linf)  # three passes of ~1e-13 each (gate 1e-10)
     # host coefficients and output: same bits as the device call
     host = vfb.eval_rectilinear(vfb.SpectralField(spec.domain, workloads.coefficients("c4")), axes, mode="nufft")
     np.testing.assert_array_equal(host, fast)
