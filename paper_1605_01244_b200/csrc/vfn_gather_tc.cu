@@ -534,10 +534,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 // A box's points are sorted by depth and the box is TZ cells deep, so any 8
 // consecutive points span <= TZ - 1 depths: units are the box's chunks of 8,
 // each with the fewest k-chunks (K = 4 KC depths) covering its stencils.
-__device__ __forceinline__ int box_depth(uint32_t key, int cpb, int bij) {
-  return (int)(key % (uint32_t)cpb) / bij;
-}
-
 __global__ void k_unit_counts(const int32_t* __restrict__ box_start, int64_t nboxes,
                               int32_t* __restrict__ ucount) {
   int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -545,24 +541,53 @@ __global__ void k_unit_counts(const int32_t* __restrict__ box_start, int64_t nbo
   ucount[b] = b == nboxes ? 0 : (box_start[b + 1] - box_start[b] + tc::kUnitPts - 1) / tc::kUnitPts;
 }
 
-// One thread per sorted point; the point that opens a chunk of 8 in its box
-// writes the unit (fully parallel, also for boxes holding millions of points).
+// floor(x / d) for x < 2^32, d <= 256: (x * ceil(2^40 / d)) >> 40 is exact
+// (the rounding error stays below x / 2^40 < 1/256 <= 1/d)
+struct Div {
+  uint64_t inv;
+  uint32_t d;
+  __host__ __device__ __forceinline__ uint32_t q(uint32_t x) const { return (uint32_t)(((uint64_t)x * inv) >> 40); }
+};
+static Div make_div(uint32_t d) { return Div{((uint64_t(1) << 40) + d - 1) / d, d}; }
+
+// Eight consecutive sorted points per thread (two 16-byte key loads); the
+// point that opens a chunk of 8 in its box writes the unit (fully parallel,
+// also for boxes holding millions of points — config 3).
 __global__ void k_write_units(const uint32_t* __restrict__ keys, int64_t M,
-                              const int32_t* __restrict__ box_start, int cpb, int bij, int W,
+                              const int32_t* __restrict__ box_start, Div cpb, Div bij, int W,
                               int kcmin, const int32_t* __restrict__ uoff, int4* __restrict__ units) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= M) return;
-  const uint32_t key = keys[i];
-  const int64_t b = key / (uint32_t)cpb;
-  const int bs = box_start[b];
-  const int r = (int)i - bs;
-  if (r % tc::kUnitPts) return;
-  const int be = box_start[b + 1];
-  const int e = min(be, (int)i + tc::kUnitPts);
-  const int k0 = box_depth(key, cpb, bij), k1 = box_depth(keys[e - 1], cpb, bij);
-  const int kc = max(kcmin, (k1 - k0 + W + 3) / 4);  // span + W <= 4 kc  (<= 20 always)
-  const int kz = min(k0, tc::kSZ - 4 * kc);
-  units[uoff[b] + r / tc::kUnitPts] = make_int4((int)i, (e - (int)i) | (kc << 4) | (kz << 8), (int)b, 0);
+  const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (i0 >= M) return;
+  uint32_t k[8];
+  if (i0 + 8 <= M) {
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(keys + i0));
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(keys + i0) + 1);
+    k[0] = a.x, k[1] = a.y, k[2] = a.z, k[3] = a.w, k[4] = b.x, k[5] = b.y, k[6] = b.z, k[7] = b.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) k[j] = i0 + j < M ? keys[i0 + j] : 0u;
+  }
+  int64_t cur = -1;
+  int bs = 0, be = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int64_t i = i0 + j;
+    if (i >= M) break;
+    const int64_t b = cpb.q(k[j]);
+    if (b != cur) {  // sorted: a thread's 8 points span few boxes
+      cur = b;
+      bs = box_start[b];
+      be = box_start[b + 1];
+    }
+    const int r = (int)i - bs;
+    if (r & (tc::kUnitPts - 1)) continue;
+    const int e = min(be, (int)i + tc::kUnitPts);
+    const uint32_t klast = e - 1 - i0 < 8 ? k[e - 1 - i0] : keys[e - 1];
+    const int k0 = (int)bij.q(k[j] - cpb.q(k[j]) * cpb.d), k1 = (int)bij.q(klast - cpb.q(klast) * cpb.d);
+    const int kc = max(kcmin, (k1 - k0 + W + 3) / 4);  // span + W <= 4 kc  (<= 20 always)
+    const int kz = min(k0, tc::kSZ - 4 * kc);
+    units[uoff[b] + r / tc::kUnitPts] = make_int4((int)i, (e - (int)i) | (kc << 4) | (kz << 8), (int)b, 0);
+  }
 }
 
 __global__ void k_tc_tile_items(const int32_t* __restrict__ uoff, int64_t ntiles, int bpt,
@@ -682,8 +707,11 @@ int launch_tc(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t*
   VFN_CUDA(cub::DeviceScan::ExclusiveSum(p->sort_tmp.ptr, t1, ucount, uoff, (int)(nb + 1), s));
   // units <= M (each holds >= 1 point)
   VFN_CHECK(p->units.ensure(sizeof(int4) * (M + 1)));
-  k_write_units<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(keys_sorted, M, box_start, g.cells_per_box, bij,
-                                                            W, (W + 3) / 4, uoff, p->units.as<int4>());
+  if (g.cells_per_box > 256 || bij > 256) return fail(VFN_ERR_INVALID, "box too large for the unit builder");
+  k_write_units<<<(unsigned)(((M + 7) / 8 + 255) / 256), 256, 0, s>>>(keys_sorted, M, box_start,
+                                                                      make_div((uint32_t)g.cells_per_box),
+                                                                      make_div((uint32_t)bij), W, (W + 3) / 4, uoff,
+                                                                      p->units.as<int4>());
   VFN_CUDA(cudaGetLastError());
   const unsigned tb = (unsigned)((g.ntiles + 1 + 255) / 256);
   k_tc_tile_items<<<tb, 256, 0, s>>>(uoff, g.ntiles, g.boxes_per_tile, nitems);

@@ -110,9 +110,12 @@ __global__ void k_map_key(const double* __restrict__ pts, int64_t M, TorusMap tm
   for (int d = 0; d < 3; ++d) {
     double x = pts[3 * i + d];
     ok = ok && inside(x, tm.a[d], tm.b[d]);
+    // one correctly rounded division per coordinate: the cell comes from u
+    // exactly as nearest_cell derives it (same u, same floor)
+    const double ud = torus_u(x, tm.a[d], tm.amb[d], tm.nd[d]);
     double delta;
-    cell[d] = nearest_cell(x, tm.a[d], tm.amb[d], tm.nd[d], tm.n[d], delta);
-    if (u) u[3 * i + d] = torus_u(x, tm.a[d], tm.amb[d], tm.nd[d]);
+    cell[d] = cell_from_u(ud, tm.nd[d], tm.n[d], delta);
+    if (u) u[3 * i + d] = ud;
   }
   if (!ok) {
     atomicMin(bad, (unsigned long long)i);
