@@ -1,6 +1,9 @@
 // extern "C" entry points of libvfnfft (see include/vfnfft.h).
 #include <algorithm>
 #include <chrono>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -212,6 +215,95 @@ int choose_geometry(vfn_plan* p, int64_t M, const double* pts_dev, cudaStream_t 
   return VFN_OK;
 }
 
+// Window polynomial tables on the device, one per (device, m, beta), kept
+// for the process (a few KB each).
+int window_table(int device, int m, double beta, WindowPoly* out) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, double>, WindowPoly> tables;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_tuple(device, m, beta);
+  auto it = tables.find(key);
+  if (it == tables.end()) {
+    const int max_deg = 26;
+    std::vector<double> coef((size_t)(2 * m + 1) * (max_deg + 1));
+    WindowPoly w;
+    w.m = m;
+    w.deg = fit_window_poly(m, beta, coef.data(), max_deg);
+    const size_t bytes = sizeof(double) * (2 * m + 1) * (w.deg + 1);
+    cudaError_t e = cudaMalloc(&w.dev, bytes);
+    if (e == cudaSuccess) e = cudaMemcpy(w.dev, coef.data(), bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      if (w.dev) cudaFree(w.dev);
+      return fail(VFN_ERR_CUDA, std::string("window table: ") + cudaGetErrorString(e));
+    }
+    it = tables.emplace(key, w).first;
+  }
+  *out = it->second;
+  return VFN_OK;
+}
+
+// Recycled plan shells: the size-independent per-plan resources.
+namespace {
+struct Shell {
+  int device;
+  cudaEvent_t ev[4], bev[4];
+  int64_t* bad_host;
+  int64_t* bad_mapped;
+  DevBuf warp_bad, dfacbuf;
+};
+std::mutex g_shell_mu;
+std::vector<Shell*> g_shells;
+constexpr size_t kShellsKept = 16;
+}  // namespace
+
+bool shell_take(vfn_plan* p) {
+  Shell* sh = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_shell_mu);
+    for (size_t i = 0; i < g_shells.size(); ++i)
+      if (g_shells[i]->device == p->device) {
+        sh = g_shells[i];
+        g_shells.erase(g_shells.begin() + i);
+        break;
+      }
+  }
+  if (!sh) return false;
+  for (int i = 0; i < 4; ++i) {
+    p->ev[i] = sh->ev[i];
+    p->bev[i] = sh->bev[i];
+  }
+  p->bad_host = sh->bad_host;
+  p->bad_mapped = sh->bad_mapped;
+  p->warp_bad = std::move(sh->warp_bad);  // holds the sentinel (restored after every use)
+  p->dfacbuf = std::move(sh->dfacbuf);
+  delete sh;
+  return true;
+}
+
+// Hand a destroyed plan's shell to the recycler; its fields are cleared so
+// the caller's destroy leaves them alone.  Only complete shells are kept.
+void shell_give(vfn_plan* p) {
+  if (!p->bad_host || !p->warp_bad.ptr) return;
+  for (int i = 0; i < 4; ++i)
+    if (!p->ev[i] || !p->bev[i]) return;
+  std::lock_guard<std::mutex> lock(g_shell_mu);
+  if (g_shells.size() >= kShellsKept) return;
+  Shell* sh = new Shell();
+  sh->device = p->device;
+  for (int i = 0; i < 4; ++i) {
+    sh->ev[i] = p->ev[i];
+    sh->bev[i] = p->bev[i];
+    p->ev[i] = p->bev[i] = nullptr;
+  }
+  sh->bad_host = p->bad_host;
+  sh->bad_mapped = p->bad_mapped;
+  p->bad_host = p->bad_mapped = nullptr;
+  sh->warp_bad = std::move(p->warp_bad);
+  sh->dfacbuf = std::move(p->dfacbuf);
+  g_shells.push_back(sh);
+}
+
 }  // namespace vfn
 
 extern "C" {
@@ -261,36 +353,36 @@ int vfn_plan_create(vfn_plan** out, int device, const int64_t nmodes[3], const d
     p->P[d] = (p->n[d] + pt - 1) / pt * pt + 2 * m;
   }
   p->beta = kb_beta(m, sigma);
-  // window polynomial table
+  // window polynomial table: fitted once per (m, beta) and uploaded once per
+  // device (process-wide, shared by plans)
   {
-    const int max_deg = 26;
-    std::vector<double> coef((size_t)(2 * m + 1) * (max_deg + 1));
-    p->poly.m = m;
-    p->poly.deg = fit_window_poly(m, p->beta, coef.data(), max_deg);
-    size_t bytes = sizeof(double) * (2 * m + 1) * (p->poly.deg + 1);
-    cudaError_t e = cudaMalloc(&p->poly.dev, bytes);
-    if (e == cudaSuccess) e = cudaMemcpy(p->poly.dev, coef.data(), bytes, cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
+    const int st = window_table(device, m, p->beta, &p->poly);
+    if (st != VFN_OK) {
+      std::string msg = vfn_last_error();
       vfn_plan_destroy(p);
-      return fail(VFN_ERR_CUDA, std::string("window table: ") + cudaGetErrorString(e));
+      return fail(st, msg);
     }
   }
-  for (int i = 0; i < 4; ++i) cudaEventCreate(&p->ev[i]);
-  for (int i = 0; i < 4; ++i) cudaEventCreate(&p->bev[i]);
-  if (cudaHostAlloc(&p->bad_host, sizeof(int64_t), cudaHostAllocMapped) != cudaSuccess ||
-      cudaHostGetDevicePointer(&p->bad_mapped, p->bad_host, 0) != cudaSuccess) {
-    cudaGetLastError();
-    if (p->bad_host) cudaFreeHost(p->bad_host);
-    p->bad_host = nullptr;  // pageable fallback (p->bad_fallback)
-    p->bad_mapped = nullptr;
-  }
-  // bad-row word of the warp path, kept at the 0x7f.. sentinel between calls
-  if (p->warp_bad.ensure(sizeof(int64_t)) != VFN_OK ||
-      cudaMemset(p->warp_bad.ptr, 0x7f, sizeof(int64_t)) != cudaSuccess) {
-    std::string msg = vfn_last_error();
-    vfn_plan_destroy(p);
-    return fail(VFN_ERR_CUDA, "plan scratch: " + msg);
+  // events, the mapped bad-row word and the small tables come from a
+  // recycled shell of a destroyed plan when one is available (creating them
+  // costs ~1-2 ms of driver calls, more than a small plan's kernels)
+  if (!shell_take(p)) {
+    for (int i = 0; i < 4; ++i) cudaEventCreate(&p->ev[i]);
+    for (int i = 0; i < 4; ++i) cudaEventCreate(&p->bev[i]);
+    if (cudaHostAlloc(&p->bad_host, sizeof(int64_t), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(&p->bad_mapped, p->bad_host, 0) != cudaSuccess) {
+      cudaGetLastError();
+      if (p->bad_host) cudaFreeHost(p->bad_host);
+      p->bad_host = nullptr;  // pageable fallback (p->bad_fallback)
+      p->bad_mapped = nullptr;
+    }
+    // bad-row word of the warp path, kept at the 0x7f.. sentinel between calls
+    if (p->warp_bad.ensure(sizeof(int64_t)) != VFN_OK ||
+        cudaMemset(p->warp_bad.ptr, 0x7f, sizeof(int64_t)) != cudaSuccess) {
+      std::string msg = vfn_last_error();
+      vfn_plan_destroy(p);
+      return fail(VFN_ERR_CUDA, "plan scratch: " + msg);
+    }
   }
   // bin keys are uint32: (tile * boxes_per_tile + box) * cells_per_box + cell
   // must stay below 2^32 for every geometry the plan can use (n1 n2 n3 ~>
@@ -310,15 +402,28 @@ int vfn_plan_create(vfn_plan** out, int device, const int64_t nmodes[3], const d
     }
   // coefficients to the device
   const size_t cbytes = sizeof(double2) * nmodes[0] * nmodes[1] * nmodes[2];
-  DevBuf staging;
-  const void* cdev = nullptr;
-  HostStager* cst = (!coeffs_on_device && cbytes >= ((size_t)1 << 20) && is_pageable(coeffs))
-                        ? device_stager(device) : nullptr;
-  int st = stage_in(staging, coeffs, cbytes, coeffs_on_device, &cdev, s, cst);
+  // host coefficients go through a pooled device buffer (no cudaMalloc /
+  // cudaFree per plan; build_grid synchronises before it is returned)
+  const void* cdev = coeffs;
+  void* staging = nullptr;
+  size_t staging_bytes = 0;
+  int st = VFN_OK;
+  if (!coeffs_on_device) {
+    staging = pool_alloc(device, cbytes, &staging_bytes);
+    if (!staging) st = fail(VFN_ERR_NOMEM, "coefficient staging allocation failed");
+    else if (cbytes >= ((size_t)1 << 20) && is_pageable(coeffs))
+      st = stage_h2d(device_stager(device), staging, coeffs, cbytes, s);
+    else if (cudaMemcpyAsync(staging, coeffs, cbytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
+      st = fail(VFN_ERR_CUDA, "coefficient upload failed");
+    cdev = staging;
+  }
   const auto t_setup = std::chrono::steady_clock::now();
   if (st == VFN_OK) st = build_grid(p, static_cast<const double*>(cdev), s);
   if (st == VFN_OK) st = make_grid_tmap(p);
-  staging.release();
+  if (staging) {
+    if (st != VFN_OK) cudaStreamSynchronize(s);
+    pool_free(device, staging, staging_bytes);
+  }
   p->build_ms[4] = std::chrono::duration<float, std::milli>(t_setup - t_start).count();
   p->build_ms[0] = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_start).count();
   if (st != VFN_OK) {
@@ -334,7 +439,8 @@ int vfn_plan_destroy(vfn_plan* p) {
   if (!p) return VFN_OK;
   DeviceGuard guard(p->device);
   if (p->grid) pool_free(p->device, p->grid, p->grid_bytes);
-  if (p->poly.dev) cudaFree(p->poly.dev);
+  p->poly.dev = nullptr;  // the device's shared window table
+  shell_give(p);          // events, mapped word, small tables back to the recycler (if it has room)
   for (int i = 0; i < 4; ++i)
     if (p->bev[i]) cudaEventDestroy(p->bev[i]);
   DevBuf* bufs[] = {&p->pts, &p->out, &p->keys, &p->keys_sorted, &p->idx, &p->perm,

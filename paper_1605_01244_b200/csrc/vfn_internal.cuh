@@ -238,9 +238,14 @@ int fit_window_poly(int m, double beta, double* coef, int max_deg);
 // Large device buffers (oversampled grids) are recycled per device instead of
 // cudaFree'd: cudaFree synchronises the whole device, and a plan rebuilt for
 // a new field (a time series of snapshots, one plan per rank) reuses the
-// previous grid's memory.  At most kPoolKeep buffers are held per device;
+// previous grid's memory.  At most four buffers are held per device;
 // vfn_pool_release() frees them.
 void* pool_alloc(int device, size_t bytes, size_t* got);
+// the device's window polynomial table for (m, beta), fitted and uploaded once
+int window_table(int device, int m, double beta, WindowPoly* out);
+// recycled size-independent plan resources (events, mapped word, small tables)
+bool shell_take(vfn_plan* p);
+void shell_give(vfn_plan* p);
 void pool_free(int device, void* ptr, size_t bytes);
 
 // ---------------------------------------------------------------- complex GEMM (vfn_zgemm.cu)

@@ -92,7 +92,7 @@ struct PoolEntry {
 };
 std::mutex g_pool_mu;
 std::vector<PoolEntry> g_pool;
-constexpr int kPoolKeep = 2;  // buffers kept per device
+constexpr int kPoolKeep = 4;  // buffers kept per device (a grid, a coefficient staging buffer, ...)
 }  // namespace
 
 void* pool_alloc(int device, size_t bytes, size_t* got) {
