@@ -764,12 +764,12 @@ int eval_device_batches(vfn_plan* p, const double* points, int64_t M, double* ou
   }
   VFN_CHECK(p->misc.ensure(sizeof(int64_t) * (nb + 8)));
   int64_t* bad_dev = p->misc.as<int64_t>();
+  // one geometry for every batch, chosen from the whole call's points
   BinGeom g;
+  VFN_CHECK(choose_geometry(p, M, static_cast<const double*>(pdev), s, &g));
   for (int64_t i = 0; i < nb; ++i) {
     const int64_t lo = i * bsz, n = std::min(bsz, M - lo);
-    VFN_CHECK(eval_enqueue(p, static_cast<const double*>(pdev) + 3 * lo, n, out_dev + lo, bad_dev + i, s,
-                           i ? &g : nullptr));
-    if (i == 0) g = p->last_geom;
+    VFN_CHECK(eval_enqueue(p, static_cast<const double*>(pdev) + 3 * lo, n, out_dev + lo, bad_dev + i, s, &g));
   }
   if (!on_device)
     VFN_CUDA(cudaMemcpyAsync(out, out_dev, sizeof(double2) * M, cudaMemcpyDeviceToHost, s));
@@ -971,8 +971,30 @@ int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* ou
   auto e_comp = [&](int64_t i) { return ev[3 * i + 1]; };
   auto e_out = [&](int64_t i) { return ev[3 * i + 2]; };
   int st = VFN_OK;
+  // one geometry for every chunk, chosen from the WHOLE call's points exactly
+  // as the device-resident call would (its density sample rows are copied
+  // up first), so host and device inputs give bitwise the same values
   BinGeom g;
-  bool have_g = false;
+  {
+    std::vector<double> hs;
+    const double* sdev = nullptr;
+    if (M >= kDensityMinM) {
+      const int S = kDensitySample;
+      hs.resize(3 * (size_t)S);
+      for (int j = 0; j < S; ++j)
+        for (int d = 0; d < 3; ++d) hs[3 * (size_t)j + d] = points[3 * ((int64_t)j * (M / S)) + d];
+      VFN_CHECK(p->sample_pts.ensure(sizeof(double) * hs.size()));
+      VFN_CUDA(cudaMemcpyAsync(p->sample_pts.ptr, hs.data(), sizeof(double) * hs.size(), cudaMemcpyHostToDevice, s));
+      sdev = p->sample_pts.as<double>();
+    }
+    int bxy = 2;
+    VFN_CHECK(choose_bxy(p, M, sdev, true, s, &bxy));
+    VFN_CUDA(cudaStreamSynchronize(s));  // hs is read by the copy above
+    g = make_geometry(p, bxy);
+    p->last_geom = g;
+    p->has_last_geom = true;
+  }
+  bool have_g = true;
   // pageable user buffers: chunk copies go through the device's pinned stager
   // (host threads copy one piece while the DMA engine moves the previous);
   // chunk i-1's output is staged out while chunk i computes

@@ -175,6 +175,7 @@ struct vfn_plan {
   vfn::DevBuf pts, out, uvals, keys, keys_sorted, idx, perm, sort_tmp, box_start, items, units, uscratch, misc;
   vfn::DevBuf warp_bad;  // first-bad-row word of the warp-per-point path (never reallocated)
   vfn::DevBuf sample;    // column-density sample of choose_geometry
+  vfn::DevBuf sample_pts;  // the density-sample rows of a host-buffer call
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t* bad_host = nullptr;  // mapped pinned word for the first-bad-row readback
   int64_t* bad_mapped = nullptr;  // its device-side address

@@ -1066,3 +1066,25 @@ def test_evaluate_runs_on_the_callers_current_stream(vfb, unit_box):
         # the legacy default stream is handle 0 (c_void_p(0).value is None)
         assert (nufft._stream_of(plan.device).value or 0) == torch.cuda.current_stream().cuda_stream
         np.testing.assert_array_equal(host, ref)
+
+
+def test_host_pipelined_call_takes_the_whole_calls_geometry(vfb):
+    """A host-buffer call of >= 2^23 points runs in chunks; its bin geometry
+    (box width) is chosen from the whole call's density sample, as the
+    device-resident call chooses it, not from the first chunk — so the two
+    give bitwise the same values even when the chunks' densities differ
+    (first half uniform: box width 2 on its own; second half a tight cloud:
+    the whole set takes width 1)."""
+    import torch
+
+    box = vfb.DomainBox((-0.5, -0.5, -0.5), (0.5, 0.5, 0.5))
+    spec = random_spectral(box, (128, 128, 128), 1400)
+    plan = vfb.NufftPlan(spec)
+    rng = np.random.default_rng(1401)
+    M = (1 << 23) + 5
+    pts = rng.uniform(-0.5, 0.5, (M, 3))
+    pts[M // 2:] = np.clip(rng.normal(0.1, 0.002, (M - M // 2, 3)), -0.5, 0.4999)
+    dev = plan.evaluate(torch.as_tensor(pts, device="cuda")).cpu().numpy()
+    assert plan.geometry(M)[0][0] == 1  # the whole set is dense enough for 1 x 1 boxes
+    host = plan.evaluate(pts)
+    np.testing.assert_array_equal(host, dev)
