@@ -104,8 +104,10 @@ int vfn_plan_info(const vfn_plan* plan, int64_t n_out[3], double* beta_out);
 int vfn_plan_grid(vfn_plan* plan, double* out_host);
 
 /* The bin-sort of M points (new): key[i] of input row i, and
- * perm = stable argsort(key) (sorted position -> input row).  Host or device
- * buffers per on_device; keys are uint32, perm int32.                    */
+ * perm = stable argsort(key) (sorted position -> input row).  key = (tile *
+ * boxes_per_tile + box) * ceil(box_depth / 2) + (depth in box) / 2, tiles and
+ * boxes row-major (vfn_plan_geometry gives box and tile sizes).  Host or
+ * device buffers per on_device; keys are uint32, perm int32.             */
 int vfn_plan_bin(vfn_plan* plan, const double* points, int64_t M, uint32_t* keys,
                  int32_t* perm, int on_device, int64_t* first_bad_row, void* stream);
 

@@ -218,15 +218,16 @@ def rectilinear(coeffs: np.ndarray, a, b, coords) -> np.ndarray:
 # A point's nearest oversampled cell c_d = l0_d mod n_d (nufft.py:248-257) is
 # grouped into gather boxes of (bi, bj, bk) cells; boxes are numbered
 # row-major inside tiles of (ti, tj, tk) cells, tiles row-major over the grid
-# (the row-major convention of tube.py:50-51), and cells depth-major inside a
-# box.  The permutation is a stable
-# sort on that key (precedent: the stable argsort of tube.py:125).
+# (the row-major convention of tube.py:50-51).  Inside a box the key keeps
+# the cell's depth pair only (c_z mod bk) // 2: key = (tile * boxes_per_tile +
+# box) * ceil(bk / 2) + depth_pair.  The permutation is a stable sort on that
+# key (precedent: the stable argsort of tube.py:125).
 # ---------------------------------------------------------------------------
 
 
 def bin_keys(points, a, b, n, box=(1, 1, 4), tile=(4, 4, 4)) -> np.ndarray:
     """Sort key of every point; see the block comment above.  Inside a box the
-    cells are numbered depth-major, (k, i, j), so a box's points sort by depth."""
+    key is the depth pair, so a box's points sort by depth pair."""
     _, l0 = nearest_cells(points, a, b, n)
     cell = l0 % np.asarray(n)
     box = np.asarray(box)
@@ -239,8 +240,8 @@ def bin_keys(points, a, b, n, box=(1, 1, 4), tile=(4, 4, 4)) -> np.ndarray:
     nbox = tile // box
     tile_id = (t[:, 0] * ntile[1] + t[:, 1]) * ntile[2] + t[:, 2]
     box_id = (inner[:, 0] * nbox[1] + inner[:, 1]) * nbox[2] + inner[:, 2]
-    cell_id = (c[:, 2] * box[0] + c[:, 0]) * box[1] + c[:, 1]
-    key = (tile_id * int(np.prod(nbox)) + box_id) * int(np.prod(box)) + cell_id
+    slots = (int(box[2]) + 1) // 2
+    key = (tile_id * int(np.prod(nbox)) + box_id) * slots + c[:, 2] // 2
     return key.astype(np.int64)
 
 

@@ -123,6 +123,7 @@ BinGeom make_geometry(const vfn_plan* p, int bxy) {
   }
   g.boxes_per_tile = g.nbox[0] * g.nbox[1] * g.nbox[2];
   g.cells_per_box = g.box[0] * g.box[1] * g.box[2];
+  g.key_slots = (g.box[2] + 1) / 2;
   for (int d = 0; d < 3; ++d) {
     g.tile_inv[d] = (((uint64_t)1 << 32) + (uint64_t)g.tile[d] - 1) / (uint64_t)g.tile[d];
     g.box_inv[d] = (((uint64_t)1 << 32) + (uint64_t)g.box[d] - 1) / (uint64_t)g.box[d];
@@ -384,7 +385,7 @@ int vfn_plan_create(vfn_plan** out, int device, const int64_t nmodes[3], const d
       return fail(VFN_ERR_CUDA, "plan scratch: " + msg);
     }
   }
-  // bin keys are uint32: (tile * boxes_per_tile + box) * cells_per_box + cell
+  // bin keys are uint32: (tile * boxes_per_tile + box) * key_slots + depth / 2
   // must stay below 2^32 for every geometry the plan can use (n1 n2 n3 ~>
   // 4.2e9 cells); checked before the grid is allocated
   for (int tm = 0; tm < 2; ++tm)
@@ -392,7 +393,7 @@ int vfn_plan_create(vfn_plan** out, int device, const int64_t nmodes[3], const d
       p->has_tmap = tm == 1;
       const BinGeom g = make_geometry(p, bxy);
       p->has_tmap = false;
-      if ((double)g.nboxes * (double)g.cells_per_box > 4294967296.0) {
+      if ((double)g.nboxes * (double)g.key_slots > 4294967296.0) {
         const std::string msg = "oversampled grid too large: its bin keys exceed 32 bits (" +
                                 std::to_string(p->n[0]) + " x " + std::to_string(p->n[1]) + " x " +
                                 std::to_string(p->n[2]) + " cells)";
@@ -619,7 +620,7 @@ static int bin_points(vfn_plan* p, const double* points, int64_t M, int on_devic
   VFN_CHECK(map_and_key(p, *pts_dev, M, g, p->keys.as<uint32_t>(), write_iota ? iota : nullptr, u,
                         *bad_dev, s));
   VFN_CHECK(sort_pairs(p, p->keys.as<uint32_t>(), p->keys_sorted.as<uint32_t>(),
-                       p->idx.as<int32_t>(), p->perm.as<int32_t>(), M, key_bits_for(g.nboxes * g.cells_per_box), s));
+                       p->idx.as<int32_t>(), p->perm.as<int32_t>(), M, key_bits_for(g.nboxes * g.key_slots), s));
   return VFN_OK;
 }
 
@@ -694,7 +695,7 @@ int eval_enqueue(vfn_plan* p, const double* pts_dev, int64_t M, double2* out_dev
   VFN_CHECK(map_and_key(p, pts_dev, M, g, p->keys.as<uint32_t>(), write_iota ? iota : nullptr, u,
                         bad_dev, s));
   VFN_CHECK(sort_pairs(p, p->keys.as<uint32_t>(), p->keys_sorted.as<uint32_t>(), p->idx.as<int32_t>(),
-                       p->perm.as<int32_t>(), M, key_bits_for(g.nboxes * g.cells_per_box), s));
+                       p->perm.as<int32_t>(), M, key_bits_for(g.nboxes * g.key_slots), s));
   mark_event(p, 1, s);
   bool used = false;
   if (p->gather_variant != 1)

@@ -239,12 +239,12 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_gather_dmma(GatherArgs A) {
 // Per-box point counts from the SORTED keys: equal boxes are runs, so each
 // warp adds one atomic per run it sees (clustered inputs put millions of
 // points in a handful of boxes; per-point atomics would serialise on them).
-__global__ void k_box_counts(const uint32_t* __restrict__ keys, int64_t M, int cells_per_box,
+__global__ void k_box_counts(const uint32_t* __restrict__ keys, int64_t M, int key_slots,
                              int32_t* __restrict__ counts) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const bool live = i < M;
-  const uint32_t box = live ? keys[i] / (uint32_t)cells_per_box : 0xffffffffu;
+  const uint32_t box = live ? keys[i] / (uint32_t)key_slots : 0xffffffffu;
   const uint32_t prev = __shfl_up_sync(0xffffffffu, box, 1);
   const bool head = live && (lane == 0 || prev != box);
   const unsigned heads = __ballot_sync(0xffffffffu, head);
@@ -333,7 +333,7 @@ int gather_boxes(vfn_plan* p, const double* pts, int64_t M, const BinGeom& g,
   int32_t* nitems = bstart + (nb + 1);
   int32_t* ioff = nitems + (g.ntiles + 1);
   VFN_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (nb + 1), s));
-  k_box_counts<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(keys_sorted, M, g.cells_per_box, counts);
+  k_box_counts<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(keys_sorted, M, g.key_slots, counts);
   VFN_CUDA(cudaGetLastError());
   size_t tmp = 0;
   VFN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, counts, bstart, (int)(nb + 1), s));

@@ -531,9 +531,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 
 // ------------------------------------------------------------------ units
 
-// A box's points are sorted by depth and the box is TZ cells deep, so any 8
-// consecutive points span <= TZ - 1 depths: units are the box's chunks of 8,
-// each with the fewest k-chunks (K = 4 KC depths) covering its stencils.
+// A box's points are sorted by depth pair and the box is TZ cells deep, so
+// any 8 consecutive points span <= TZ - 1 depths: units are the box's chunks
+// of 8, each with the fewest k-chunks (K = 4 KC depths) covering the
+// stencils of its depth-pair range.
 __global__ void k_unit_counts(const int32_t* __restrict__ box_start, int64_t nboxes,
                               int32_t* __restrict__ ucount) {
   int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -554,7 +555,7 @@ static Div make_div(uint32_t d) { return Div{((uint64_t(1) << 40) + d - 1) / d, 
 // point that opens a chunk of 8 in its box writes the unit (fully parallel,
 // also for boxes holding millions of points — config 3).
 __global__ void k_write_units(const uint32_t* __restrict__ keys, int64_t M,
-                              const int32_t* __restrict__ box_start, Div cpb, Div bij, int W,
+                              const int32_t* __restrict__ box_start, Div cpb, int W,
                               int kcmin, const int32_t* __restrict__ uoff, int4* __restrict__ units) {
   const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (i0 >= M) return;
@@ -583,7 +584,8 @@ __global__ void k_write_units(const uint32_t* __restrict__ keys, int64_t M,
     if (r & (tc::kUnitPts - 1)) continue;
     const int e = min(be, (int)i + tc::kUnitPts);
     const uint32_t klast = e - 1 - i0 < 8 ? k[e - 1 - i0] : keys[e - 1];
-    const int k0 = (int)bij.q(k[j] - cpb.q(k[j]) * cpb.d), k1 = (int)bij.q(klast - cpb.q(klast) * cpb.d);
+    // the key holds depth pairs: the unit's depths lie in [2 q0, 2 q1 + 1]
+    const int k0 = 2 * (int)(k[j] - cpb.q(k[j]) * cpb.d), k1 = 2 * (int)(klast - cpb.q(klast) * cpb.d) + 1;
     const int kc = max(kcmin, (k1 - k0 + W + 3) / 4);  // span + W <= 4 kc  (<= 20 always)
     const int kz = min(k0, tc::kSZ - 4 * kc);
     units[uoff[b] + r / tc::kUnitPts] = make_int4((int)i, (e - (int)i) | (kc << 4) | (kz << 8), (int)b, 0);
@@ -689,7 +691,6 @@ int launch_tc(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t*
               const int32_t* box_start, double2* out, const BinGeom& g, int64_t M,
               cudaStream_t s) {
   const int64_t nb = g.nboxes;
-  const int bij = g.box[0] * g.box[1];
   const int W = 2 * p->m + 1;
   // scratch: ucount/uoff (nb + 1 each), nitems/ioff (ntiles + 1 each)
   VFN_CHECK(p->uscratch.ensure(sizeof(int32_t) * (2 * (nb + 1) + 2 * (g.ntiles + 1))));
@@ -707,11 +708,10 @@ int launch_tc(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t*
   VFN_CUDA(cub::DeviceScan::ExclusiveSum(p->sort_tmp.ptr, t1, ucount, uoff, (int)(nb + 1), s));
   // units <= M (each holds >= 1 point)
   VFN_CHECK(p->units.ensure(sizeof(int4) * (M + 1)));
-  if (g.cells_per_box > 256 || bij > 256) return fail(VFN_ERR_INVALID, "box too large for the unit builder");
+  if (g.key_slots > 256) return fail(VFN_ERR_INVALID, "box too deep for the unit builder");
   k_write_units<<<(unsigned)(((M + 7) / 8 + 255) / 256), 256, 0, s>>>(keys_sorted, M, box_start,
-                                                                      make_div((uint32_t)g.cells_per_box),
-                                                                      make_div((uint32_t)bij), W, (W + 3) / 4, uoff,
-                                                                      p->units.as<int4>());
+                                                                      make_div((uint32_t)g.key_slots), W, (W + 3) / 4,
+                                                                      uoff, p->units.as<int4>());
   VFN_CUDA(cudaGetLastError());
   const unsigned tb = (unsigned)((g.ntiles + 1 + 255) / 256);
   k_tc_tile_items<<<tb, 256, 0, s>>>(uoff, g.ntiles, g.boxes_per_tile, nitems);

@@ -473,7 +473,7 @@ class NufftPlan:
         for d in range(3):
             ntiles *= -(-self._n[d] // tile[d])
         nkeys = ntiles * (tile[0] // box[0]) * (tile[1] // box[1]) * (tile[2] // box[2])
-        nkeys *= box[0] * box[1] * box[2]
+        nkeys *= (box[2] + 1) // 2  # key slots per box: depth pairs (include/vfnfft.h vfn_plan_bin)
         bits = max(1, int(nkeys - 1).bit_length())
         sort = 2 + 2 * -(-bits // 8)
         if 2 <= self.params.cutoff <= 7 and tile[2] == 20 - 2 * self.params.cutoff:
