@@ -230,7 +230,7 @@ class _Timer:
 
 
 def evaluate_sharded(plan, points, group=None, mode: str = "keyrange", out=None, stats: ShardStats | None = None,
-                     samples_per_rank: int = 4096, comm=None):
+                     samples_per_rank: int = 1 << 18, comm=None):
     """Values of this rank's block of one point set, in input order (see the
     module docstring).  ``points``: this rank's (m, 3) block (a CUDA tensor
     on the plan's device); the blocks of ranks 0..P-1 concatenated in rank

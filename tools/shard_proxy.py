@@ -66,7 +66,7 @@ def main():
     variant, box = plan.decide(M, sample)
     plan.pin(variant, box)
     # key ranges: splitters from the same per-rank samples evaluate_sharded draws
-    kstride = max(1, M // (4096 * P))
+    kstride = max(1, M // ((1 << 18) * P))
     keys = torch.cat([plan.part_keys(pts[slice(*shard_range(M, P, r))], kstride, shard_range(M, P, r)[0])
                       for r in range(P)])
     split = splitters_from_samples(keys, P)
