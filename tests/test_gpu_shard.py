@@ -151,3 +151,43 @@ def test_sharded_outside_point_fails_every_rank(vfb, unit_box):
         return True
 
     assert all(run_ranks(3, rank))
+
+
+@pytest.mark.parametrize("draw", range(8))
+def test_sharded_fuzz(vfb, draw):
+    """Random rank counts, sizes (warp path, binned without and with the
+    density sample), boxes, grids and point distributions (uniform, clouds
+    straddling the periodic seam, mixtures, a single repeated point): the
+    key-range sharded evaluate equals the unsharded call bitwise."""
+    import torch
+
+    from paper_1605_01244_b200.parallel import evaluate_sharded, shard_range
+
+    rng = np.random.default_rng(1500 + draw)
+    a = rng.uniform(-3, 3, 3)
+    w = rng.uniform(0.5, 4, 3)
+    box = vfb.DomainBox(tuple(a), tuple(a + w))
+    shape = tuple(int(2 * rng.integers(4, 33)) for _ in range(3))
+    spec = random_spectral(box, shape, 1510 + draw)
+    M = int(rng.choice([20000, 300000, 1 << 20, 2500000]))
+    kind = draw % 4
+    if kind == 0:
+        u = rng.uniform(0, 1, (M, 3))
+    elif kind == 1:  # a cloud over the seam at 0 / 1
+        u = np.mod(rng.normal(0.0, 0.01, (M, 3)), 1.0)
+    elif kind == 2:  # mixture
+        u = np.concatenate([rng.uniform(0, 1, (M // 2, 3)),
+                            np.mod(rng.normal(rng.uniform(0, 1, 3), 0.003, (M - M // 2, 3)), 1.0)])
+        u = u[rng.permutation(M)]
+    else:  # one point repeated, plus a few others
+        u = np.repeat(rng.uniform(0, 1, (1, 3)), M, axis=0)
+        u[:: 97] = rng.uniform(0, 1, (len(u[:: 97]), 3))
+    pts = np.asarray(box.a) + np.minimum(u, np.nextafter(1.0, 0.0)) * (np.asarray(box.b) - np.asarray(box.a))
+    pts = np.minimum(pts, np.nextafter(np.asarray(box.b), -np.inf))
+    dpts = torch.as_tensor(pts, device="cuda")
+    ref = vfb.NufftPlan(spec).evaluate(dpts).cpu().numpy()
+    P = int(rng.choice([2, 3, 5, 8]))
+    plans = [vfb.NufftPlan(spec) for _ in range(P)]
+    res = run_ranks(P, lambda r, comm: evaluate_sharded(
+        plans[r], dpts[slice(*shard_range(M, P, r))], comm=comm).cpu().numpy())
+    np.testing.assert_array_equal(np.concatenate(res), ref, err_msg=f"draw {draw}: P={P} M={M} kind={kind}")
