@@ -16,7 +16,7 @@ OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libvfnfft.so")
 LIB_CHECKS = os.path.join(HERE, "libvfnfft_checks.so")
 SOURCES = ["vfn_host.cpp", "vfn_stage.cpp", "vfn_kernels.cu", "vfn_gather.cu", "vfn_gather_tc.cu", "vfn_rect.cu",
-           "vfn_direct.cu", "vfn_util.cu", "vfn_tube.cu", "vfn_io.cpp", "vfn_io_kernels.cu", "vfn_shard.cu", "vfn_zgemm.cu", "vfn_rect_nufft.cu", "vfn_api.cu"]
+           "vfn_direct.cu", "vfn_util.cu", "vfn_tube.cu", "vfn_io.cpp", "vfn_io_kernels.cu", "vfn_shard.cu", "vfn_zgemm.cu", "vfn_rect_nufft.cu", "vfn_sort.cu", "vfn_api.cu"]
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

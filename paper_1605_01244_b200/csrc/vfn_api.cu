@@ -618,7 +618,7 @@ static int bin_points(vfn_plan* p, const double* points, int64_t M, int on_devic
     VFN_CHECK(p->uvals.ensure(sizeof(double) * 3 * M));
     u = p->uvals.as<double>();
   }
-  VFN_CHECK(map_and_key(p, *pts_dev, M, g, p->keys.as<uint32_t>(), write_iota ? iota : nullptr, u,
+  VFN_CHECK(map_and_key(p, *pts_dev, M, g, p->keys.as<uint32_t>(), write_iota && use_cub_sort() ? iota : nullptr, u,
                         *bad_dev, s));
   VFN_CHECK(sort_pairs(p, p->keys.as<uint32_t>(), p->keys_sorted.as<uint32_t>(),
                        p->idx.as<int32_t>(), p->perm.as<int32_t>(), M, key_bits_for(g.nboxes * g.key_slots), s));
@@ -693,7 +693,7 @@ int eval_enqueue(vfn_plan* p, const double* pts_dev, int64_t M, double2* out_dev
     VFN_CHECK(p->uvals.ensure(sizeof(double) * 3 * M));
     u = p->uvals.as<double>();
   }
-  VFN_CHECK(map_and_key(p, pts_dev, M, g, p->keys.as<uint32_t>(), write_iota ? iota : nullptr, u,
+  VFN_CHECK(map_and_key(p, pts_dev, M, g, p->keys.as<uint32_t>(), write_iota && use_cub_sort() ? iota : nullptr, u,
                         bad_dev, s));
   VFN_CHECK(sort_pairs(p, p->keys.as<uint32_t>(), p->keys_sorted.as<uint32_t>(), p->idx.as<int32_t>(),
                        p->perm.as<int32_t>(), M, key_bits_for(g.nboxes * g.key_slots), s));

@@ -285,6 +285,10 @@ int map_and_key(vfn_plan* p, const double* pts_dev, int64_t M, const BinGeom& g,
                 int32_t* iota, double* u, int64_t* bad_dev, cudaStream_t s);
 int sort_pairs(vfn_plan* p, const uint32_t* keys_in, uint32_t* keys_out, const int32_t* vals_in,
                int32_t* vals_out, int64_t M, int key_bits, cudaStream_t s);
+// hand-written stable LSD radix sort, values = input row (vfn_sort.cu)
+int radix_sort_pairs(DevBuf& tmp, const uint32_t* keys_in, uint32_t* keys_out, int32_t* vals_out, int64_t M,
+                     int key_bits, cudaStream_t s);
+bool use_cub_sort();  // VFN_SORT=cub: CUB onesweep instead (A/B runs)
 int launch_torus(const TorusMap& tm, const double* pts, int64_t M, double* zeta, cudaStream_t s);
 int gather_simple(vfn_plan* p, const double* pts_dev, int64_t M, const int32_t* perm,
                   double2* out_dev, cudaStream_t s);

@@ -6,6 +6,7 @@
 #include <mutex>
 #include <cmath>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -170,8 +171,20 @@ int launch_torus(const TorusMap& tm, const double* pts, int64_t M, double* zeta,
   return VFN_OK;
 }
 
+bool use_cub_sort() {
+  static const bool cub = [] {
+    const char* e = std::getenv("VFN_SORT");
+    return e && std::string(e) == "cub";
+  }();
+  return cub;
+}
+
+// Stable sort of (key, value) pairs: the hand-written LSD radix sort
+// (vfn_sort.cu; values = the row index, implicit) or, with VFN_SORT=cub for
+// A/B runs, CUB's onesweep with the iota values written by k_map_key.
 int sort_pairs(vfn_plan* p, const uint32_t* keys_in, uint32_t* keys_out, const int32_t* vals_in,
                int32_t* vals_out, int64_t M, int key_bits, cudaStream_t s) {
+  if (!use_cub_sort()) return radix_sort_pairs(p->sort_tmp, keys_in, keys_out, vals_out, M, key_bits, s);
   size_t tmp = 0;
   VFN_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys_in, keys_out, vals_in, vals_out,
                                            (int)M, 0, key_bits, s));
