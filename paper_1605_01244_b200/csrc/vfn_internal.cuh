@@ -288,7 +288,7 @@ int sort_pairs(vfn_plan* p, const uint32_t* keys_in, uint32_t* keys_out, const i
 // hand-written stable LSD radix sort, values = input row (vfn_sort.cu)
 int radix_sort_pairs(DevBuf& tmp, const uint32_t* keys_in, uint32_t* keys_out, int32_t* vals_out, int64_t M,
                      int key_bits, cudaStream_t s);
-bool use_cub_sort();  // VFN_SORT=cub: CUB onesweep instead (A/B runs)
+bool use_cub_sort();  // default; VFN_SORT=radix selects radix_sort_pairs (A/B runs)
 int launch_torus(const TorusMap& tm, const double* pts, int64_t M, double* zeta, cudaStream_t s);
 int gather_simple(vfn_plan* p, const double* pts_dev, int64_t M, const int32_t* perm,
                   double2* out_dev, cudaStream_t s);

@@ -58,58 +58,89 @@ __global__ void __launch_bounds__(kThreads) k_rs_upsweep(const uint32_t* __restr
   }
 }
 
-// Exclusive scan of n ints in place by one CTA of 1024 threads.
+// Exclusive scan of n ints in place by one CTA of 1024 threads: chunks of
+// 4096 (four consecutive ints per thread, coalesced), warp-shuffle scans and
+// a carried chunk total.
 __global__ void __launch_bounds__(1024) k_rs_scan(int32_t* __restrict__ a, int n) {
-  __shared__ int part[1024];
-  const int t = threadIdx.x;
-  const int per = (n + 1023) / 1024, lo = t * per, hi = min(n, lo + per);
-  int s = 0;
-  for (int i = lo; i < hi; ++i) s += a[i];
-  part[t] = s;
+  __shared__ int wsum[32];
+  __shared__ int carry_s;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (t == 0) carry_s = 0;
   __syncthreads();
-  for (int off = 1; off < 1024; off <<= 1) {  // Hillis-Steele inclusive scan of the parts
-    const int v = t >= off ? part[t - off] : 0;
+  for (int c0 = 0; c0 < n; c0 += 4096) {
+    const int i0 = c0 + 4 * t;
+    int v[4], s = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = i0 + k < n ? a[i0 + k] : 0;
+      s += v[k];
+    }
+    int incl = s;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
     __syncthreads();
-    part[t] += v;
+    if (warp == 0) {
+      const int w = wsum[lane];
+      int wi = w;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, wi, off);
+        if (lane >= off) wi += y;
+      }
+      wsum[lane] = wi - w;  // exclusive warp offsets
+    }
     __syncthreads();
-  }
-  int run = t ? part[t - 1] : 0;
-  for (int i = lo; i < hi; ++i) {
-    const int v = a[i];
-    a[i] = run;
-    run += v;
+    int e = carry_s + wsum[warp] + incl - s;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (i0 + k < n) a[i0 + k] = e;
+      e += v[k];
+    }
+    __syncthreads();
+    if (t == 1023) carry_s = e;  // the chunk's last running value
+    __syncthreads();
   }
 }
 
 template <bool IOTA>
-__global__ void __launch_bounds__(kThreads) k_rs_downsweep(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
-                                                           uint32_t* __restrict__ kout, int32_t* __restrict__ vout,
-                                                           int64_t M, int64_t seg, int shift, int nseg,
-                                                           const int32_t* __restrict__ offs) {
+__global__ void __launch_bounds__(kThreads, 4) k_rs_downsweep(const uint32_t* __restrict__ kin,
+                                                              const int32_t* __restrict__ vin,
+                                                              uint32_t* __restrict__ kout, int32_t* __restrict__ vout,
+                                                              int64_t M, int64_t seg, int shift, int nseg,
+                                                              const int32_t* __restrict__ offs) {
   __shared__ int wc[kWarps][kRadix];      // per-warp digit counts of the tile, then the warps' prefixes
   __shared__ int dstart[kRadix + 1];      // digit starts inside the tile
   __shared__ int run[kRadix];             // next output position of each digit (this segment)
-  __shared__ uint32_t sk[kTile];
+  __shared__ uint32_t sk[kTile];          // the tile's keys, loaded once; reordered by digit in place of sv below
   __shared__ int32_t sv[kTile];
+  // each key's rank among the warp's keys of its digit; aliases sv, which is
+  // written only after every thread has read its ranks back
+  uint16_t* rk = reinterpret_cast<uint16_t*>(sv);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int d = tid; d < kRadix; d += kThreads) run[d] = offs[(int64_t)d * nseg + blockIdx.x];
   const int64_t lo = (int64_t)blockIdx.x * seg, hi = min(M, lo + seg);
+  const int wbase = warp * kWarpKeys;
   for (int64_t base = lo; base < hi; base += kTile) {
     const int n = (int)(hi - base < kTile ? hi - base : kTile);
     for (int i = tid; i < kWarps * kRadix; i += kThreads) (&wc[0][0])[i] = 0;
     __syncthreads();
-    // this warp's 512 keys, item-major: key wbase + j * 32 + lane
-    const int wbase = warp * kWarpKeys;
-    uint32_t k[kItems];
-    int32_t v[kItems];
-    int r[kItems];
+    // rank: this warp's 512 keys item-major (key wbase + j * 32 + lane), so
+    // the lanes of item j are in input order
+    uint32_t kr[kItems];
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      const int q = wbase + j * 32 + lane;
+      kr[j] = q < n ? __ldcs(kin + base + q) : 0xffffffffu;
+    }
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
       const int q = wbase + j * 32 + lane;
       const bool live = q < n;
-      k[j] = live ? __ldcs(kin + base + q) : 0xffffffffu;
-      v[j] = IOTA ? (int32_t)(base + q) : (live ? __ldcs(vin + base + q) : 0);
-      const int d = live ? (int)((k[j] >> shift) & 0xff) : kRadix;  // kRadix: past the end
+      const int d = live ? (int)((kr[j] >> shift) & 0xff) : kRadix;  // kRadix: past the end
       const unsigned peers = __match_any_sync(0xffffffffu, d);
       const int leader = __ffs(peers) - 1;
       int before = 0;
@@ -118,7 +149,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_downsweep(const uint32_t* __res
         wc[warp][d] = before + __popc(peers);
       }
       before = __shfl_sync(0xffffffffu, before, leader);
-      r[j] = before + __popc(peers & ((1u << lane) - 1u));
+      rk[q] = (uint16_t)(before + __popc(peers & ((1u << lane) - 1u)));
     }
     __syncthreads();
     // digit totals of the tile and each warp's prefix inside its digit
@@ -155,15 +186,22 @@ __global__ void __launch_bounds__(kThreads) k_rs_downsweep(const uint32_t* __res
       if (lane == 31) dstart[kRadix] = e;
     }
     __syncthreads();
-    // reorder the tile by digit in shared memory
+    // reorder the tile by digit in shared memory (tile positions first: rk
+    // and sv share storage)
+    int pos[kItems];
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
       const int q = wbase + j * 32 + lane;
-      if (q < n) {
-        const int d = (int)((k[j] >> shift) & 0xff);
-        const int p = dstart[d] + wc[warp][d] + r[j];
-        sk[p] = k[j];
-        sv[p] = v[j];
+      const int d = (int)((kr[j] >> shift) & 0xff);
+      pos[j] = q < n ? dstart[d] + wc[warp][d] + rk[q] : -1;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      const int q = wbase + j * 32 + lane;
+      if (pos[j] >= 0) {
+        sk[pos[j]] = kr[j];
+        sv[pos[j]] = IOTA ? (int32_t)(base + q) : __ldcs(vin + base + q);
       }
     }
     __syncthreads();
@@ -193,9 +231,9 @@ int radix_sort_pairs(DevBuf& tmp, const uint32_t* keys_in, uint32_t* keys_out, i
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  // segments: whole tiles, ~8 per SM
+  // segments: whole tiles, 4 per SM (the downsweep's residency)
   const int64_t tiles = (M + rs::kTile - 1) / rs::kTile;
-  const int64_t per = std::max<int64_t>(1, (tiles + nsm * 8 - 1) / (nsm * 8));
+  const int64_t per = std::max<int64_t>(1, (tiles + nsm * 4 - 1) / (nsm * 4));
   const int64_t seg = per * rs::kTile;
   const int nseg = (int)((M + seg - 1) / seg);
   const int ncnt = rs::kRadix * nseg;
