@@ -1088,3 +1088,45 @@ def test_host_pipelined_call_takes_the_whole_calls_geometry(vfb):
     assert plan.geometry(M)[0][0] == 1  # the whole set is dense enough for 1 x 1 boxes
     host = plan.evaluate(pts)
     np.testing.assert_array_equal(host, dev)
+
+
+def test_hand_written_radix_sort_matches_stable_argsort(tmp_path):
+    """The hand-written LSD radix sort (VFN_SORT=radix, csrc/vfn_sort.cu)
+    gives the stable permutation of the bin keys and the same evaluate bits
+    as the default sort (run in a subprocess: the choice is made once per
+    process)."""
+    import subprocess
+    import sys
+
+    from conftest import REPO
+
+    code = r'''
+import numpy as np, sys
+sys.path.insert(0, %r)
+import paper_1605_01244_b200 as vfb
+from oracle import nfft_oracle as O
+rng = np.random.default_rng(1600)
+box = vfb.DomainBox((-1.5, 0.25, 2.0), (2.5, 1.25, 7.0))
+coeffs = rng.standard_normal((32, 24, 16)) + 1j * rng.standard_normal((32, 24, 16))
+plan = vfb.NufftPlan(vfb.SpectralField(box, coeffs))
+for M in (70000, 1 << 20, (1 << 21) + 37):
+    pts = rng.uniform(box.a, box.b, (M, 3))
+    pts[: M // 3] = pts[0]
+    keys, perm = plan.bin(pts)
+    b, t = plan.geometry(M)
+    ref = O.bin_keys(pts, box.a, box.b, plan._n, b, t)
+    assert np.array_equal(keys.astype(np.int64), ref)
+    assert np.array_equal(perm, np.argsort(ref, kind="stable"))
+    np.save(%r + "/vals_%%d.npy" %% M, plan.evaluate(pts))
+print("ok")
+''' % (REPO, str(tmp_path))
+    import os
+
+    for env in ({"VFN_SORT": "radix"}, {}):
+        res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                             env=dict(os.environ, **env), cwd=REPO)
+        assert res.returncode == 0 and "ok" in res.stdout, res.stderr[-2000:]
+        if env:
+            radix = {M: np.load(tmp_path / f"vals_{M}.npy") for M in (70000, 1 << 20, (1 << 21) + 37)}
+    for M, v in radix.items():
+        np.testing.assert_array_equal(v, np.load(tmp_path / f"vals_{M}.npy"))
