@@ -282,6 +282,27 @@ int vfn_plan_partition(vfn_plan* plan, const double* points, int64_t M, int64_t 
 int vfn_gather_values(int device, const double* values, const int32_t* pos, int64_t M, double* out,
                       void* stream);
 
+/* Evaluate M received points (device) and store each value in the buffer
+ * of the rank that owns the point, instead of a local output: point i
+ * belongs to owner o with seg_off[o] <= i < seg_off[o + 1] (host array of
+ * npeers + 1 offsets, npeers <= 64) and its value goes to
+ * outs[o][rows[i]] (outs: host array of device pointers, IPC-mapped peer
+ * buffers over NVLink; rows: device int32).  The tensor-core gather stores
+ * straight from its epilogue (the return exchange fused into the gather);
+ * other gathers are followed by a scatter kernel.  Same values as
+ * vfn_plan_eval with the same settings.                                   */
+int vfn_plan_eval_to_peers(vfn_plan* plan, const double* points, int64_t M, const int32_t* rows, int npeers,
+                           const int64_t* seg_off, double* const* outs, int64_t* first_bad_row, void* stream);
+
+/* IPC-shared device buffers for the owners' outputs: allocate + export a
+ * 64-byte handle, open a peer's handle (another process; cudaIpc*), close,
+ * free; and a synchronised device-to-device copy.                       */
+int vfn_ipc_alloc(int device, int64_t bytes, void** ptr, unsigned char handle[64]);
+int vfn_ipc_open(int device, const unsigned char handle[64], void** ptr);
+int vfn_ipc_close(int device, void* ptr);
+int vfn_ipc_free(int device, void* ptr);
+int vfn_copy_device(int device, void* dst, const void* src, int64_t bytes, void* stream);
+
 /* The gather decisions an evaluate of M points makes (gather variant 3 =
  * warp per point or 4 = binned; box width 1 or 2), so that every rank of a
  * sharded evaluate can pin the ones the unsharded call would take: values

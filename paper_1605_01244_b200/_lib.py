@@ -149,6 +149,16 @@ SIGNATURES = {
         ctypes.c_int,
         [_vp, ctypes.c_int64, _vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), _vp],
     ),
+    "vfn_plan_eval_to_peers": (
+        ctypes.c_int,
+        [_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_vp),
+         ctypes.POINTER(ctypes.c_int64), _vp],
+    ),
+    "vfn_ipc_alloc": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.POINTER(_vp), ctypes.c_ubyte * 64]),
+    "vfn_ipc_open": (ctypes.c_int, [ctypes.c_int, ctypes.c_ubyte * 64, ctypes.POINTER(_vp)]),
+    "vfn_ipc_close": (ctypes.c_int, [ctypes.c_int, _vp]),
+    "vfn_ipc_free": (ctypes.c_int, [ctypes.c_int, _vp]),
+    "vfn_copy_device": (ctypes.c_int, [ctypes.c_int, _vp, _vp, ctypes.c_int64, _vp]),
     "vfn_plan_build_timing": (ctypes.c_int, [_vp, ctypes.c_float * 5]),
     "vfn_pool_release": (ctypes.c_int, [ctypes.c_int]),
     "vfn_plan_last_timing": (

@@ -1058,15 +1058,9 @@ int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* ou
   return VFN_OK;
 }
 
-}  // namespace
-
-extern "C" {
-
-int vfn_plan_eval(vfn_plan* p, const double* points, int64_t M, double* out, int on_device,
-                  int64_t* first_bad_row, void* stream) {
-  vfn::NvtxRange nvtx_range("vfn evaluate");
-  if (!p || (M > 0 && (!points || !out))) return fail(VFN_ERR_INVALID, "null argument");
-  std::lock_guard<std::mutex> plan_lock(p->mu);
+// vfn_plan_eval with the plan lock held (also the body of vfn_plan_eval_to_peers)
+int plan_eval_locked(vfn_plan* p, const double* points, int64_t M, double* out, int on_device,
+                     int64_t* first_bad_row, void* stream) {
   if (M < 0) return fail(VFN_ERR_INVALID, "point count out of range");
   if (first_bad_row) *first_bad_row = -1;
   if (M == 0) return VFN_OK;
@@ -1101,9 +1095,12 @@ int vfn_plan_eval(vfn_plan* p, const double* points, int64_t M, double* out, int
     mark_event(p, 2, s);
   } else {
     bool graphed = false;
-    VFN_CHECK(eval_graphed(p, static_cast<const double*>(pdev), M, out_dev, bad_dev, s, &graphed));
+    if (!p->peer_dev)  // graphs bake in their output pointers
+      VFN_CHECK(eval_graphed(p, static_cast<const double*>(pdev), M, out_dev, bad_dev, s, &graphed));
     if (!graphed) VFN_CHECK(eval_enqueue(p, static_cast<const double*>(pdev), M, out_dev, bad_dev, s, nullptr));
   }
+  if (p->peer_dev && !p->peer_used)  // gathers without the fused epilogue: values out to their owners now
+    VFN_CHECK(scatter_to_peers(out_dev, M, p->peer_dev, s));
   if (st_out)
     VFN_CHECK(stage_d2h(st_out, out, out_dev, sizeof(double2) * M, s));
   else if (!on_device)
@@ -1124,6 +1121,52 @@ int vfn_plan_eval(vfn_plan* p, const double* points, int64_t M, double* out, int
   p->timing_pending = true;  // elapsed times are read lazily (vfn_plan_last_timing)
   if (bad != kBadSentinel) return outside(bad, first_bad_row);
   return VFN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vfn_plan_eval(vfn_plan* p, const double* points, int64_t M, double* out, int on_device,
+                  int64_t* first_bad_row, void* stream) {
+  vfn::NvtxRange nvtx_range("vfn evaluate");
+  if (!p || (M > 0 && (!points || !out))) return fail(VFN_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> plan_lock(p->mu);
+  return plan_eval_locked(p, points, M, out, on_device, first_bad_row, stream);
+}
+
+int vfn_plan_eval_to_peers(vfn_plan* p, const double* points, int64_t M, const int32_t* rows, int npeers,
+                           const int64_t* seg_off, double* const* outs, int64_t* first_bad_row, void* stream) {
+  vfn::NvtxRange nvtx_range("vfn evaluate (values to their owners)");
+  if (!p || !seg_off || !outs || (M > 0 && (!points || !rows))) return fail(VFN_ERR_INVALID, "null argument");
+  if (npeers < 1 || npeers > kMaxPeers) return fail(VFN_ERR_INVALID, "peer count must be in 1..64");
+  if (seg_off[0] != 0 || seg_off[npeers] != M) return fail(VFN_ERR_INVALID, "peer ranges must cover the points");
+  std::lock_guard<std::mutex> plan_lock(p->mu);
+  if (first_bad_row) *first_bad_row = -1;
+  if (M == 0) return VFN_OK;
+  DeviceGuard guard(p->device);
+  cudaStream_t s = as_stream(stream);
+  VFN_CHECK(check_on_device(points, p->device, "points"));
+  PeerTable h;
+  h.n = npeers;
+  h.rows = rows;
+  for (int o = 0; o <= npeers; ++o) h.off[o] = seg_off[o];
+  for (int o = 0; o < npeers; ++o) h.out[o] = reinterpret_cast<double2*>(outs[o]);
+  VFN_CHECK(p->peer_buf.ensure(sizeof(PeerTable)));
+  VFN_CUDA(cudaMemcpyAsync(p->peer_buf.ptr, &h, sizeof(PeerTable), cudaMemcpyHostToDevice, s));
+  VFN_CUDA(cudaStreamSynchronize(s));  // h lives on this stack frame
+  // the evaluate's own output is scratch; values land in the owners' buffers
+  VFN_CHECK(p->out.ensure(sizeof(double2) * M));
+  const bool fused = M <= max_batch();  // batched calls index the rows per batch: scatter afterwards
+  p->peer_dev = fused ? p->peer_buf.as<PeerTable>() : nullptr;
+  p->peer_used = false;
+  int st = plan_eval_locked(p, points, M, p->out.as<double>(), 1, first_bad_row, stream);
+  p->peer_dev = nullptr;
+  if (st == VFN_OK && !fused) {
+    st = scatter_to_peers(p->out.as<double2>(), M, p->peer_buf.as<PeerTable>(), s);
+    if (st == VFN_OK && cudaStreamSynchronize(s) != cudaSuccess) st = fail(VFN_ERR_CUDA, "peer scatter failed");
+  }
+  return st;
 }
 
 int vfn_rect_eval(int device, const int64_t nmodes[3], const double a[3], const double b[3],

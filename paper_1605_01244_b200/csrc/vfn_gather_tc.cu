@@ -97,6 +97,7 @@ struct Args {
   int64_t nunits;         // unit-list capacity (bounds checks)
   TorusMap tm;
   BinGeom g;
+  const PeerTable* peer;  // non-null: values go to their owners' buffers (sharded evaluate)
 };
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -376,7 +377,19 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
   acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 1);
   acc_re += __shfl_xor_sync(0xffffffffu, acc_re, 2);
   acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 2);
-  if (valid && tig == 0) __stcs(A.out + prow, make_double2(acc_re, acc_im));
+  if (valid && tig == 0) {
+    const double2 v = make_double2(acc_re, acc_im);
+    if (A.peer) {
+      // fused return exchange: the value goes straight to the rank whose
+      // block the point came from (IPC-mapped peer memory over NVLink)
+      const PeerTable* T = A.peer;
+      int o = 0;
+      while (o + 1 < T->n && prow >= T->off[o + 1]) ++o;
+      T->out[o][T->rows[prow]] = v;
+    } else {
+      __stcs(A.out + prow, v);
+    }
+  }
   __syncwarp();  // the weight tables are rewritten by the next unit
 }
 
@@ -525,6 +538,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     kk = kk_n;
     up = up_n;
   }
+  if (A.peer) __threadfence_system();  // peer stores visible before the owners read
 }
 
 }  // namespace tc
@@ -735,6 +749,8 @@ int launch_tc(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t*
   A.nunits = M + 1;
   A.tm = p->map;
   A.g = g;
+  A.peer = p->peer_dev;
+  if (p->peer_dev) p->peer_used = true;
   mark_event(p, 1, s);  // gather timing starts here (binning prep excluded)
   switch (p->m) {
     case 2: return launch_m<2>(p, A, g.box[0], s);

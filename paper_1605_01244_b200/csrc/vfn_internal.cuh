@@ -142,6 +142,18 @@ struct WindowPoly {
   double* dev = nullptr;  // (2m+1)*(deg+1) doubles
 };
 
+// Outputs of a sharded evaluate that go straight to their owners (the
+// ranks whose input blocks the points came from) over NVLink: point i of
+// the evaluate belongs to the owner o with off[o] <= i < off[o + 1] and its
+// value is stored at out[o][rows[i]] (IPC-mapped peer memory).
+constexpr int kMaxPeers = 64;
+struct PeerTable {
+  int n = 0;
+  const int32_t* rows = nullptr;
+  int64_t off[kMaxPeers + 1];
+  double2* out[kMaxPeers];
+};
+
 }  // namespace vfn
 
 struct vfn_plan {
@@ -181,6 +193,12 @@ struct vfn_plan {
   vfn::DevBuf pts, out, uvals, keys, keys_sorted, idx, perm, sort_tmp, box_start, items, units, uscratch, misc;
   vfn::DevBuf warp_bad;  // first-bad-row word of the warp-per-point path (never reallocated)
   vfn::DevBuf sample;    // column-density sample of choose_geometry
+  // peer outputs of the current vfn_plan_eval_to_peers call (device table),
+  // consumed by the tensor-core gather's epilogue (peer_used) or by a
+  // scatter kernel after any other gather
+  const vfn::PeerTable* peer_dev = nullptr;
+  bool peer_used = false;
+  vfn::DevBuf peer_buf;
   vfn::DevBuf sample_pts;  // the density-sample rows of a host-buffer call
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t* bad_host = nullptr;  // mapped pinned word for the first-bad-row readback
@@ -316,6 +334,8 @@ bool tc_supported(int m);      // tensor-core gather covers this cutoff
 int tc_tile_depth(int m);     // its tile / box depth in cells (20 - 2m)
 void tc_tile_xy(int m, int* tx, int* ty);  // its tile x, y extents in cells
 bool tc_applicable(const vfn_plan* p, const BinGeom& g);
+// values[i] -> table.out[owner(i)][table.rows[i]] (vfn_shard.cu)
+int scatter_to_peers(const double2* values, int64_t M, const PeerTable* table_dev, cudaStream_t s);
 int launch_tc(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t* keys_sorted,
               const int32_t* box_start, double2* out, const BinGeom& g, int64_t M,
               cudaStream_t s);

@@ -14,6 +14,8 @@
 // so a key range is a run of whole tiles (x-slabs for a uniform set), and
 // ties inside one tile (config 3's dense cloud) are split by row.
 #include <algorithm>
+#include <cstring>
+#include <string>
 #include <vector>
 
 #include <cub/device/device_scan.cuh>
@@ -150,6 +152,16 @@ __global__ void k_gather_values(const double2* __restrict__ vals, const int32_t*
   if (i < M) out[i] = vals[pos[i]];
 }
 
+__global__ void k_scatter_to_peers(const double2* __restrict__ vals, int64_t M, const PeerTable* __restrict__ T) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < M) {
+    int o = 0;
+    while (o + 1 < T->n && i >= T->off[o + 1]) ++o;
+    T->out[o][T->rows[i]] = vals[i];
+  }
+  __threadfence_system();
+}
+
 TileMap tile_map(const vfn_plan* p) {
   TileMap T;
   T.tm = p->map;
@@ -162,6 +174,13 @@ TileMap tile_map(const vfn_plan* p) {
 }
 
 }  // namespace
+
+int scatter_to_peers(const double2* values, int64_t M, const PeerTable* table_dev, cudaStream_t s) {
+  if (M <= 0) return VFN_OK;
+  k_scatter_to_peers<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(values, M, table_dev);
+  VFN_CUDA(cudaGetLastError());
+  return VFN_OK;
+}
 
 }  // namespace vfn
 
@@ -241,6 +260,56 @@ int vfn_gather_values(int device, const double* values, const int32_t* pos, int6
   k_gather_values<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(reinterpret_cast<const double2*>(values), pos, M,
                                                               reinterpret_cast<double2*>(out));
   VFN_CUDA(cudaGetLastError());
+  return VFN_OK;
+}
+
+// ---- IPC-shared device buffers (the owners' output buffers of a sharded
+// evaluate; every rank maps the others' over NVLink)
+int vfn_ipc_alloc(int device, int64_t bytes, void** ptr, unsigned char handle[64]) {
+  if (!ptr || !handle || bytes <= 0) return fail(VFN_ERR_INVALID, "bad argument");
+  DeviceGuard guard(device);
+  *ptr = nullptr;
+  VFN_CUDA(cudaMalloc(ptr, (size_t)bytes));
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, *ptr);
+  if (e != cudaSuccess) {
+    cudaFree(*ptr);
+    *ptr = nullptr;
+    return fail(VFN_ERR_CUDA, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+  }
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  std::memcpy(handle, &h, 64);
+  return VFN_OK;
+}
+
+int vfn_ipc_open(int device, const unsigned char handle[64], void** ptr) {
+  if (!ptr || !handle) return fail(VFN_ERR_INVALID, "bad argument");
+  DeviceGuard guard(device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  VFN_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return VFN_OK;
+}
+
+int vfn_ipc_close(int device, void* ptr) {
+  DeviceGuard guard(device);
+  VFN_CUDA(cudaIpcCloseMemHandle(ptr));
+  return VFN_OK;
+}
+
+int vfn_ipc_free(int device, void* ptr) {
+  DeviceGuard guard(device);
+  VFN_CUDA(cudaFree(ptr));
+  return VFN_OK;
+}
+
+// dst <- src, device to device on `stream`, synchronised
+int vfn_copy_device(int device, void* dst, const void* src, int64_t bytes, void* stream) {
+  if (bytes <= 0) return VFN_OK;
+  DeviceGuard guard(device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  VFN_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, s));
+  VFN_CUDA(cudaStreamSynchronize(s));
   return VFN_OK;
 }
 

@@ -305,6 +305,12 @@ class NufftPlan:
         self._handle = handle
 
     def __del__(self):
+        po = getattr(self, "_peer_outputs", None)
+        if po is not None:
+            try:
+                po.close()
+            except Exception:
+                pass
         h = getattr(self, "_handle", None)
         if h is not None and _lib is not None and _lib._lib is not None:
             try:
@@ -400,6 +406,23 @@ class NufftPlan:
         if raise_outside:
             return send, list(counts), pos
         return send, list(counts), pos, -1
+
+    def evaluate_to_peers(self, points, rows, seg_off, outs) -> None:
+        """Evaluate received points (CUDA (M, 3)) and store each value at
+        outs[o][rows[i]] for its owner o (seg_off[o] <= i < seg_off[o + 1]);
+        ``outs``: device addresses (ints) of the owners' IPC-mapped buffers
+        (include/vfnfft.h vfn_plan_eval_to_peers)."""
+        M = int(points.shape[0])
+        n = len(outs)
+        off = (ctypes.c_int64 * (n + 1))(*[int(x) for x in seg_off])
+        ptrs = (ctypes.c_void_p * n)(*[int(x) for x in outs])
+        bad = ctypes.c_int64(-1)
+        st = _lib.load().vfn_plan_eval_to_peers(self._handle, _lib.ptr(points) if M else None, M,
+                                                _lib.ptr(rows) if M else None, n, off, ptrs,
+                                                ctypes.byref(bad), _stream_of(self.device))
+        if st == _lib.VFN_ERR_OUTSIDE:
+            raise ValueError(_outside_message(points, bad.value, self.domain))
+        _lib.check(st)
 
     def build_timing(self) -> dict:
         """Where the plan build went (ms): host wall time of the whole

@@ -16,7 +16,10 @@ plan; how the subsets are formed is this layer's choice:
   of key samples, the points move to the rank owning their key range with
   one all-to-all, each rank evaluates a spatially compact range of whole
   tiles at full point density, and the values come back with a second
-  all-to-all and are put back in input order on the device.  Input-order
+  all-to-all and are put back in input order on the device — or, by
+  default, the gathers store every value straight into its owner's
+  IPC-shared output buffer over NVLink (the return exchange fused into the
+  gather's epilogue, `vfn_plan_eval_to_peers`).  Input-order
   blocks would instead leave every rank with a sparse sample of the whole
   box: each grid tile staged for 1/P of its points (profiles/r01/
   pcie_chunks.md: a 1/8 block costs 2.3x its share of the gather).
@@ -128,6 +131,10 @@ class _Comm:
         out = torch.cat([p[:c] for p, c in zip(parts, counts)])
         return out.to(t.device)
 
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier(group=self.group)
+
     def all_reduce_min(self, v: int) -> int:
         import torch
 
@@ -207,6 +214,91 @@ def _gather_values(values, pos):
     return values[pos.long()]  # host tensors: the CPU plumbing tests only
 
 
+class _PeerOutputs:
+    """Every rank's output buffer for its own block, allocated by the library
+    (cudaMalloc) and exported as a CUDA IPC handle, so the gathers of all
+    ranks store the values of this rank's points straight into it over
+    NVLink (vfn_plan_eval_to_peers).  Two slots, used on alternate calls: a
+    rank copying call k's values out of its slot is never written by a call
+    k+1 gather (that uses the other slot), and call k+2 cannot start before
+    every rank has passed call k+1's collectives.  Ranks in the same process
+    (tests/simcomm.py threads) use each other's pointers directly."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.cap = 0
+        self.local = [None, None]       # (ptr, handle bytes) per slot
+        self.peers = None               # per slot: list of device addresses by rank
+        self.opened = {}                # (rank, handle) -> opened address
+        self.calls = 0
+
+    def _alloc(self, cap: int):
+        import ctypes
+
+        from . import _lib
+
+        lib = _lib.load()
+        for k in range(2):
+            if self.local[k] is not None:
+                lib.vfn_ipc_free(self.device, self.local[k][0])
+            ptr = ctypes.c_void_p()
+            h = (ctypes.c_ubyte * 64)()
+            _lib.check(lib.vfn_ipc_alloc(self.device, 16 * cap, ctypes.byref(ptr), h))
+            self.local[k] = (ptr.value, bytes(h))
+        self.cap = cap
+
+    def prepare(self, comm, m: int):
+        """Collective: slot buffers of every rank hold >= its block size; returns
+        (slot, local address, owners' addresses by rank)."""
+        import ctypes
+        import os
+
+        import numpy as np
+
+        from . import _lib
+
+        if m > self.cap or self.local[0] is None:
+            self._alloc(max(m + m // 4, 1024))
+        mine = [os.getpid()]
+        for k in range(2):
+            mine.append(self.local[k][0])
+            mine.extend(int(x) for x in np.frombuffer(self.local[k][1], dtype=np.int64))
+        allv = comm.all_gather_ints(mine)
+        pid = os.getpid()
+        peers = [[0] * comm.world for _ in range(2)]
+        for r, row in enumerate(allv):
+            for k in range(2):
+                ptr = row[1 + 9 * k]
+                handle = np.asarray(row[2 + 9 * k: 11 + 9 * k], dtype=np.int64).tobytes()
+                if r == comm.rank or row[0] == pid:
+                    peers[k][r] = ptr
+                    continue
+                key = (r, handle)
+                if key not in self.opened:
+                    out = ctypes.c_void_p()
+                    _lib.check(_lib.load().vfn_ipc_open(self.device, (ctypes.c_ubyte * 64)(*handle),
+                                                        ctypes.byref(out)))
+                    self.opened[key] = out.value
+                peers[k][r] = self.opened[key]
+        slot = self.calls & 1
+        self.calls += 1
+        return slot, self.local[slot][0], peers[slot]
+
+    def close(self):
+        from . import _lib
+
+        if _lib._lib is None:
+            return
+        lib = _lib._lib
+        for addr in self.opened.values():
+            lib.vfn_ipc_close(self.device, addr)
+        self.opened.clear()
+        for k in range(2):
+            if self.local[k] is not None:
+                lib.vfn_ipc_free(self.device, self.local[k][0])
+                self.local[k] = None
+
+
 class _Timer:
     def __init__(self, enabled: bool):
         import torch
@@ -230,17 +322,23 @@ class _Timer:
 
 
 def evaluate_sharded(plan, points, group=None, mode: str = "keyrange", out=None, stats: ShardStats | None = None,
-                     samples_per_rank: int = 1 << 18, comm=None):
+                     samples_per_rank: int = 1 << 18, comm=None, values: str = "p2p"):
     """Values of this rank's block of one point set, in input order (see the
     module docstring).  ``points``: this rank's (m, 3) block (a CUDA tensor
     on the plan's device); the blocks of ranks 0..P-1 concatenated in rank
     order are the whole set.  Every rank of ``group`` must call this.
     ``comm`` replaces the torch.distributed group with an object offering
-    `_Comm`'s methods (tests run P ranks as threads of one process)."""
+    `_Comm`'s methods (tests run P ranks as threads of one process).
+    ``values``: how the values get back to their owners — "p2p" (default):
+    the gathers store them straight into the owners' IPC-shared buffers over
+    NVLink (the return all-to-all fused into the gather epilogue); "nccl":
+    an all-to-all of the values and a local reorder."""
     import torch
 
     if mode not in ("keyrange", "block"):
         raise ValueError("mode must be 'keyrange' or 'block'")
+    if values not in ("p2p", "nccl"):
+        raise ValueError("values must be 'p2p' or 'nccl'")
     comm = comm if comm is not None else _Comm(group)
     if points.dim() != 2 or points.shape[1] != 3:
         raise ValueError(f"points must be an (M, 3) array, got shape {tuple(points.shape)}")
@@ -295,15 +393,43 @@ def evaluate_sharded(plan, points, group=None, mode: str = "keyrange", out=None,
         timer.mark()
         recv_counts = [c[comm.rank] for c in comm.all_gather_ints(send_counts)]
         recv = comm.all_to_all(send, send_counts, recv_counts)
-        timer.mark()
-        vals = plan.evaluate(recv)
-        timer.mark()
-        back = comm.all_to_all(torch.view_as_real(vals), recv_counts, send_counts)
-        timer.mark()
-        res = _gather_values(torch.view_as_complex(back.contiguous()), pos)
-        if out is not None:
-            out.copy_(res)
+        p2p = values == "p2p" and points.is_cuda and hasattr(plan, "evaluate_to_peers")
+        if p2p:
+            # each point travels with its row in the owner's block; the
+            # evaluate stores its value there (no return all-to-all)
+            rowinv = torch.empty(m, dtype=torch.int32, device=points.device)
+            rowinv[pos.long()] = torch.arange(m, dtype=torch.int32, device=points.device)
+            recv_rows = comm.all_to_all(rowinv, send_counts, recv_counts)
+            po = getattr(plan, "_peer_outputs", None)
+            if po is None:
+                po = plan._peer_outputs = _PeerOutputs(plan.device)
+            slot, mine, owners = po.prepare(comm, m)
+            timer.mark()
+            seg = [0]
+            for c in recv_counts:
+                seg.append(seg[-1] + c)
+            plan.evaluate_to_peers(recv, recv_rows, seg, owners)
+            timer.mark()
+            comm.barrier()  # every rank's stores into my buffer are done
+            timer.mark()
+            if out is None:
+                out = torch.empty(m, dtype=torch.complex128, device=points.device)
+            from . import _lib
+            from .nufft import _stream_of
+
+            _lib.check(_lib.load().vfn_copy_device(plan.device, out.data_ptr(), mine, 16 * m,
+                                                   _stream_of(plan.device)))
             res = out
+        else:
+            timer.mark()
+            vals = plan.evaluate(recv)
+            timer.mark()
+            back = comm.all_to_all(torch.view_as_real(vals), recv_counts, send_counts)
+            timer.mark()
+            res = _gather_values(torch.view_as_complex(back.contiguous()), pos)
+            if out is not None:
+                out.copy_(res)
+                res = out
         timer.mark()
         if stats is not None:
             sp = timer.spans(6)

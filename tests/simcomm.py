@@ -29,6 +29,9 @@ class ThreadComm:
         self.g.barrier.wait()
         return vals
 
+    def barrier(self):
+        self.g.barrier.wait()
+
     def all_gather_ints(self, values):
         return [list(v) for v in self._exchange(list(values))]
 

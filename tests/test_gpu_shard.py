@@ -191,3 +191,97 @@ def test_sharded_fuzz(vfb, draw):
     res = run_ranks(P, lambda r, comm: evaluate_sharded(
         plans[r], dpts[slice(*shard_range(M, P, r))], comm=comm).cpu().numpy())
     np.testing.assert_array_equal(np.concatenate(res), ref, err_msg=f"draw {draw}: P={P} M={M} kind={kind}")
+
+
+@pytest.mark.parametrize("values", ["p2p", "nccl"])
+def test_value_return_modes(vfb, offset_box, values):
+    """Both ways values get back to their owners — stored straight into the
+    owners' buffers by the gather (p2p, the default) or an all-to-all and a
+    reorder (nccl) — give the unsharded values bitwise, also with a
+    caller-provided ``out`` and on repeated calls (alternating buffers)."""
+    import torch
+
+    from paper_1605_01244_b200.parallel import evaluate_sharded, shard_range
+
+    spec = random_spectral(offset_box, (20, 24, 16), 1700)
+    pts = np.random.default_rng(1701).uniform(offset_box.a, offset_box.b, (400000, 3))
+    dpts = torch.as_tensor(pts, device="cuda")
+    ref = vfb.NufftPlan(spec).evaluate(dpts).cpu().numpy()
+    plans = [vfb.NufftPlan(spec) for _ in range(3)]
+
+    def rank(r, comm):
+        lo, hi = shard_range(len(pts), 3, r)
+        outs = []
+        for rep in range(3):
+            o = torch.empty(hi - lo, dtype=torch.complex128, device="cuda") if rep == 1 else None
+            v = evaluate_sharded(plans[r], dpts[lo:hi], comm=comm, values=values, out=o)
+            outs.append(v.cpu().numpy())
+        return outs
+
+    res = run_ranks(3, rank)
+    for rep in range(3):
+        np.testing.assert_array_equal(np.concatenate([x[rep] for x in res]), ref)
+
+
+def _ipc_worker(rank, world, port, q):
+    import os
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1605_01244_b200 as vfb
+    from paper_1605_01244_b200.parallel import ShardStats, evaluate_sharded, shard_range
+
+    try:
+        box = vfb.DomainBox((-0.5, -0.5, -0.5), (0.5, 0.5, 0.5))
+        rng = np.random.default_rng(1710)
+        coeffs = rng.standard_normal((32, 32, 32)) + 1j * rng.standard_normal((32, 32, 32))
+        spec = vfb.SpectralField(box, coeffs)
+        pts = np.random.default_rng(1711).uniform(-0.5, 0.5, (1 << 20, 3))
+        dpts = torch.as_tensor(pts, device="cuda")
+        plan = vfb.NufftPlan(spec)
+        ref = plan.evaluate(dpts).cpu().numpy()
+        lo, hi = shard_range(len(pts), world, rank)
+        ok = True
+        for _ in range(3):
+            st = ShardStats()
+            got = evaluate_sharded(plan, dpts[lo:hi], stats=st).cpu().numpy()
+            ok &= bool(np.array_equal(got, ref[lo:hi]))
+        q.put((rank, ok, st.received, None))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, False, 0, repr(e)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_processes_store_values_over_ipc():
+    """Two processes (gloo control plane, both on this GPU): each evaluates a
+    key range and the gather stores the values into the OTHER process's
+    IPC-mapped output buffer (cudaIpcOpenMemHandle), as ranks on separate
+    GPUs do over NVLink; every rank gets its block's unsharded values
+    bitwise, on repeated calls."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(2)])
+    for p in procs:
+        p.join(timeout=120)
+    for rank, ok, received, err in res:
+        assert err is None, err
+        assert ok, f"rank {rank}: sharded values differ"
+        assert 0.4 * (1 << 20) < received < 0.6 * (1 << 20)
