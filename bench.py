@@ -70,6 +70,9 @@ def parse():
     p.add_argument("--shard-mode", choices=["keyrange", "block"], default="keyrange",
                    help="strong scaling over N>1 ranks: keyrange (sample sort + all-to-all, default) or "
                         "block (each rank gathers its own input-order block)")
+    p.add_argument("--values", choices=["p2p", "nccl"], default="p2p",
+                   help="sharded evaluate: values stored by the gather into their owners' buffers over NVLink "
+                        "(p2p, default) or returned by an NCCL all-to-all")
     p.add_argument("--cutoff", type=int, default=6,
                    help="window half-width m (BASELINE's metric is quoted at the default 6)")
     return p.parse_args()
@@ -336,7 +339,7 @@ def run_ours(args):
 
     def step(p, o):
         if sharded:
-            return evaluate_sharded(plan, p, out=o, stats=stats, mode=args.shard_mode)
+            return evaluate_sharded(plan, p, out=o, stats=stats, mode=args.shard_mode, values=args.values)
         return plan.evaluate(p, out=o)
 
     # ---- device-resident timing
@@ -374,10 +377,14 @@ def run_ours(args):
     if sharded:
         shard_info = {
             "mode": args.shard_mode,
+            "values": "p2p: the gather stores each value into its owner's IPC-shared buffer over NVLink "
+                      "(return all-to-all fused into the gather epilogue)" if args.values == "p2p"
+                      else "nccl: all-to-all of the values, then a reorder",
             "partition_ms": max_over_ranks(stats.partition_ms),
             "all_to_all_points_ms": max_over_ranks(stats.exchange_in_ms),
             "evaluate_ms": max_over_ranks(stats.evaluate_ms),
-            "all_to_all_values_ms": max_over_ranks(stats.exchange_out_ms),
+            "values_return_ms": max_over_ranks(stats.exchange_out_ms),
+            "output_copy_ms": max_over_ranks(stats.restore_ms),
             "decide_ms": max_over_ranks(stats.decide_ms),
             "received_max": int(max_over_ranks(float(stats.received))),
             "received_min": int(-max_over_ranks(-float(stats.received))),
@@ -400,7 +407,7 @@ def run_ours(args):
     def e2e_step():
         if sharded:  # this rank's block: H2D, sharded evaluate, D2H
             pts.copy_(pts_host, non_blocking=True)
-            r = evaluate_sharded(plan, pts, out=out, mode=args.shard_mode)
+            r = evaluate_sharded(plan, pts, out=out, mode=args.shard_mode, values=args.values)
             out_host.copy_(r, non_blocking=True)
             torch.cuda.current_stream(dev).synchronize()
         else:

@@ -263,13 +263,14 @@ class _PeerOutputs:
         for k in range(2):
             mine.append(self.local[k][0])
             mine.extend(int(x) for x in np.frombuffer(self.local[k][1], dtype=np.int64))
+        mine.append(self.calls)
         allv = comm.all_gather_ints(mine)
         pid = os.getpid()
         peers = [[0] * comm.world for _ in range(2)]
         for r, row in enumerate(allv):
             for k in range(2):
                 ptr = row[1 + 9 * k]
-                handle = np.asarray(row[2 + 9 * k: 11 + 9 * k], dtype=np.int64).tobytes()
+                handle = np.asarray(row[2 + 9 * k: 10 + 9 * k], dtype=np.int64).tobytes()
                 if r == comm.rank or row[0] == pid:
                     peers[k][r] = ptr
                     continue
@@ -280,8 +281,11 @@ class _PeerOutputs:
                                                         ctypes.byref(out)))
                     self.opened[key] = out.value
                 peers[k][r] = self.opened[key]
-        slot = self.calls & 1
-        self.calls += 1
+        # one slot for the whole call, agreed by all ranks (their call counts
+        # may differ: a plan can join later calls of another rank set)
+        c = max(row[-1] for row in allv)
+        slot = c & 1
+        self.calls = c + 1
         return slot, self.local[slot][0], peers[slot]
 
     def close(self):

@@ -253,8 +253,10 @@ def _ipc_worker(rank, world, port, q):
             got = evaluate_sharded(plan, dpts[lo:hi], stats=st).cpu().numpy()
             ok &= bool(np.array_equal(got, ref[lo:hi]))
         q.put((rank, ok, st.received, None))
-    except Exception as e:  # noqa: BLE001
-        q.put((rank, False, 0, repr(e)))
+    except Exception:  # noqa: BLE001
+        import traceback
+
+        q.put((rank, False, 0, traceback.format_exc()))
     dist.barrier()
     dist.destroy_process_group()
 
