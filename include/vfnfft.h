@@ -281,6 +281,20 @@ int vfn_plan_partition(vfn_plan* plan, const double* points, int64_t M, int64_t 
                        int64_t* counts, int64_t* first_bad_row, void* stream);
 int vfn_gather_values(int device, const double* values, const int32_t* pos, int64_t M, double* out,
                       void* stream);
+/* The same split with the all-to-all of the points fused in: the count
+ * phase (counts per destination, host; the plan keeps the destinations),
+ * then — once every rank knows its offset dst_off[d] inside destination
+ * d's receive buffer (an all-gather of the counts) — the scatter phase
+ * writes point i to recv_pts[d] + 3 (dst_off[d] + q) and its row i to
+ * recv_rows[d][dst_off[d] + q], q its position among this rank's points
+ * of destination d, in input order: the receiving ranks' IPC-mapped
+ * buffers over NVLink.                                                   */
+int vfn_plan_partition_count(vfn_plan* plan, const double* points, int64_t M, int64_t row0,
+                             const uint64_t* splitters, int nparts, int64_t* counts, int64_t* first_bad_row,
+                             void* stream);
+int vfn_plan_partition_scatter_peers(vfn_plan* plan, const double* points, int64_t M, int nparts,
+                                     const int64_t* dst_off, double* const* recv_pts, int32_t* const* recv_rows,
+                                     void* stream);
 
 /* Evaluate M received points (device) and store each value in the buffer
  * of the rank that owns the point, instead of a local output: point i

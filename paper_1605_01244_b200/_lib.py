@@ -144,6 +144,16 @@ SIGNATURES = {
         [_vp, _vp, ctypes.c_int64, ctypes.c_int64, _vp, ctypes.c_int, _vp, _vp, _vp,
          ctypes.POINTER(ctypes.c_int64), _vp],
     ),
+    "vfn_plan_partition_count": (
+        ctypes.c_int,
+        [_vp, _vp, ctypes.c_int64, ctypes.c_int64, _vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
+         ctypes.POINTER(ctypes.c_int64), _vp],
+    ),
+    "vfn_plan_partition_scatter_peers": (
+        ctypes.c_int,
+        [_vp, _vp, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_vp),
+         ctypes.POINTER(_vp), _vp],
+    ),
     "vfn_gather_values": (ctypes.c_int, [ctypes.c_int, _vp, _vp, ctypes.c_int64, _vp, _vp]),
     "vfn_plan_decide": (
         ctypes.c_int,

@@ -3,6 +3,7 @@
 
 #include <cstdint>
 #include <mutex>
+#include <vector>
 
 #include <nvtx3/nvToolsExt.h>
 #include <cstdio>
@@ -199,6 +200,11 @@ struct vfn_plan {
   const vfn::PeerTable* peer_dev = nullptr;
   bool peer_used = false;
   vfn::DevBuf peer_buf;
+  // count phase of the last vfn_plan_partition_count (for the scatter phase)
+  int64_t part_M = -1;
+  int part_n = 0;
+  std::vector<int64_t> part_start;  // local send-buffer start of each destination
+  vfn::DevBuf part_buf;
   vfn::DevBuf sample_pts;  // the density-sample rows of a host-buffer call
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t* bad_host = nullptr;  // mapped pinned word for the first-bad-row readback

@@ -101,11 +101,23 @@ __global__ void __launch_bounds__(kPartThreads) k_part_count(const double* __res
 // processed in rounds of 256; inside a round the order is warp-major, then
 // lane, so ranks come from __match_any_sync within a warp plus per-warp
 // per-destination prefix sums in shared memory.
+// Destinations of a partition that writes straight into the receiving
+// ranks' buffers (IPC-mapped over NVLink): the point at local send
+// position p of destination d goes to pts[d] + 3 (base[d] + p), its row
+// to rows[d][base[d] + p] (base = my offset in d's buffer - d's local start).
+struct PartDst {
+  double* pts[kPartMax];
+  int32_t* rows[kPartMax];
+  int64_t base[kPartMax];
+};
+
+template <bool REMOTE>
 __global__ void __launch_bounds__(kPartThreads) k_part_scatter(const double* __restrict__ pts, int64_t M,
                                                                const uint8_t* __restrict__ dest,
                                                                const int32_t* __restrict__ offs, int nparts,
                                                                int nblocks, double* __restrict__ send,
-                                                               int32_t* __restrict__ pos) {
+                                                               int32_t* __restrict__ pos,
+                                                               const PartDst* __restrict__ dst) {
   constexpr int kW = kPartThreads / 32;
   __shared__ int s_run[kPartMax];        // next position per destination
   __shared__ int s_wc[kW][kPartMax];     // this round's count per warp and destination
@@ -125,11 +137,20 @@ __global__ void __launch_bounds__(kPartThreads) k_part_scatter(const double* __r
     if (live) {
       int p = s_run[d] + rank;
       for (int w = 0; w < warp; ++w) p += s_wc[w][d];
-      pos[i] = p;
       const double x0 = pts[3 * i], x1 = pts[3 * i + 1], x2 = pts[3 * i + 2];
-      send[3 * (int64_t)p] = x0;
-      send[3 * (int64_t)p + 1] = x1;
-      send[3 * (int64_t)p + 2] = x2;
+      if (REMOTE) {
+        const int64_t q = dst->base[d] + p;
+        double* o = dst->pts[d] + 3 * q;
+        o[0] = x0;
+        o[1] = x1;
+        o[2] = x2;
+        dst->rows[d][q] = (int32_t)i;
+      } else {
+        pos[i] = p;
+        send[3 * (int64_t)p] = x0;
+        send[3 * (int64_t)p + 1] = x1;
+        send[3 * (int64_t)p + 2] = x2;
+      }
     }
     __syncthreads();
     for (int e = threadIdx.x; e < nparts; e += blockDim.x) {
@@ -139,6 +160,7 @@ __global__ void __launch_bounds__(kPartThreads) k_part_scatter(const double* __r
     }
     __syncthreads();  // s_wc is zeroed by the next round
   }
+  if (REMOTE) __threadfence_system();  // peer stores visible before the receivers read
 }
 
 __global__ void k_part_totals(const int32_t* __restrict__ offs, int nparts, int nblocks, int64_t* __restrict__ out) {
@@ -235,7 +257,7 @@ int vfn_plan_partition(vfn_plan* p, const double* points, int64_t M, int64_t row
   VFN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, off, (int)ncnt, s));
   VFN_CHECK(p->sort_tmp.ensure(tmp));
   VFN_CUDA(cub::DeviceScan::ExclusiveSum(p->sort_tmp.ptr, tmp, cnt, off, (int)ncnt, s));
-  k_part_scatter<<<nb, kPartThreads, 0, s>>>(points, M, dest, off, nparts, nb, send, pos);
+  k_part_scatter<false><<<nb, kPartThreads, 0, s>>>(points, M, dest, off, nparts, nb, send, pos, nullptr);
   VFN_CUDA(cudaGetLastError());
   k_part_totals<<<1, 288, 0, s>>>(off, nparts, nb, tot);
   VFN_CUDA(cudaGetLastError());
@@ -248,6 +270,91 @@ int vfn_plan_partition(vfn_plan* p, const double* points, int64_t M, int64_t row
     return fail(VFN_ERR_OUTSIDE, "point (row " + std::to_string(b) + ") lies outside the domain");
   }
   for (int d = 0; d < nparts; ++d) counts[d] = h[d + 1] - h[d];
+  return VFN_OK;
+}
+
+// Count phase of a partition whose scatter writes to the receiving ranks:
+// destinations, per-destination counts (host) and the first bad row; the
+// plan keeps the destination bytes and block offsets for
+// vfn_plan_partition_scatter_peers with the same points.
+int vfn_plan_partition_count(vfn_plan* p, const double* points, int64_t M, int64_t row0, const uint64_t* splitters,
+                             int nparts, int64_t* counts, int64_t* first_bad_row, void* stream) {
+  vfn::NvtxRange nvtx_range("vfn partition: count");
+  if (!p || !counts || (M > 0 && !points) || (nparts > 1 && !splitters)) return fail(VFN_ERR_INVALID, "null argument");
+  if (nparts < 1 || nparts > kPartMax) return fail(VFN_ERR_INVALID, "destination count must be in 1..256");
+  if (M < 0 || M > INT32_MAX) return fail(VFN_ERR_INVALID, "point count out of range");
+  if (first_bad_row) *first_bad_row = -1;
+  for (int d = 0; d < nparts; ++d) counts[d] = 0;
+  std::lock_guard<std::mutex> plan_lock(p->mu);
+  p->part_M = M;
+  p->part_n = nparts;
+  if (M == 0) return VFN_OK;
+  DeviceGuard guard(p->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int nb = (int)((M + kPartChunk - 1) / kPartChunk);
+  const int64_t ncnt = (int64_t)nparts * nb + 1;
+  VFN_CHECK(p->keys.ensure(M));
+  VFN_CHECK(p->uscratch.ensure(sizeof(int32_t) * 2 * ncnt + sizeof(int64_t) * (nparts + 2)));
+  uint8_t* dest = p->keys.as<uint8_t>();
+  int32_t* cnt = p->uscratch.as<int32_t>();
+  int32_t* off = cnt + ncnt;
+  int64_t* tot = reinterpret_cast<int64_t*>(off + ncnt);
+  int64_t* bad = tot + nparts + 1;
+  VFN_CUDA(cudaMemsetAsync(bad, 0x7f, sizeof(int64_t), s));
+  VFN_CUDA(cudaMemsetAsync(cnt + ncnt - 1, 0, sizeof(int32_t), s));
+  k_part_count<<<nb, kPartThreads, 0, s>>>(points, M, row0, tile_map(p), splitters, nparts - 1, dest, cnt, nb,
+                                           reinterpret_cast<unsigned long long*>(bad));
+  VFN_CUDA(cudaGetLastError());
+  size_t tmp = 0;
+  VFN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, off, (int)ncnt, s));
+  VFN_CHECK(p->sort_tmp.ensure(tmp));
+  VFN_CUDA(cub::DeviceScan::ExclusiveSum(p->sort_tmp.ptr, tmp, cnt, off, (int)ncnt, s));
+  k_part_totals<<<1, 288, 0, s>>>(off, nparts, nb, tot);
+  VFN_CUDA(cudaGetLastError());
+  std::vector<int64_t> h(nparts + 2);
+  VFN_CUDA(cudaMemcpyAsync(h.data(), tot, sizeof(int64_t) * (nparts + 2), cudaMemcpyDeviceToHost, s));
+  VFN_CUDA(cudaStreamSynchronize(s));
+  const int64_t b = h[nparts + 1];
+  if (b != (int64_t)0x7f7f7f7f7f7f7f7fLL) {
+    if (first_bad_row) *first_bad_row = b;
+    return fail(VFN_ERR_OUTSIDE, "point (row " + std::to_string(b) + ") lies outside the domain");
+  }
+  p->part_start.assign(h.begin(), h.begin() + nparts);
+  for (int d = 0; d < nparts; ++d) counts[d] = h[d + 1] - h[d];
+  return VFN_OK;
+}
+
+// Scatter phase: point i of destination d (local send position q inside d)
+// goes to recv_pts[d] + 3 (dst_off[d] + q) and its row i to
+// recv_rows[d][dst_off[d] + q] — the receiving ranks' IPC-mapped buffers,
+// written over NVLink (the all-to-all of the points fused into the split).
+int vfn_plan_partition_scatter_peers(vfn_plan* p, const double* points, int64_t M, int nparts,
+                                     const int64_t* dst_off, double* const* recv_pts, int32_t* const* recv_rows,
+                                     void* stream) {
+  vfn::NvtxRange nvtx_range("vfn partition: scatter to peers");
+  if (!p || !dst_off || !recv_pts || !recv_rows || (M > 0 && !points)) return fail(VFN_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> plan_lock(p->mu);
+  if (M != p->part_M || nparts != p->part_n || (int)p->part_start.size() != (M ? nparts : 0))
+    return fail(VFN_ERR_INVALID, "partition scatter without a matching count phase");
+  if (M == 0) return VFN_OK;
+  DeviceGuard guard(p->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int nb = (int)((M + kPartChunk - 1) / kPartChunk);
+  const int64_t ncnt = (int64_t)nparts * nb + 1;
+  PartDst h;
+  for (int d = 0; d < nparts; ++d) {
+    h.pts[d] = recv_pts[d];
+    h.rows[d] = recv_rows[d];
+    h.base[d] = dst_off[d] - p->part_start[d];
+  }
+  VFN_CHECK(p->part_buf.ensure(sizeof(PartDst)));
+  VFN_CUDA(cudaMemcpyAsync(p->part_buf.ptr, &h, sizeof(PartDst), cudaMemcpyHostToDevice, s));
+  const uint8_t* dest = p->keys.as<uint8_t>();
+  const int32_t* off = p->uscratch.as<int32_t>() + ncnt;
+  k_part_scatter<true><<<nb, kPartThreads, 0, s>>>(points, M, dest, off, nparts, nb, nullptr, nullptr,
+                                                   p->part_buf.as<PartDst>());
+  VFN_CUDA(cudaGetLastError());
+  VFN_CUDA(cudaStreamSynchronize(s));  // h lives on this stack frame; the receivers read after a barrier
   return VFN_OK;
 }
 

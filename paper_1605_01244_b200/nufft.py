@@ -305,7 +305,7 @@ class NufftPlan:
         self._handle = handle
 
     def __del__(self):
-        po = getattr(self, "_peer_outputs", None)
+        po = getattr(self, "_peer_buffers", None)
         if po is not None:
             try:
                 po.close()
@@ -407,22 +407,51 @@ class NufftPlan:
             return send, list(counts), pos
         return send, list(counts), pos, -1
 
-    def evaluate_to_peers(self, points, rows, seg_off, outs) -> None:
-        """Evaluate received points (CUDA (M, 3)) and store each value at
-        outs[o][rows[i]] for its owner o (seg_off[o] <= i < seg_off[o + 1]);
-        ``outs``: device addresses (ints) of the owners' IPC-mapped buffers
-        (include/vfnfft.h vfn_plan_eval_to_peers)."""
-        M = int(points.shape[0])
+    def evaluate_to_peers(self, points, rows, seg_off, outs, M: int | None = None) -> None:
+        """Evaluate received points (CUDA (M, 3), or a device address with
+        ``M``) and store each value at outs[o][rows[i]] for its owner o
+        (seg_off[o] <= i < seg_off[o + 1]); ``outs``: device addresses (ints)
+        of the owners' IPC-mapped buffers; ``rows``: CUDA int32 tensor or
+        device address (include/vfnfft.h vfn_plan_eval_to_peers)."""
+        if M is None:
+            M = int(points.shape[0])
+        pp = points if isinstance(points, int) else _lib.ptr(points)
+        rp = rows if isinstance(rows, int) else _lib.ptr(rows)
         n = len(outs)
         off = (ctypes.c_int64 * (n + 1))(*[int(x) for x in seg_off])
         ptrs = (ctypes.c_void_p * n)(*[int(x) for x in outs])
         bad = ctypes.c_int64(-1)
-        st = _lib.load().vfn_plan_eval_to_peers(self._handle, _lib.ptr(points) if M else None, M,
-                                                _lib.ptr(rows) if M else None, n, off, ptrs,
-                                                ctypes.byref(bad), _stream_of(self.device))
+        st = _lib.load().vfn_plan_eval_to_peers(self._handle, pp if M else None, M, rp if M else None, n, off,
+                                                ptrs, ctypes.byref(bad), _stream_of(self.device))
         if st == _lib.VFN_ERR_OUTSIDE:
             raise ValueError(_outside_message(points, bad.value, self.domain))
         _lib.check(st)
+
+    def partition_count(self, points, splitters, row0: int = 0):
+        """Count phase of a partition scattered straight to the receiving ranks:
+        (per-destination counts, first out-of-domain local row or -1)."""
+        M = int(points.shape[0])
+        nparts = int(splitters.shape[0]) + 1
+        counts = (ctypes.c_int64 * nparts)()
+        bad = ctypes.c_int64(-1)
+        st = _lib.load().vfn_plan_partition_count(self._handle, _lib.ptr(points) if M else None, M, int(row0),
+                                                  _lib.ptr(splitters) if nparts > 1 else None, nparts, counts,
+                                                  ctypes.byref(bad), _stream_of(self.device))
+        if st == _lib.VFN_ERR_OUTSIDE:
+            return [0] * nparts, bad.value
+        _lib.check(st)
+        return list(counts), -1
+
+    def partition_scatter_peers(self, points, dst_off, recv_pts, recv_rows) -> None:
+        """Scatter phase: this rank's points into the destinations' receive
+        buffers (device addresses), at dst_off[d] + position (vfn_plan_partition_scatter_peers)."""
+        M = int(points.shape[0])
+        n = len(dst_off)
+        off = (ctypes.c_int64 * n)(*[int(x) for x in dst_off])
+        rp = (ctypes.c_void_p * n)(*[int(x) for x in recv_pts])
+        rr = (ctypes.c_void_p * n)(*[int(x) for x in recv_rows])
+        _lib.check(_lib.load().vfn_plan_partition_scatter_peers(self._handle, _lib.ptr(points) if M else None, M, n,
+                                                                off, rp, rr, _stream_of(self.device)))
 
     def build_timing(self) -> dict:
         """Where the plan build went (ms): host wall time of the whole

@@ -214,42 +214,50 @@ def _gather_values(values, pos):
     return values[pos.long()]  # host tensors: the CPU plumbing tests only
 
 
-class _PeerOutputs:
-    """Every rank's output buffer for its own block, allocated by the library
-    (cudaMalloc) and exported as a CUDA IPC handle, so the gathers of all
-    ranks store the values of this rank's points straight into it over
-    NVLink (vfn_plan_eval_to_peers).  Two slots, used on alternate calls: a
-    rank copying call k's values out of its slot is never written by a call
-    k+1 gather (that uses the other slot), and call k+2 cannot start before
-    every rank has passed call k+1's collectives.  Ranks in the same process
-    (tests/simcomm.py threads) use each other's pointers directly."""
+class _PeerBuffers:
+    """Per rank, two slots of IPC-shared device buffers (allocated by the
+    library with cudaMalloc, exported as CUDA IPC handles and mapped by every
+    other rank; ranks in the same process — tests/simcomm.py threads — use
+    each other's pointers directly):
+
+    * ``out`` — the values of this rank's own block; every rank's gather
+      stores into it over NVLink (vfn_plan_eval_to_peers);
+    * ``in``  — the points (24 B) and their rows in their owners' blocks
+      (4 B) that the other ranks' partition kernels scatter into it over
+      NVLink (vfn_plan_partition_scatter_peers).
+
+    The slots alternate between calls on a slot number the ranks agree on:
+    a rank still reading call k's buffers is never written by a call k + 1
+    kernel (that uses the other slot), and call k + 2 cannot start before
+    every rank has passed call k + 1's collectives."""
+
+    KINDS = ("out", "in")
 
     def __init__(self, device: int):
         self.device = device
-        self.cap = 0
-        self.local = [None, None]       # (ptr, handle bytes) per slot
-        self.peers = None               # per slot: list of device addresses by rank
-        self.opened = {}                # (rank, handle) -> opened address
+        self.cap = {"out": 0, "in": 0}
+        self.local = {"out": [None, None], "in": [None, None]}  # (address, handle bytes) per slot
+        self.opened = {}  # (rank, handle) -> mapped address
         self.calls = 0
 
-    def _alloc(self, cap: int):
+    def _alloc(self, kind: str, cap: int, elem: int):
         import ctypes
 
         from . import _lib
 
         lib = _lib.load()
         for k in range(2):
-            if self.local[k] is not None:
-                lib.vfn_ipc_free(self.device, self.local[k][0])
+            if self.local[kind][k] is not None:
+                lib.vfn_ipc_free(self.device, self.local[kind][k][0])
             ptr = ctypes.c_void_p()
             h = (ctypes.c_ubyte * 64)()
-            _lib.check(lib.vfn_ipc_alloc(self.device, 16 * cap, ctypes.byref(ptr), h))
-            self.local[k] = (ptr.value, bytes(h))
-        self.cap = cap
+            _lib.check(lib.vfn_ipc_alloc(self.device, elem * cap, ctypes.byref(ptr), h))
+            self.local[kind][k] = (ptr.value, bytes(h))
+        self.cap[kind] = cap
 
-    def prepare(self, comm, m: int):
-        """Collective: slot buffers of every rank hold >= its block size; returns
-        (slot, local address, owners' addresses by rank)."""
+    def prepare(self, comm, m_out: int, m_in: int = 0):
+        """Collective: this rank's slots hold m_out values and m_in received
+        points; returns (slot, {kind: local address}, {kind: addresses by rank})."""
         import ctypes
         import os
 
@@ -257,22 +265,30 @@ class _PeerOutputs:
 
         from . import _lib
 
-        if m > self.cap or self.local[0] is None:
-            self._alloc(max(m + m // 4, 1024))
-        mine = [os.getpid()]
-        for k in range(2):
-            mine.append(self.local[k][0])
-            mine.extend(int(x) for x in np.frombuffer(self.local[k][1], dtype=np.int64))
-        mine.append(self.calls)
+        for kind, m, elem in (("out", m_out, 16), ("in", m_in, 28)):
+            if m > self.cap[kind] or self.local[kind][0] is None:
+                self._alloc(kind, max(m + m // 4, 1024), elem)
+        mine = [os.getpid(), self.calls, self.cap["in"]]
+        for kind in self.KINDS:
+            for k in range(2):
+                mine.append(self.local[kind][k][0])
+                mine.extend(int(x) for x in np.frombuffer(self.local[kind][k][1], dtype=np.int64))
         allv = comm.all_gather_ints(mine)
         pid = os.getpid()
-        peers = [[0] * comm.world for _ in range(2)]
+        # one slot for the whole call, agreed by all ranks (their call counts
+        # may differ: a plan can join later calls of another rank set)
+        c = max(row[1] for row in allv)
+        slot = c & 1
+        self.calls = c + 1
+        addrs = {kind: [0] * comm.world for kind in self.KINDS}
+        caps_in = [row[2] for row in allv]
         for r, row in enumerate(allv):
-            for k in range(2):
-                ptr = row[1 + 9 * k]
-                handle = np.asarray(row[2 + 9 * k: 10 + 9 * k], dtype=np.int64).tobytes()
+            for ki, kind in enumerate(self.KINDS):
+                base = 3 + 9 * (2 * ki + slot)
+                ptr = row[base]
+                handle = np.asarray(row[base + 1: base + 9], dtype=np.int64).tobytes()
                 if r == comm.rank or row[0] == pid:
-                    peers[k][r] = ptr
+                    addrs[kind][r] = ptr
                     continue
                 key = (r, handle)
                 if key not in self.opened:
@@ -280,13 +296,10 @@ class _PeerOutputs:
                     _lib.check(_lib.load().vfn_ipc_open(self.device, (ctypes.c_ubyte * 64)(*handle),
                                                         ctypes.byref(out)))
                     self.opened[key] = out.value
-                peers[k][r] = self.opened[key]
-        # one slot for the whole call, agreed by all ranks (their call counts
-        # may differ: a plan can join later calls of another rank set)
-        c = max(row[-1] for row in allv)
-        slot = c & 1
-        self.calls = c + 1
-        return slot, self.local[slot][0], peers[slot]
+                addrs[kind][r] = self.opened[key]
+        local = {kind: self.local[kind][slot][0] for kind in self.KINDS}
+        self.caps_in = caps_in
+        return slot, local, addrs
 
     def close(self):
         from . import _lib
@@ -297,10 +310,11 @@ class _PeerOutputs:
         for addr in self.opened.values():
             lib.vfn_ipc_close(self.device, addr)
         self.opened.clear()
-        for k in range(2):
-            if self.local[k] is not None:
-                lib.vfn_ipc_free(self.device, self.local[k][0])
-                self.local[k] = None
+        for kind in self.KINDS:
+            for k in range(2):
+                if self.local[kind][k] is not None:
+                    lib.vfn_ipc_free(self.device, self.local[kind][k][0])
+                    self.local[kind][k] = None
 
 
 class _Timer:
@@ -333,10 +347,12 @@ def evaluate_sharded(plan, points, group=None, mode: str = "keyrange", out=None,
     order are the whole set.  Every rank of ``group`` must call this.
     ``comm`` replaces the torch.distributed group with an object offering
     `_Comm`'s methods (tests run P ranks as threads of one process).
-    ``values``: how the values get back to their owners — "p2p" (default):
-    the gathers store them straight into the owners' IPC-shared buffers over
-    NVLink (the return all-to-all fused into the gather epilogue); "nccl":
-    an all-to-all of the values and a local reorder."""
+    ``values``: how points and values move — "p2p" (default): the partition
+    kernel stores every point into its destination's IPC-shared receive
+    buffer and the gather's epilogue stores every value into its owner's
+    output buffer, both over NVLink (the two all-to-alls fused into the
+    kernels around them); "nccl": all-to-alls of points and values and a
+    local reorder."""
     import torch
 
     if mode not in ("keyrange", "block"):
@@ -384,7 +400,11 @@ def evaluate_sharded(plan, points, group=None, mode: str = "keyrange", out=None,
         keys = plan.part_keys(points, kstride, row0)
         kcounts = [c[0] for c in comm.all_gather_ints([int(keys.shape[0])])]
         split = splitters_from_samples(comm.all_gather_rows(keys, kcounts), comm.world)
-        send, send_counts, pos, bad = plan.partition(points, split, row0, raise_outside=False)
+        p2p = values == "p2p" and points.is_cuda and hasattr(plan, "partition_scatter_peers")
+        if p2p:
+            send_counts, bad = plan.partition_count(points, split, row0)
+        else:
+            send, send_counts, pos, bad = plan.partition(points, split, row0, raise_outside=False)
         # an outside point anywhere fails every rank with the global first row
         first = comm.all_reduce_min(row0 + bad if bad >= 0 else total)
         if first < total:
@@ -395,36 +415,39 @@ def evaluate_sharded(plan, points, group=None, mode: str = "keyrange", out=None,
             raise ValueError(f"point {bad_pt} (row {first}) lies outside the domain "
                              f"{list(plan.domain.a)} .. {list(plan.domain.b)}")
         timer.mark()
-        recv_counts = [c[comm.rank] for c in comm.all_gather_ints(send_counts)]
-        recv = comm.all_to_all(send, send_counts, recv_counts)
-        p2p = values == "p2p" and points.is_cuda and hasattr(plan, "evaluate_to_peers")
+        cmat = comm.all_gather_ints(send_counts)  # cmat[source][destination]
+        recv_counts = [c[comm.rank] for c in cmat]
         if p2p:
-            # each point travels with its row in the owner's block; the
-            # evaluate stores its value there (no return all-to-all)
-            rowinv = torch.empty(m, dtype=torch.int32, device=points.device)
-            rowinv[pos.long()] = torch.arange(m, dtype=torch.int32, device=points.device)
-            recv_rows = comm.all_to_all(rowinv, send_counts, recv_counts)
-            po = getattr(plan, "_peer_outputs", None)
+            # the points go straight into the destinations' receive buffers and
+            # the values straight into their owners' output buffers, both over
+            # NVLink (IPC-mapped); no all-to-all on the data path
+            r_in = sum(recv_counts)
+            po = getattr(plan, "_peer_buffers", None)
             if po is None:
-                po = plan._peer_outputs = _PeerOutputs(plan.device)
-            slot, mine, owners = po.prepare(comm, m)
+                po = plan._peer_buffers = _PeerBuffers(plan.device)
+            slot, local, addrs = po.prepare(comm, m, r_in)
+            dst_off = [sum(cmat[s_][d] for s_ in range(comm.rank)) for d in range(comm.world)]
+            rows_of = [addrs["in"][d] + 24 * po.caps_in[d] for d in range(comm.world)]
+            plan.partition_scatter_peers(points, dst_off, addrs["in"], rows_of)
+            comm.barrier()  # every rank's points are in my receive buffer
             timer.mark()
             seg = [0]
             for c in recv_counts:
                 seg.append(seg[-1] + c)
-            plan.evaluate_to_peers(recv, recv_rows, seg, owners)
+            plan.evaluate_to_peers(local["in"], local["in"] + 24 * po.cap["in"], seg, addrs["out"], M=r_in)
             timer.mark()
-            comm.barrier()  # every rank's stores into my buffer are done
+            comm.barrier()  # every rank's values for my block are in my output buffer
             timer.mark()
             if out is None:
                 out = torch.empty(m, dtype=torch.complex128, device=points.device)
             from . import _lib
             from .nufft import _stream_of
 
-            _lib.check(_lib.load().vfn_copy_device(plan.device, out.data_ptr(), mine, 16 * m,
+            _lib.check(_lib.load().vfn_copy_device(plan.device, out.data_ptr(), local["out"], 16 * m,
                                                    _stream_of(plan.device)))
             res = out
         else:
+            recv = comm.all_to_all(send, send_counts, recv_counts)
             timer.mark()
             vals = plan.evaluate(recv)
             timer.mark()
