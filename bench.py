@@ -377,11 +377,12 @@ def run_ours(args):
     if sharded:
         shard_info = {
             "mode": args.shard_mode,
-            "values": "p2p: the gather stores each value into its owner's IPC-shared buffer over NVLink "
-                      "(return all-to-all fused into the gather epilogue)" if args.values == "p2p"
-                      else "nccl: all-to-all of the values, then a reorder",
-            "partition_ms": max_over_ranks(stats.partition_ms),
-            "all_to_all_points_ms": max_over_ranks(stats.exchange_in_ms),
+            "exchange": "p2p: the partition kernel stores each point into its destination's IPC-shared receive "
+                        "buffer and the gather's epilogue stores each value into its owner's output buffer, both "
+                        "over NVLink (no all-to-all on the data path)" if args.values == "p2p"
+                        else "nccl: all_to_all_single of the points and of the values, then a reorder",
+            "partition_count_ms": max_over_ranks(stats.partition_ms),
+            "points_exchange_ms": max_over_ranks(stats.exchange_in_ms),
             "evaluate_ms": max_over_ranks(stats.evaluate_ms),
             "values_return_ms": max_over_ranks(stats.exchange_out_ms),
             "output_copy_ms": max_over_ranks(stats.restore_ms),
