@@ -265,15 +265,22 @@ class _PeerBuffers:
 
         from . import _lib
 
-        for kind, m, elem in (("out", m_out, 16), ("in", m_in, 28)):
-            if m > self.cap[kind] or self.local[kind][0] is None:
-                self._alloc(kind, max(m + m // 4, 1024), elem)
-        mine = [os.getpid(), self.calls, self.cap["in"]]
+        good = 1
+        try:
+            for kind, m, elem in (("out", m_out, 16), ("in", m_in, 28)):
+                if m > self.cap[kind] or self.local[kind][0] is None:
+                    self._alloc(kind, max(m + m // 4, 1024), elem)
+        except Exception:  # allocation failed: still join the collective below
+            good = 0
+        mine = [os.getpid(), self.calls, self.cap["in"] if good else 0, good]
         for kind in self.KINDS:
             for k in range(2):
-                mine.append(self.local[kind][k][0])
-                mine.extend(int(x) for x in np.frombuffer(self.local[kind][k][1], dtype=np.int64))
+                entry = self.local[kind][k] if good else None
+                mine.append(entry[0] if entry else 0)
+                mine.extend(int(x) for x in np.frombuffer(entry[1], dtype=np.int64)) if entry else mine.extend([0] * 8)
         allv = comm.all_gather_ints(mine)
+        if min(row[3] for row in allv) == 0:
+            raise RuntimeError("a rank could not allocate its peer buffers")
         pid = os.getpid()
         # one slot for the whole call, agreed by all ranks (their call counts
         # may differ: a plan can join later calls of another rank set)
@@ -284,7 +291,7 @@ class _PeerBuffers:
         caps_in = [row[2] for row in allv]
         for r, row in enumerate(allv):
             for ki, kind in enumerate(self.KINDS):
-                base = 3 + 9 * (2 * ki + slot)
+                base = 4 + 9 * (2 * ki + slot)
                 ptr = row[base]
                 handle = np.asarray(row[base + 1: base + 9], dtype=np.int64).tobytes()
                 if r == comm.rank or row[0] == pid:
@@ -400,7 +407,8 @@ def evaluate_sharded(plan, points, group=None, mode: str = "keyrange", out=None,
         keys = plan.part_keys(points, kstride, row0)
         kcounts = [c[0] for c in comm.all_gather_ints([int(keys.shape[0])])]
         split = splitters_from_samples(comm.all_gather_rows(keys, kcounts), comm.world)
-        p2p = values == "p2p" and points.is_cuda and hasattr(plan, "partition_scatter_peers")
+        p2p = (values == "p2p" and points.is_cuda and hasattr(plan, "partition_scatter_peers")
+               and not getattr(plan, "_p2p_failed", False))
         if p2p:
             send_counts, bad = plan.partition_count(points, split, row0)
         else:
@@ -425,7 +433,14 @@ def evaluate_sharded(plan, points, group=None, mode: str = "keyrange", out=None,
             po = getattr(plan, "_peer_buffers", None)
             if po is None:
                 po = plan._peer_buffers = _PeerBuffers(plan.device)
-            slot, local, addrs = po.prepare(comm, m, r_in)
+            try:
+                slot, local, addrs = po.prepare(comm, m, r_in)
+                ok = 1
+            except Exception:  # e.g. no peer access between two GPUs: every rank falls back
+                ok = 0
+            if comm.all_reduce_min(ok) == 0:
+                plan._p2p_failed = True
+                return evaluate_sharded(plan, points, group, mode, out, stats, samples_per_rank, comm, "nccl")
             dst_off = [sum(cmat[s_][d] for s_ in range(comm.rank)) for d in range(comm.world)]
             rows_of = [addrs["in"][d] + 24 * po.caps_in[d] for d in range(comm.world)]
             plan.partition_scatter_peers(points, dst_off, addrs["in"], rows_of)
