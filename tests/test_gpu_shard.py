@@ -287,3 +287,34 @@ def test_two_processes_store_values_over_ipc():
         assert err is None, err
         assert ok, f"rank {rank}: sharded values differ"
         assert 0.4 * (1 << 20) < received < 0.6 * (1 << 20)
+
+
+def test_peer_buffer_failure_falls_back_on_every_rank(vfb, offset_box):
+    """If one rank cannot allocate its IPC buffers, every rank takes the NCCL
+    exchange for that call and later ones (no rank left waiting in a
+    collective), with the same values."""
+    import torch
+
+    from paper_1605_01244_b200.parallel import _PeerBuffers, evaluate_sharded, shard_range
+
+    spec = random_spectral(offset_box, (16, 16, 16), 1800)
+    pts = np.random.default_rng(1801).uniform(offset_box.a, offset_box.b, (300000, 3))
+    dpts = torch.as_tensor(pts, device="cuda")
+    ref = vfb.NufftPlan(spec).evaluate(dpts).cpu().numpy()
+    plans = [vfb.NufftPlan(spec) for _ in range(3)]
+
+    def broken_alloc(self, kind, cap, elem):
+        raise RuntimeError("simulated allocation failure")
+
+    pb = _PeerBuffers(plans[1].device)
+    pb._alloc = broken_alloc.__get__(pb)
+    plans[1]._peer_buffers = pb
+
+    def rank(r, comm):
+        lo, hi = shard_range(len(pts), 3, r)
+        return [evaluate_sharded(plans[r], dpts[lo:hi], comm=comm).cpu().numpy() for _ in range(2)]
+
+    res = run_ranks(3, rank)
+    for k in range(2):
+        np.testing.assert_array_equal(np.concatenate([x[k] for x in res]), ref)
+    assert all(getattr(p, "_p2p_failed", False) for p in plans)
