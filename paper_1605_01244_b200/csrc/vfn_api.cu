@@ -105,6 +105,7 @@ namespace vfn {
 // else from the global density.
 BinGeom make_geometry(const vfn_plan* p, int bxy) {
   BinGeom g;
+  if (tc_supported(p->m) && p->has_tmap) bxy = std::min(bxy, tc_max_box(p->m));
   const int K = ((2 * p->m + 1) + 3) / 4 * 4;  // DMMA k-extent
   const int bk = K - 2 * p->m;                  // box depth in cells (2 or 4)
   const bool tc = tc_supported(p->m) && p->has_tmap;  // vfn_gather_tc.cu: 4x4xTZ tiles, depth-TZ boxes

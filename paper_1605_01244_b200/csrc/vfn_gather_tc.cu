@@ -49,30 +49,33 @@ constexpr int kWarpsDense = 16, kWarpsSparse = 12;
 constexpr int kSZ = 20;                   // staged z extent (TZ + 2m)
 constexpr int kLine = kSZ * 16;           // bytes per staged (x, y) line
 constexpr int kItemUnits = 48;            // units per work item
-constexpr int kXO = 1, kXS = 17;          // axes 1, 2 weight tables: j in [-1, 16)
+constexpr int kXO = 1;                    // axes 1, 2 weight tables: entry kXO + j holds phi_j, j >= -1
+constexpr int kScb = 16;                  // weight-DMMA B fragments per lane: 4 k-chunks x 3 n-blocks (+1 pad)
 
 template <int MC>
 struct Cfg {
-  static_assert(MC >= 2 && MC <= 7, "tensor-core gather covers m = 2..7");
+  static_assert(MC >= 2 && MC <= 8, "tensor-core gather covers m = 2..8");
   static constexpr int W = 2 * MC + 1;            // stencil width
   static constexpr int TZ = kSZ - 2 * MC;         // tile / box depth in cells
-  // tile x, y extents in cells: 4 x 4, and 4 x 2 at m = 7 so that two
-  // staged tiles still fit next to the weight tables
-  static constexpr int TX = 4, TY = MC == 7 ? 2 : 4;
+  // tile x, y extents in cells: 4 x 4, 4 x 2 at m = 7 and 2 x 1 at m = 8
+  // (1 x 1 boxes only) so that two staged tiles still fit next to the
+  // weight tables
+  static constexpr int TX = MC == 8 ? 2 : 4, TY = MC == 7 ? 2 : (MC == 8 ? 1 : 4);
   static constexpr int SX = TX + 2 * MC, SY = TY + 2 * MC;  // staged x, y extents
   static constexpr int kTileBytes = SX * SY * kLine;
   static constexpr int KCmin = (W + 3) / 4;       // fewest k-chunks a unit can use
   // A fragments from a per-warp axis-3 table (entry kAO + j holds phi_j,
   // j in [-TZ, 21)), or at m = 7 straight from the weight DMMA's registers
   // by quad shuffles (no table: its shared memory holds the larger tiles)
-  static constexpr bool kShflA = MC == 7;
+  static constexpr bool kShflA = MC >= 7;
   static constexpr int kAO = TZ, kAS = kShflA ? 0 : (TZ + 21) | 1;
+  static constexpr int kXS = MC == 8 ? 19 : 17;   // x / y tables: j in [-1, kXS - 1)
   static constexpr int kWarpW = kUnitPts * (kAS + 2 * kXS);
 };
 
 size_t smem_bytes(int mc, int nw) {
   auto f = [nw](int tile, int warpw) {
-    return (size_t)1024 + 2 * (size_t)tile + 48 + sizeof(double) * ((size_t)nw * warpw + 32 * 8);
+    return (size_t)1024 + 2 * (size_t)tile + 48 + sizeof(double) * ((size_t)nw * warpw + 32 * kScb);
   };
   switch (mc) {
     case 2: return f(Cfg<2>::kTileBytes, Cfg<2>::kWarpW);
@@ -80,6 +83,7 @@ size_t smem_bytes(int mc, int nw) {
     case 4: return f(Cfg<4>::kTileBytes, Cfg<4>::kWarpW);
     case 5: return f(Cfg<5>::kTileBytes, Cfg<5>::kWarpW);
     case 7: return f(Cfg<7>::kTileBytes, Cfg<7>::kWarpW);
+    case 8: return f(Cfg<8>::kTileBytes, Cfg<8>::kWarpW);
     default: return f(Cfg<6>::kTileBytes, Cfg<6>::kWarpW);
   }
 }
@@ -233,36 +237,42 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
   // 4 k-chunks of 4 powers (the fits have degree 12..14 for m <= 8), 8
   // stencil columns per n-block
   constexpr int NBW = (C::W + 7) / 8;
+  constexpr int kXS = C::kXS;
   double* wA = wt;                              // [8][kAS]  axis 3 (absent with kShflA)
   double* wX = wt + kUnitPts * kAS;             // [8][kXS]  axis 1
   double* wY = wX + kUnitPts * kXS;             // [8][kXS]  axis 2
-  double z00 = 0.0, z01 = 0.0, z10 = 0.0, z11 = 0.0;  // axis-3 weights in registers (kShflA)
+  // axis-3 weights in registers (kShflA): n-block nb, column pair e
+  double z[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     const double x1 = dl[d], x2 = x1 * x1, x4 = x2 * x2;
     double pw = tig == 0 ? 1.0 : (tig == 1 ? x1 : (tig == 2 ? x2 : x2 * x1));
-    double w00 = 0.0, w01 = 0.0, w10 = 0.0, w11 = 0.0;
+    double w[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
     for (int kc = 0; kc < 4; ++kc) {
-      const double2 c = *reinterpret_cast<const double2*>(scb + 2 * kc);  // (nb 0, nb 1)
-      dmma(w00, w01, pw, c.x);
-      if (NBW > 1) dmma(w10, w11, pw, c.y);
+      const double* c = scb + 4 * kc;  // (nb 0, nb 1 | nb 2, pad)
+      const double2 c01 = *reinterpret_cast<const double2*>(c);
+      dmma(w[0][0], w[0][1], pw, c01.x);
+      if (NBW > 1) dmma(w[1][0], w[1][1], pw, c01.y);
+      if (NBW > 2) dmma(w[2][0], w[2][1], pw, c[2]);
       pw *= x4;
     }
     if (C::kShflA && d == 2) {
-      z00 = w00;
-      z01 = w01;
-      z10 = w10;
-      z11 = w11;
+#pragma unroll
+      for (int nb = 0; nb < NBW; ++nb) {
+        z[nb][0] = w[nb][0];
+        z[nb][1] = w[nb][1];
+      }
       continue;
     }
     double* row = d == 2 ? wA + g * kAS + kAO : (d == 0 ? wX : wY) + g * kXS + kXO;
-    row[2 * tig] = w00;      // j = 2 tig, 2 tig + 1, 8 + 2 tig, 9 + 2 tig;
-    row[2 * tig + 1] = w01;  // j >= W come out exactly 0 (zero coefficients)
-    if (NBW > 1) {
-      row[8 + 2 * tig] = w10;
-      row[9 + 2 * tig] = w11;
-    }
+    // j = 8 nb + 2 tig + e; taps j >= W come out exactly 0 (zero
+    // coefficients) and are not stored past the tables (pre-zeroed)
+#pragma unroll
+    for (int nb = 0; nb < NBW; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        if (8 * nb + 2 * tig + e < C::W) row[8 * nb + 2 * tig + e] = w[nb][e];
   }
   __syncwarp();
   // A fragments: axis-3 weights of point g at staged depth kz + 4 kc + tig
@@ -273,10 +283,13 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
     for (int kc = 0; kc < KC; ++kc) {
       const int j = kz + 4 * kc + tig - ck;
       const int src = 4 * g + ((j & 7) >> 1);
-      const double v00 = __shfl_sync(0xffffffffu, z00, src), v01 = __shfl_sync(0xffffffffu, z01, src);
-      const double v10 = __shfl_sync(0xffffffffu, z10, src), v11 = __shfl_sync(0xffffffffu, z11, src);
-      const double v = (j & 8) ? ((j & 1) ? v11 : v10) : ((j & 1) ? v01 : v00);
-      a[kc] = (inbox && j >= 0 && j < 16) ? v : 0.0;
+      double v = 0.0;
+#pragma unroll
+      for (int nb = 0; nb < NBW; ++nb) {
+        const double v0 = __shfl_sync(0xffffffffu, z[nb][0], src), v1 = __shfl_sync(0xffffffffu, z[nb][1], src);
+        if ((j >> 3) == nb) v = (j & 1) ? v1 : v0;
+      }
+      a[kc] = (inbox && j >= 0 && j < 8 * NBW) ? v : 0.0;
     }
   } else {
     const double* wa = wA + g * kAS + kAO + kz + tig - ck;
@@ -404,7 +417,9 @@ __device__ __forceinline__ void dispatch_unit(const Args& A, const double* scb, 
   if constexpr (Cfg<MC>::KCmin <= 3) {
     if (kc == 3) return gather_unit<MC, BXY, 3>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane);
   }
-  if (kc == 4) return gather_unit<MC, BXY, 4>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane);
+  if constexpr (Cfg<MC>::KCmin <= 4) {
+    if (kc == 4) return gather_unit<MC, BXY, 4>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane);
+  }
   gather_unit<MC, BXY, 5>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane);
 }
 
@@ -421,7 +436,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   int* ctr = done + 2;                                       // next CTA unit to hand out
   int* loaded = done + 4;                                    // loaded[2]: item ordinal per buffer
   double* wts = reinterpret_cast<double*>(ctl + 48);         // [kWarps][kWarpW]
-  double* scb_all = wts + kWarps * C::kWarpW;                // [32 lanes][8]
+  double* scb_all = wts + kWarps * C::kWarpW;                // [32 lanes][kScb]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tig = lane & 3;
@@ -432,12 +447,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 #pragma unroll
     for (int kc = 0; kc < 4; ++kc)
 #pragma unroll
-      for (int nb = 0; nb < 2; ++nb) {
+      for (int nb = 0; nb < 3; ++nb) {
         const int d = 4 * kc + tig, j = 8 * nb + g;
-        scb_all[lane * 8 + 2 * kc + nb] = (d <= A.deg && j < C::W) ? A.poly[j * (A.deg + 1) + d] : 0.0;
+        scb_all[lane * kScb + 4 * kc + nb] = (d <= A.deg && j < C::W) ? A.poly[j * (A.deg + 1) + d] : 0.0;
       }
   }
-  const double* scb = scb_all + lane * 8;
+  const double* scb = scb_all + lane * kScb;
   // this CTA's k-th item: strided over the tile-ordered item list, so the
   // 148 CTAs work on neighbouring tiles at any moment and share the tiles'
   // halos through L2 (contiguous blocks per CTA measured 38% more DRAM reads)
@@ -628,12 +643,15 @@ __global__ void k_tc_items(const int32_t* __restrict__ uoff, const int32_t* __re
     items[first + j] = make_int4((int)t, u0 + j * tc::kItemUnits, min(u1, u0 + (j + 1) * tc::kItemUnits), 0);
 }
 
-bool tc_supported(int m) { return m >= 2 && m <= 7; }
+bool tc_supported(int m) { return m >= 2 && m <= 8; }
 
 void tc_tile_xy(int m, int* tx, int* ty) {
-  *tx = 4;
-  *ty = m == 7 ? 2 : 4;
+  *tx = m == 8 ? 2 : 4;
+  *ty = m == 7 ? 2 : (m == 8 ? 1 : 4);
 }
+
+// box widths the tensor-core gather takes at cutoff m (m = 8: 2 x 1 tiles hold 1 x 1 boxes only)
+int tc_max_box(int m) { return m == 8 ? 1 : 2; }
 
 int tc_tile_depth(int m) { return tc::kSZ - 2 * m; }
 
@@ -673,7 +691,7 @@ bool tc_applicable(const vfn_plan* p, const BinGeom& g) {
   int tx, ty;
   tc_tile_xy(p->m, &tx, &ty);
   return g.tile[0] == tx && g.tile[1] == ty && g.tile[2] == tz && g.box[2] == tz && g.box[0] == g.box[1] &&
-         (g.box[0] == 1 || g.box[0] == 2);
+         g.box[0] >= 1 && g.box[0] <= tc_max_box(p->m);
 }
 
 template <int MC, int BXY, int NW>
@@ -691,13 +709,19 @@ static int launch(vfn_plan* p, const tc::Args& A, cudaStream_t s) {
 
 template <int MC>
 static int launch_m(vfn_plan* p, const tc::Args& A, int bxy, cudaStream_t s) {
-  // 12-warp CTAs below ~5 points per 1x1x8 column (config 2 at 3.8; a 0.12
-  // chunk of c5 at 1.9), 16 above (a 0.38 chunk of c5 at 6.1: 66.4 -> 62.7 ms)
-  bool sparse = p->col_density < 5.0;
-  if (const char* e = std::getenv("VFN_WARPS")) sparse = std::atoi(e) == tc::kWarpsSparse;  // experiments
-  if (bxy == 1)
-    return sparse ? launch<MC, 1, tc::kWarpsSparse>(p, A, s) : launch<MC, 1, tc::kWarpsDense>(p, A, s);
-  return sparse ? launch<MC, 2, tc::kWarpsSparse>(p, A, s) : launch<MC, 2, tc::kWarpsDense>(p, A, s);
+  if constexpr (MC == 8) {
+    // the m = 8 tiles and weight tables fit next to 12 warps only, 1 x 1 boxes
+    (void)bxy;
+    return launch<8, 1, tc::kWarpsSparse>(p, A, s);
+  } else {
+    // 12-warp CTAs below ~5 points per 1x1x8 column (config 2 at 3.8; a 0.12
+    // chunk of c5 at 1.9), 16 above (a 0.38 chunk of c5 at 6.1: 66.4 -> 62.7 ms)
+    bool sparse = p->col_density < 5.0;
+    if (const char* e = std::getenv("VFN_WARPS")) sparse = std::atoi(e) == tc::kWarpsSparse;  // experiments
+    if (bxy == 1)
+      return sparse ? launch<MC, 1, tc::kWarpsSparse>(p, A, s) : launch<MC, 1, tc::kWarpsDense>(p, A, s);
+    return sparse ? launch<MC, 2, tc::kWarpsSparse>(p, A, s) : launch<MC, 2, tc::kWarpsDense>(p, A, s);
+  }
 }
 
 // Build units and items from the box offsets, then run the tensor-core gather.
@@ -758,6 +782,7 @@ int launch_tc(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t*
     case 4: return launch_m<4>(p, A, g.box[0], s);
     case 5: return launch_m<5>(p, A, g.box[0], s);
     case 7: return launch_m<7>(p, A, g.box[0], s);
+    case 8: return launch_m<8>(p, A, g.box[0], s);
     default: return launch_m<6>(p, A, g.box[0], s);
   }
 }

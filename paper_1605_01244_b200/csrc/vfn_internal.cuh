@@ -339,6 +339,7 @@ int make_grid_tmap(vfn_plan* p);
 bool tc_supported(int m);      // tensor-core gather covers this cutoff
 int tc_tile_depth(int m);     // its tile / box depth in cells (20 - 2m)
 void tc_tile_xy(int m, int* tx, int* ty);  // its tile x, y extents in cells
+int tc_max_box(int m);        // widest box it takes at this cutoff (1 or 2)
 bool tc_applicable(const vfn_plan* p, const BinGeom& g);
 // values[i] -> table.out[owner(i)][table.rows[i]] (vfn_shard.cu)
 int scatter_to_peers(const double2* values, int64_t M, const PeerTable* table_dev, cudaStream_t s);

@@ -667,9 +667,10 @@ def test_ragged_grids_many_points(vfb, offset_box, shape, sigma):
         assert l2 < 1e-13 and linf < 1e-13, (bxy, l2, linf)
 
 
-@pytest.mark.parametrize("m", [2, 3, 4, 5, 7])
+@pytest.mark.parametrize("m", [2, 3, 4, 5, 7, 8])
 def test_tensor_core_gather_other_cutoffs(vfb, offset_box, m):
-    """The tensor-core gather at m = 2, 3, 4, 5, 7 (tiles 4x4x(20-2m), 4x2x6 at m = 7): uniform
+    """The tensor-core gather at m = 2, 3, 4, 5, 7, 8 (tiles 4x4x(20-2m), 4x2x6 at m = 7,
+    2x1x4 with 1x1 boxes only at m = 8): uniform
     points plus a dense cluster (boxes with many units, every k-chunk count),
     at both box widths, against the oracle's gather on the same grid and
     against the thread-per-point gather."""
@@ -682,7 +683,7 @@ def test_tensor_core_gather_other_cutoffs(vfb, offset_box, m):
     pts = np.vstack([uni, clu])
     plan = vfb.NufftPlan(spec, vfb.NufftParams(cutoff=m, eps=0.999))
     box, tile = plan.geometry(len(pts))
-    assert tile == (4, 2 if m == 7 else 4, 20 - 2 * m)
+    assert tile == ((2, 1, 4) if m == 8 else (4, 2 if m == 7 else 4, 20 - 2 * m))
     sub = np.concatenate([rng.choice(150000, 2500, replace=False), 150000 + rng.choice(50000, 1500, replace=False)])
     grid, n, beta = O.oversampled_grid(spec.coeffs, offset_box.a, offset_box.b, 2.0, m)
     ref = O.gather_eval(grid, n, m, beta, pts[sub], offset_box.a, offset_box.b)
