@@ -50,7 +50,6 @@ constexpr int kSZ = 20;                   // staged z extent (TZ + 2m)
 constexpr int kLine = kSZ * 16;           // bytes per staged (x, y) line
 constexpr int kItemUnits = 48;            // units per work item
 constexpr int kXO = 1;                    // axes 1, 2 weight tables: entry kXO + j holds phi_j, j >= -1
-constexpr int kScb = 16;                  // weight-DMMA B fragments per lane: 4 k-chunks x 3 n-blocks (+1 pad)
 
 template <int MC>
 struct Cfg {
@@ -70,21 +69,23 @@ struct Cfg {
   static constexpr bool kShflA = MC >= 7;
   static constexpr int kAO = TZ, kAS = kShflA ? 0 : (TZ + 21) | 1;
   static constexpr int kXS = MC == 8 ? 19 : 17;   // x / y tables: j in [-1, kXS - 1)
+  static constexpr int kNB = (W + 7) / 8 > 2 ? 3 : 2;  // weight-DMMA n-blocks in the per-lane B table
+  static constexpr int kScb = 4 * kNB;                 // its doubles per lane (4 k-chunks)
   static constexpr int kWarpW = kUnitPts * (kAS + 2 * kXS);
 };
 
 size_t smem_bytes(int mc, int nw) {
-  auto f = [nw](int tile, int warpw) {
-    return (size_t)1024 + 2 * (size_t)tile + 48 + sizeof(double) * ((size_t)nw * warpw + 32 * kScb);
+  auto f = [nw](int tile, int warpw, int scb) {
+    return (size_t)1024 + 2 * (size_t)tile + 48 + sizeof(double) * ((size_t)nw * warpw + 32 * (size_t)scb);
   };
   switch (mc) {
-    case 2: return f(Cfg<2>::kTileBytes, Cfg<2>::kWarpW);
-    case 3: return f(Cfg<3>::kTileBytes, Cfg<3>::kWarpW);
-    case 4: return f(Cfg<4>::kTileBytes, Cfg<4>::kWarpW);
-    case 5: return f(Cfg<5>::kTileBytes, Cfg<5>::kWarpW);
-    case 7: return f(Cfg<7>::kTileBytes, Cfg<7>::kWarpW);
-    case 8: return f(Cfg<8>::kTileBytes, Cfg<8>::kWarpW);
-    default: return f(Cfg<6>::kTileBytes, Cfg<6>::kWarpW);
+    case 2: return f(Cfg<2>::kTileBytes, Cfg<2>::kWarpW, Cfg<2>::kScb);
+    case 3: return f(Cfg<3>::kTileBytes, Cfg<3>::kWarpW, Cfg<3>::kScb);
+    case 4: return f(Cfg<4>::kTileBytes, Cfg<4>::kWarpW, Cfg<4>::kScb);
+    case 5: return f(Cfg<5>::kTileBytes, Cfg<5>::kWarpW, Cfg<5>::kScb);
+    case 7: return f(Cfg<7>::kTileBytes, Cfg<7>::kWarpW, Cfg<7>::kScb);
+    case 8: return f(Cfg<8>::kTileBytes, Cfg<8>::kWarpW, Cfg<8>::kScb);
+    default: return f(Cfg<6>::kTileBytes, Cfg<6>::kWarpW, Cfg<6>::kScb);
   }
 }
 
@@ -208,7 +209,7 @@ __device__ __forceinline__ UnitPoints load_unit_points(const Args& A, int4 desc,
 // Per part the lane's C rows have fixed y, so the x-weights are applied per
 // tile (2 FMA per row pair) and the y-weights once at the end.  Rows past
 // the box read a clamped valid row and get weight 0.
-template <int MC, int BXY, int KC>
+template <int MC, int BXY, int KC, bool PEER>
 __device__ __forceinline__ void gather_unit(const Args& A, const double* __restrict__ scb, double* wt,
                                             unsigned tile_s, int tile, int ox, int oy, int oz,
                                             int4 desc, const UnitPoints& up, int lane) {
@@ -241,38 +242,44 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
   double* wA = wt;                              // [8][kAS]  axis 3 (absent with kShflA)
   double* wX = wt + kUnitPts * kAS;             // [8][kXS]  axis 1
   double* wY = wX + kUnitPts * kXS;             // [8][kXS]  axis 2
-  // axis-3 weights in registers (kShflA): n-block nb, column pair e
-  double z[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  double z00 = 0.0, z01 = 0.0, z10 = 0.0, z11 = 0.0;  // axis-3 weights in registers (kShflA)
+  double z20 = 0.0, z21 = 0.0;                        // third n-block (m = 8)
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     const double x1 = dl[d], x2 = x1 * x1, x4 = x2 * x2;
     double pw = tig == 0 ? 1.0 : (tig == 1 ? x1 : (tig == 2 ? x2 : x2 * x1));
-    double w[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    double w00 = 0.0, w01 = 0.0, w10 = 0.0, w11 = 0.0, w20 = 0.0, w21 = 0.0;
 #pragma unroll
     for (int kc = 0; kc < 4; ++kc) {
-      const double* c = scb + 4 * kc;  // (nb 0, nb 1 | nb 2, pad)
-      const double2 c01 = *reinterpret_cast<const double2*>(c);
-      dmma(w[0][0], w[0][1], pw, c01.x);
-      if (NBW > 1) dmma(w[1][0], w[1][1], pw, c01.y);
-      if (NBW > 2) dmma(w[2][0], w[2][1], pw, c[2]);
+      if constexpr (NBW > 2) {
+        const double* c = scb + 3 * kc;  // (nb 0, nb 1, nb 2)
+        dmma(w00, w01, pw, c[0]);
+        dmma(w10, w11, pw, c[1]);
+        dmma(w20, w21, pw, c[2]);
+      } else {
+        const double2 c = *reinterpret_cast<const double2*>(scb + 2 * kc);  // (nb 0, nb 1)
+        dmma(w00, w01, pw, c.x);
+        if (NBW > 1) dmma(w10, w11, pw, c.y);
+      }
       pw *= x4;
     }
     if (C::kShflA && d == 2) {
-#pragma unroll
-      for (int nb = 0; nb < NBW; ++nb) {
-        z[nb][0] = w[nb][0];
-        z[nb][1] = w[nb][1];
-      }
+      z00 = w00;
+      z01 = w01;
+      z10 = w10;
+      z11 = w11;
+      z20 = w20;
+      z21 = w21;
       continue;
     }
     double* row = d == 2 ? wA + g * kAS + kAO : (d == 0 ? wX : wY) + g * kXS + kXO;
-    // j = 8 nb + 2 tig + e; taps j >= W come out exactly 0 (zero
-    // coefficients) and are not stored past the tables (pre-zeroed)
-#pragma unroll
-    for (int nb = 0; nb < NBW; ++nb)
-#pragma unroll
-      for (int e = 0; e < 2; ++e)
-        if (8 * nb + 2 * tig + e < C::W) row[8 * nb + 2 * tig + e] = w[nb][e];
+    row[2 * tig] = w00;      // j = 2 tig, 2 tig + 1, 8 + 2 tig, 9 + 2 tig;
+    row[2 * tig + 1] = w01;  // j >= W come out exactly 0 (zero coefficients)
+    if (NBW > 1) {
+      row[8 + 2 * tig] = w10;
+      row[9 + 2 * tig] = w11;
+    }
+    if (NBW > 2 && tig == 0) row[16] = w20;  // m = 8: tap 16 is the third block's only one (W = 17)
   }
   __syncwarp();
   // A fragments: axis-3 weights of point g at staged depth kz + 4 kc + tig
@@ -283,11 +290,12 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
     for (int kc = 0; kc < KC; ++kc) {
       const int j = kz + 4 * kc + tig - ck;
       const int src = 4 * g + ((j & 7) >> 1);
-      double v = 0.0;
-#pragma unroll
-      for (int nb = 0; nb < NBW; ++nb) {
-        const double v0 = __shfl_sync(0xffffffffu, z[nb][0], src), v1 = __shfl_sync(0xffffffffu, z[nb][1], src);
-        if ((j >> 3) == nb) v = (j & 1) ? v1 : v0;
+      const double v00 = __shfl_sync(0xffffffffu, z00, src), v01 = __shfl_sync(0xffffffffu, z01, src);
+      const double v10 = __shfl_sync(0xffffffffu, z10, src), v11 = __shfl_sync(0xffffffffu, z11, src);
+      double v = (j & 8) ? ((j & 1) ? v11 : v10) : ((j & 1) ? v01 : v00);
+      if constexpr (NBW > 2) {
+        const double v20 = __shfl_sync(0xffffffffu, z20, src), v21 = __shfl_sync(0xffffffffu, z21, src);
+        if (j >= 16) v = (j & 1) ? v21 : v20;
       }
       a[kc] = (inbox && j >= 0 && j < 8 * NBW) ? v : 0.0;
     }
@@ -304,6 +312,11 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
   VFN_DCHECK(kXO - ci >= 0 && kXO - ci + XB <= kXS && kXO - cj >= 0 && kXO - cj + YB <= kXS);
   // the unit's K window [kz, kz + 4 KC) of staged depths holds every point's
   // stencil (staged depths ck .. ck + W - 1) and lies inside the staged tile
+#ifdef VFN_CHECKS
+  if (!(kz >= 0 && kz + 4 * KC <= kSZ && (!inbox || (ck >= kz && ck + C::W <= kz + 4 * KC))))
+    printf("unit window: m %d KC %d kz %d ck %d desc (%d, %d, %d) tile %d oz %d cell %d %d %d cnt %d g %d\n", MC, KC,
+           kz, ck, desc.x, desc.y, desc.z, tile, oz, cell[0], cell[1], cell[2], cnt, g);
+#endif
   VFN_DCHECK(kz >= 0 && kz + 4 * KC <= kSZ && (!inbox || (ck >= kz && ck + C::W <= kz + 4 * KC)));
 
   const unsigned base = tile_s + (unsigned)((kz + tig) * 16 + (X0 * C::SY + Y0) * kLine);
@@ -378,7 +391,11 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
     for (int q = 0; q < (XB + 7) / 8; ++q) {
       double cr0, cr1, ci0_, ci1_;
       tile_mma<KC>(bd + min(8 * q + g, XB - 1) * kX, a, cr0, cr1, ci0_, ci1_, tile_s, tile_s + C::kTileBytes);
-      const double w0 = wx[8 * q + 2 * tig], w1 = wx[8 * q + 2 * tig + 1];
+      // past the footprint the x weights are 0 (m = 8: the octets reach past
+      // the x table, whose rows are kXS = XB + 2 long)
+      const int xa = 8 * q + 2 * tig;
+      const double w0 = (8 * ((XB + 7) / 8) <= kXS - kXO || xa < XB) ? wx[xa] : 0.0;
+      const double w1 = (8 * ((XB + 7) / 8) <= kXS - kXO || xa + 1 < XB) ? wx[xa + 1] : 0.0;
       tr = fma(w0, cr0, fma(w1, cr1, tr));
       ti = fma(w0, ci0_, fma(w1, ci1_, ti));
     }
@@ -392,7 +409,7 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
   acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 2);
   if (valid && tig == 0) {
     const double2 v = make_double2(acc_re, acc_im);
-    if (A.peer) {
+    if constexpr (PEER) {
       // fused return exchange: the value goes straight to the rank whose
       // block the point came from (IPC-mapped peer memory over NVLink)
       const PeerTable* T = A.peer;
@@ -406,24 +423,24 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
   __syncwarp();  // the weight tables are rewritten by the next unit
 }
 
-template <int MC, int BXY>
+template <int MC, int BXY, bool PEER>
 __device__ __forceinline__ void dispatch_unit(const Args& A, const double* scb, double* wt, unsigned tile_s,
                                               int tile, int ox, int oy, int oz, int4 desc,
                                               const UnitPoints& up, int lane) {
   const int kc = (desc.y >> 4) & 7;
   if constexpr (Cfg<MC>::KCmin <= 2) {
-    if (kc == 2) return gather_unit<MC, BXY, 2>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane);
+    if (kc == 2) return gather_unit<MC, BXY, 2, PEER>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane);
   }
   if constexpr (Cfg<MC>::KCmin <= 3) {
-    if (kc == 3) return gather_unit<MC, BXY, 3>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane);
+    if (kc == 3) return gather_unit<MC, BXY, 3, PEER>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane);
   }
   if constexpr (Cfg<MC>::KCmin <= 4) {
-    if (kc == 4) return gather_unit<MC, BXY, 4>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane);
+    if (kc == 4) return gather_unit<MC, BXY, 4, PEER>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane);
   }
-  gather_unit<MC, BXY, 5>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane);
+  gather_unit<MC, BXY, 5, PEER>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane);
 }
 
-template <int MC, int BXY, int kWarps>
+template <int MC, int BXY, int kWarps, bool PEER>
 __global__ void __launch_bounds__(kWarps * 32, 1)
     k_gather_tc(const __grid_constant__ CUtensorMap tmap, const Args A) {
   using C = Cfg<MC>;
@@ -436,7 +453,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   int* ctr = done + 2;                                       // next CTA unit to hand out
   int* loaded = done + 4;                                    // loaded[2]: item ordinal per buffer
   double* wts = reinterpret_cast<double*>(ctl + 48);         // [kWarps][kWarpW]
-  double* scb_all = wts + kWarps * C::kWarpW;                // [32 lanes][kScb]
+  double* scb_all = wts + kWarps * C::kWarpW;                // [32 lanes][C::kScb]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tig = lane & 3;
@@ -447,12 +464,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 #pragma unroll
     for (int kc = 0; kc < 4; ++kc)
 #pragma unroll
-      for (int nb = 0; nb < 3; ++nb) {
+      for (int nb = 0; nb < C::kNB; ++nb) {
         const int d = 4 * kc + tig, j = 8 * nb + g;
-        scb_all[lane * kScb + 4 * kc + nb] = (d <= A.deg && j < C::W) ? A.poly[j * (A.deg + 1) + d] : 0.0;
+        scb_all[lane * C::kScb + C::kNB * kc + nb] = (d <= A.deg && j < C::W) ? A.poly[j * (A.deg + 1) + d] : 0.0;
       }
   }
-  const double* scb = scb_all + lane * kScb;
+  const double* scb = scb_all + lane * C::kScb;
   // this CTA's k-th item: strided over the tile-ordered item list, so the
   // 148 CTAs work on neighbouring tiles at any moment and share the tiles'
   // halos through L2 (contiguous blocks per CTA measured 38% more DRAM reads)
@@ -537,7 +554,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     // until the buffer's load for item kk has been issued
     while (*reinterpret_cast<volatile int*>(&loaded[b]) != kk) __nanosleep(64);
     mbar_wait(bar_s + 8 * b, (kk >> 1) & 1);
-    dispatch_unit<MC, BXY>(A, scb, wt, tile_s, tile, t0 * C::TX, t1 * C::TY, t2 * C::TZ, desc, up, lane);
+    dispatch_unit<MC, BXY, PEER>(A, scb, wt, tile_s, tile, t0 * C::TX, t1 * C::TY, t2 * C::TZ, desc, up, lane);
     if (lane == 0) {
       if (atomicAdd(&done[b], 1) == item.z - item.y - 1) {  // last unit of item kk
         done[b] = 0;
@@ -553,7 +570,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     kk = kk_n;
     up = up_n;
   }
-  if (A.peer) __threadfence_system();  // peer stores visible before the owners read
+  if constexpr (PEER) __threadfence_system();  // peer stores visible before the owners read
 }
 
 }  // namespace tc
@@ -572,11 +589,15 @@ __global__ void k_unit_counts(const int32_t* __restrict__ box_start, int64_t nbo
 }
 
 // floor(x / d) for x < 2^32, d <= 256: (x * ceil(2^40 / d)) >> 40 is exact
-// (the rounding error stays below x / 2^40 < 1/256 <= 1/d)
+// (the rounding error stays below x / 2^40 < 1/256 <= 1/d); the product
+// needs up to 72 bits, so its high word comes from __umul64hi
 struct Div {
   uint64_t inv;
   uint32_t d;
-  __host__ __device__ __forceinline__ uint32_t q(uint32_t x) const { return (uint32_t)(((uint64_t)x * inv) >> 40); }
+  __device__ __forceinline__ uint32_t q(uint32_t x) const {
+    const uint64_t lo = (uint64_t)x * inv, hi = __umul64hi((uint64_t)x, inv);
+    return (uint32_t)((hi << 24) | (lo >> 40));
+  }
 };
 static Div make_div(uint32_t d) { return Div{((uint64_t(1) << 40) + d - 1) / d, d}; }
 
@@ -694,17 +715,24 @@ bool tc_applicable(const vfn_plan* p, const BinGeom& g) {
          g.box[0] >= 1 && g.box[0] <= tc_max_box(p->m);
 }
 
-template <int MC, int BXY, int NW>
-static int launch(vfn_plan* p, const tc::Args& A, cudaStream_t s) {
+template <int MC, int BXY, int NW, bool PEER>
+static int launch_k(vfn_plan* p, const tc::Args& A, cudaStream_t s) {
   const size_t smem = tc::smem_bytes(MC, NW);
-  VFN_CUDA(cudaFuncSetAttribute(tc::k_gather_tc<MC, BXY, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  VFN_CUDA(cudaFuncSetAttribute(tc::k_gather_tc<MC, BXY, NW, PEER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  tc::k_gather_tc<MC, BXY, NW><<<nsm, NW * 32, smem, s>>>(p->tmap, A);
+  tc::k_gather_tc<MC, BXY, NW, PEER><<<nsm, NW * 32, smem, s>>>(p->tmap, A);
   VFN_CUDA(cudaGetLastError());
   return VFN_OK;
+}
+
+// the peer-store epilogue (sharded evaluates) is its own instantiation, so
+// the plain kernel carries none of its code
+template <int MC, int BXY, int NW>
+static int launch(vfn_plan* p, const tc::Args& A, cudaStream_t s) {
+  return A.peer ? launch_k<MC, BXY, NW, true>(p, A, s) : launch_k<MC, BXY, NW, false>(p, A, s);
 }
 
 template <int MC>

@@ -1131,3 +1131,27 @@ print("ok")
             radix = {M: np.load(tmp_path / f"vals_{M}.npy") for M in (70000, 1 << 20, (1 << 21) + 37)}
     for M, v in radix.items():
         np.testing.assert_array_equal(v, np.load(tmp_path / f"vals_{M}.npy"))
+
+
+def test_large_grid_bin_keys_and_units(vfb):
+    """A 512^3 oversampled grid at m = 8 (2 x 1 x 4 tiles: 2^25 boxes, bin
+    keys up to 2^26): the unit builder's multiply-shift division must stay
+    exact past 2^25 (its 72-bit product), so the tensor-core gather matches
+    the thread-per-point gather on the same grid."""
+    import torch
+
+    rng = np.random.default_rng(1900)
+    N = 256
+    coeffs = torch.complex(torch.randn((N, N, N), dtype=torch.float64, device="cuda"),
+                           torch.randn((N, N, N), dtype=torch.float64, device="cuda"))
+    box = vfb.DomainBox((-0.5, -0.5, -0.5), (0.5, 0.5, 0.5))
+    plan = vfb.NufftPlan(vfb.SpectralField(box, coeffs), vfb.NufftParams(cutoff=8, eps=1e-16))
+    pts = torch.as_tensor(rng.uniform(-0.5, 0.5, (1 << 20, 3)), device="cuda")
+    fast = plan.evaluate(pts)
+    box_, tile = plan.geometry(1 << 20)
+    assert tile == (2, 1, 4) and box_[0] == 1
+    sub = pts[: 1 << 15]
+    plan.set_gather(1)
+    ref = plan.evaluate(sub)
+    l2, linf = rel_err(fast[: 1 << 15].cpu().numpy(), ref.cpu().numpy())
+    assert l2 < 1e-13 and linf < 1e-13, (l2, linf)
