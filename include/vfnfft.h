@@ -105,9 +105,10 @@ int vfn_plan_grid(vfn_plan* plan, double* out_host);
 
 /* The bin-sort of M points (new): key[i] of input row i, and
  * perm = stable argsort(key) (sorted position -> input row).  key = (tile *
- * boxes_per_tile + box) * ceil(box_depth / 2) + (depth in box) / 2, tiles and
- * boxes row-major (vfn_plan_geometry gives box and tile sizes).  Host or
- * device buffers per on_device; keys are uint32, perm int32.             */
+ * boxes_per_tile + box) * ceil(box_depth / 2^s) + ((depth in box) >> s),
+ * tiles and boxes row-major (vfn_plan_geometry gives box and tile sizes,
+ * vfn_plan_key_shift s).  Host or device buffers per on_device; keys are
+ * uint32, perm int32.                                                     */
 int vfn_plan_bin(vfn_plan* plan, const double* points, int64_t M, uint32_t* keys,
                  int32_t* perm, int on_device, int64_t* first_bad_row, void* stream);
 
@@ -144,6 +145,9 @@ int vfn_direct_eval(int device, const int64_t nmodes[3], const double a[3], cons
  * point-independent rule for M points): the box and staging-tile sizes in
  * cells that define the bin key.                        */
 int vfn_plan_geometry(const vfn_plan* plan, int64_t M, int box_out[3], int tile_out[3]);
+/* Depth resolution of the same geometry's bin key: the key holds the cell's
+ * depth in its box shifted right by *shift_out (1: depth pairs, 0: depths). */
+int vfn_plan_key_shift(const vfn_plan* plan, int64_t M, int* shift_out);
 
 /* Gather box width in cells (0 = automatic, 1 or 2).  Values are bitwise
  * reproducible for a fixed box width; the automatic choice depends on the

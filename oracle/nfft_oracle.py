@@ -219,15 +219,16 @@ def rectilinear(coeffs: np.ndarray, a, b, coords) -> np.ndarray:
 # grouped into gather boxes of (bi, bj, bk) cells; boxes are numbered
 # row-major inside tiles of (ti, tj, tk) cells, tiles row-major over the grid
 # (the row-major convention of tube.py:50-51).  Inside a box the key keeps
-# the cell's depth pair only (c_z mod bk) // 2: key = (tile * boxes_per_tile +
-# box) * ceil(bk / 2) + depth_pair.  The permutation is a stable sort on that
+# the cell's depth (c_z mod bk) >> s only, s = 1 (depth pairs) except for
+# odd m on the tensor-core gather (s = 0): key = (tile * boxes_per_tile +
+# box) * ceil(bk / 2^s) + (depth >> s).  The permutation is a stable sort on that
 # key (precedent: the stable argsort of tube.py:125).
 # ---------------------------------------------------------------------------
 
 
-def bin_keys(points, a, b, n, box=(1, 1, 4), tile=(4, 4, 4)) -> np.ndarray:
+def bin_keys(points, a, b, n, box=(1, 1, 4), tile=(4, 4, 4), key_shift: int = 1) -> np.ndarray:
     """Sort key of every point; see the block comment above.  Inside a box the
-    key is the depth pair, so a box's points sort by depth pair."""
+    key is the depth >> key_shift (1: depth pairs), so a box's points sort by it."""
     _, l0 = nearest_cells(points, a, b, n)
     cell = l0 % np.asarray(n)
     box = np.asarray(box)
@@ -240,14 +241,14 @@ def bin_keys(points, a, b, n, box=(1, 1, 4), tile=(4, 4, 4)) -> np.ndarray:
     nbox = tile // box
     tile_id = (t[:, 0] * ntile[1] + t[:, 1]) * ntile[2] + t[:, 2]
     box_id = (inner[:, 0] * nbox[1] + inner[:, 1]) * nbox[2] + inner[:, 2]
-    slots = (int(box[2]) + 1) // 2
-    key = (tile_id * int(np.prod(nbox)) + box_id) * slots + c[:, 2] // 2
+    slots = (int(box[2]) + (1 << key_shift) - 1) >> key_shift
+    key = (tile_id * int(np.prod(nbox)) + box_id) * slots + (c[:, 2] >> key_shift)
     return key.astype(np.int64)
 
 
-def bin_permutation(points, a, b, n, box=(1, 1, 4), tile=(4, 4, 4)) -> np.ndarray:
+def bin_permutation(points, a, b, n, box=(1, 1, 4), tile=(4, 4, 4), key_shift: int = 1) -> np.ndarray:
     """Stable argsort of bin_keys: sorted position -> input row."""
-    return np.argsort(bin_keys(points, a, b, n, box, tile), kind="stable")
+    return np.argsort(bin_keys(points, a, b, n, box, tile, key_shift), kind="stable")
 
 
 def partition_keys(points, a, b, n, tile, row0: int = 0) -> np.ndarray:

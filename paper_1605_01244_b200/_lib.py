@@ -76,6 +76,7 @@ SIGNATURES = {
     ),
     "vfn_plan_set_gather": (ctypes.c_int, [_vp, ctypes.c_int]),
     "vfn_plan_set_box": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "vfn_plan_key_shift": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.POINTER(ctypes.c_int)]),
     "vfn_plan_set_graphs": (ctypes.c_int, [_vp, ctypes.c_int]),
     "vfn_plan_geometry": (
         ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int * 3, ctypes.c_int * 3]

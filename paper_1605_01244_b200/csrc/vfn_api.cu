@@ -124,7 +124,11 @@ BinGeom make_geometry(const vfn_plan* p, int bxy) {
   }
   g.boxes_per_tile = g.nbox[0] * g.nbox[1] * g.nbox[2];
   g.cells_per_box = g.box[0] * g.box[1] * g.box[2];
-  g.key_slots = (g.box[2] + 1) / 2;
+  // depth pairs unless the tensor-core gather's K window has a single spare
+  // depth for a window of W = 2m + 1 taps (odd m: W = 4 KCmin - 1), where
+  // a conservative pair span would cost a whole k-chunk
+  g.key_shift = (tc && (2 * p->m + 1) % 4 == 3) ? 0 : 1;
+  g.key_slots = (g.box[2] + (1 << g.key_shift) - 1) >> g.key_shift;
   for (int d = 0; d < 3; ++d) {
     g.tile_inv[d] = (((uint64_t)1 << 32) + (uint64_t)g.tile[d] - 1) / (uint64_t)g.tile[d];
     g.box_inv[d] = (((uint64_t)1 << 32) + (uint64_t)g.box[d] - 1) / (uint64_t)g.box[d];
@@ -508,6 +512,16 @@ int vfn_plan_decide(vfn_plan* p, int64_t M, const double* sample, int nsample, i
   (void)cells;
   *variant_out = v;
   *box_out = bxy;
+  return VFN_OK;
+}
+
+int vfn_plan_key_shift(const vfn_plan* p, int64_t M, int* shift_out) {
+  if (!p || !shift_out) return fail(VFN_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> plan_lock(p->mu);
+  const double cells = (double)p->n[0] * (double)p->n[1] * (double)p->n[2];
+  const BinGeom g = p->has_last_geom ? p->last_geom
+                                     : make_geometry(p, p->box_mode ? p->box_mode : (M >= cells ? 1 : 2));
+  *shift_out = g.key_shift;
   return VFN_OK;
 }
 

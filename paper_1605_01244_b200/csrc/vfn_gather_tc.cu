@@ -605,7 +605,7 @@ static Div make_div(uint32_t d) { return Div{((uint64_t(1) << 40) + d - 1) / d, 
 // point that opens a chunk of 8 in its box writes the unit (fully parallel,
 // also for boxes holding millions of points — config 3).
 __global__ void k_write_units(const uint32_t* __restrict__ keys, int64_t M,
-                              const int32_t* __restrict__ box_start, Div cpb, int W,
+                              const int32_t* __restrict__ box_start, Div cpb, int shift, int W,
                               int kcmin, const int32_t* __restrict__ uoff, int4* __restrict__ units) {
   const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (i0 >= M) return;
@@ -634,8 +634,9 @@ __global__ void k_write_units(const uint32_t* __restrict__ keys, int64_t M,
     if (r & (tc::kUnitPts - 1)) continue;
     const int e = min(be, (int)i + tc::kUnitPts);
     const uint32_t klast = e - 1 - i0 < 8 ? k[e - 1 - i0] : keys[e - 1];
-    // the key holds depth pairs: the unit's depths lie in [2 q0, 2 q1 + 1]
-    const int k0 = 2 * (int)(k[j] - cpb.q(k[j]) * cpb.d), k1 = 2 * (int)(klast - cpb.q(klast) * cpb.d) + 1;
+    // the key holds depth >> shift: the unit's depths lie in [q0 << s, ((q1 + 1) << s) - 1]
+    const int k0 = (int)(k[j] - cpb.q(k[j]) * cpb.d) << shift;
+    const int k1 = (((int)(klast - cpb.q(klast) * cpb.d) + 1) << shift) - 1;
     const int kc = max(kcmin, (k1 - k0 + W + 3) / 4);  // span + W <= 4 kc  (<= 20 always)
     const int kz = min(k0, tc::kSZ - 4 * kc);
     units[uoff[b] + r / tc::kUnitPts] = make_int4((int)i, (e - (int)i) | (kc << 4) | (kz << 8), (int)b, 0);
@@ -776,7 +777,8 @@ int launch_tc(vfn_plan* p, const double* u, const int32_t* perm, const uint32_t*
   VFN_CHECK(p->units.ensure(sizeof(int4) * (M + 1)));
   if (g.key_slots > 256) return fail(VFN_ERR_INVALID, "box too deep for the unit builder");
   k_write_units<<<(unsigned)(((M + 7) / 8 + 255) / 256), 256, 0, s>>>(keys_sorted, M, box_start,
-                                                                      make_div((uint32_t)g.key_slots), W, (W + 3) / 4,
+                                                                      make_div((uint32_t)g.key_slots), g.key_shift, W,
+                                                                      (W + 3) / 4,
                                                                       uoff, p->units.as<int4>());
   VFN_CUDA(cudaGetLastError());
   const unsigned tb = (unsigned)((g.ntiles + 1 + 255) / 256);

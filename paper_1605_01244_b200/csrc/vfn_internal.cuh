@@ -127,7 +127,9 @@ struct BinGeom {
   // runs; x, y inside the box and the low depth bit carry no information for
   // it), which keeps the key short enough for one radix pass fewer (c5: 24
   // bits, 3 passes of 8)
-  int key_slots;      // (box[2] + 1) / 2
+  int key_shift;      // 1: depth pairs; 0: single depths (odd m on the tensor-core gather,
+                      // where one spare depth decides the unit's k-chunk count)
+  int key_slots;      // (box[2] + 2^key_shift - 1) >> key_shift
   int64_t ntiles;
   int64_t nboxes;  // ntiles * boxes_per_tile
   // ceil(2^32 / d) for d = tile[k], box[k]: floor(x / d) = (x * inv) >> 32

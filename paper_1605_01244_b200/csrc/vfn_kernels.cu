@@ -122,9 +122,9 @@ __global__ void k_map_key(const double* __restrict__ pts, int64_t M, TorusMap tm
     atomicMin(bad, (unsigned long long)i);
     cell[0] = cell[1] = cell[2] = 0;  // any in-range key; the call fails anyway
   }
-  // key = (tile * boxes_per_tile + box) * key_slots + depth / 2, tiles and
-  // boxes row-major: a box's points come out sorted by depth pair (the
-  // gather's units are depth runs; BinGeom::key_slots)
+  // key = (tile * boxes_per_tile + box) * key_slots + (depth >> key_shift),
+  // tiles and boxes row-major: a box's points come out sorted by depth pair
+  // or depth (the gather's units are depth runs; BinGeom::key_shift)
   int t[3], in[3], c[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
@@ -137,7 +137,7 @@ __global__ void k_map_key(const double* __restrict__ pts, int64_t M, TorusMap tm
   }
   int64_t tile_id = ((int64_t)t[0] * g.ntile[1] + t[1]) * g.ntile[2] + t[2];
   int box_id = (in[0] * g.nbox[1] + in[1]) * g.nbox[2] + in[2];
-  const int slot = c[2] >> 1;
+  const int slot = c[2] >> g.key_shift;
   VFN_DCHECK(tile_id < g.ntiles && box_id < g.boxes_per_tile && slot < g.key_slots);
   keys[i] = (uint32_t)((tile_id * g.boxes_per_tile + box_id) * g.key_slots + slot);
   if (iota) iota[i] = (int32_t)i;

@@ -510,6 +510,13 @@ class NufftPlan:
         _lib.check(_lib.load().vfn_plan_geometry(self._handle, int(M), box, tile))
         return tuple(box), tuple(tile)
 
+    def key_shift(self, M: int = 0) -> int:
+        """Depth resolution of the bin key of the last evaluate/bin call (else
+        the point-independent choice for M points): 1 = depth pairs, 0 = depths."""
+        v = ctypes.c_int()
+        _lib.check(_lib.load().vfn_plan_key_shift(self._handle, int(M), ctypes.byref(v)))
+        return v.value
+
     def launch_count(self, M: int) -> int:
         """Kernels of this library one evaluate of M points launches (for M above
         CUB's single-tile sort threshold): map+key, the onesweep radix sort
@@ -525,7 +532,8 @@ class NufftPlan:
         for d in range(3):
             ntiles *= -(-self._n[d] // tile[d])
         nkeys = ntiles * (tile[0] // box[0]) * (tile[1] // box[1]) * (tile[2] // box[2])
-        nkeys *= (box[2] + 1) // 2  # key slots per box: depth pairs (include/vfnfft.h vfn_plan_bin)
+        sh = self.key_shift(M)
+        nkeys *= (box[2] + (1 << sh) - 1) >> sh  # key slots per box (include/vfnfft.h vfn_plan_bin)
         bits = max(1, int(nkeys - 1).bit_length())
         sort = 2 + 2 * -(-bits // 8)
         if 2 <= self.params.cutoff <= 7 and tile[2] == 20 - 2 * self.params.cutoff:

@@ -77,7 +77,7 @@ def test_random_configuration(vfb, seed):
     # bin keys and the stable permutation, bit-exact
     keys, perm = plan.bin(pts)
     bx, tl = plan.geometry(len(pts))
-    ref_keys = O.bin_keys(pts, a, b, plan._n, bx, tl)
+    ref_keys = O.bin_keys(pts, a, b, plan._n, bx, tl, plan.key_shift())
     np.testing.assert_array_equal(keys.astype(np.int64), ref_keys)
     np.testing.assert_array_equal(perm, np.argsort(ref_keys, kind="stable"))
 

@@ -78,7 +78,7 @@ def test_far_offset_and_tiny_boxes(vfb, a, w):
     plan = vfb.NufftPlan(spec)
     keys, perm = plan.bin(pts)
     bx, tl = plan.geometry(len(pts))
-    ref_keys = O.bin_keys(pts, a, b, plan._n, bx, tl)
+    ref_keys = O.bin_keys(pts, a, b, plan._n, bx, tl, plan.key_shift())
     np.testing.assert_array_equal(keys.astype(np.int64), ref_keys)
     np.testing.assert_array_equal(perm, np.argsort(ref_keys, kind="stable"))
     grid, n, beta = O.oversampled_grid(spec.coeffs, tuple(a), tuple(b), 2.0, 6)
@@ -98,7 +98,7 @@ def test_bin_sort_bit_exact_vs_cpu_stable_sort(vfb, offset_box):
     pts = np.vstack([g["points"], rng.uniform(g["a"], g["b"], (20000, 3))])
     keys, perm = plan.bin(pts)
     box, tile = plan.geometry(len(pts))
-    ref_keys = O.bin_keys(pts, g["a"], g["b"], plan._n, box, tile)
+    ref_keys = O.bin_keys(pts, g["a"], g["b"], plan._n, box, tile, plan.key_shift())
     np.testing.assert_array_equal(keys.astype(np.int64), ref_keys)
     np.testing.assert_array_equal(perm, np.argsort(ref_keys, kind="stable"))
 
@@ -111,7 +111,7 @@ def test_bin_sort_bit_exact_clustered(vfb):
     plan = vfb.NufftPlan(vfb.SpectralField(box, g["coeffs"]))
     keys, perm = plan.bin(g["points"])
     bx, tl = plan.geometry(len(g["points"]))
-    ref = O.bin_keys(g["points"], box.a, box.b, plan._n, bx, tl)
+    ref = O.bin_keys(g["points"], box.a, box.b, plan._n, bx, tl, plan.key_shift())
     np.testing.assert_array_equal(keys.astype(np.int64), ref)
     np.testing.assert_array_equal(perm, np.argsort(ref, kind="stable"))
 
@@ -1115,7 +1115,7 @@ for M in (70000, 1 << 20, (1 << 21) + 37):
     pts[: M // 3] = pts[0]
     keys, perm = plan.bin(pts)
     b, t = plan.geometry(M)
-    ref = O.bin_keys(pts, box.a, box.b, plan._n, b, t)
+    ref = O.bin_keys(pts, box.a, box.b, plan._n, b, t, plan.key_shift())
     assert np.array_equal(keys.astype(np.int64), ref)
     assert np.array_equal(perm, np.argsort(ref, kind="stable"))
     np.save(%r + "/vals_%%d.npy" %% M, plan.evaluate(pts))
