@@ -87,3 +87,27 @@ def test_exact_passes_ragged_gemm_shapes(vfb, offset_box, M, K):
     got = vfb.eval_rectilinear(spec, coords)
     l2, linf = rel_err(got, ref)
     assert l2 < 1e-13 and linf < 1e-13, (l2, linf)
+
+
+def test_nufft_passes_unsorted_duplicate_coordinates_and_out(vfb, offset_box):
+    """The NUFFT passes take coordinate vectors in any order, with repeats and
+    the left endpoint, host or device, and write into a caller's ``out``."""
+    import torch
+
+    spec = random_spectral(offset_box, (16, 8, 32), 1950)
+    rng = np.random.default_rng(1951)
+    coords = []
+    for d, M in enumerate((11, 7, 13)):
+        c = rng.uniform(offset_box.a[d], offset_box.b[d], M)
+        c[2] = c[5]                      # a repeat
+        c[0] = offset_box.a[d]           # the left endpoint
+        coords.append(c)                 # unsorted
+    ref = O.rectilinear(spec.coeffs, offset_box.a, offset_box.b, coords)
+    host = vfb.eval_rectilinear(spec, coords, mode="nufft")
+    assert rel_err(host, ref)[1] < 5e-12
+    out = np.empty((11, 7, 13), dtype=np.complex128)
+    assert vfb.eval_rectilinear(spec, coords, out=out, mode="nufft") is out
+    np.testing.assert_array_equal(out, host)
+    dspec = vfb.SpectralField(offset_box, torch.as_tensor(spec.coeffs, device="cuda"))
+    dev = vfb.eval_rectilinear(dspec, coords, mode="nufft")
+    np.testing.assert_array_equal(dev.cpu().numpy(), host)
