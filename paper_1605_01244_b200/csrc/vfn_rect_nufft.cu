@@ -40,14 +40,28 @@ struct Pass {
   int64_t nlines;     // A * B
   int N, n, logn, M, m, W, G, deg;
   const double* fac;  // N: (-1)^k / phihat(k) / n / sqrt(w)
-  const int* l0;      // M: nearest cell of each coordinate (mod n)
-  const double* wts;  // M x W: window weights of each coordinate
+  const int* l0;      // M: nearest cell of each coordinate (mod n), coordinates sorted
+  const double* wts;  // M x W: window weights of each coordinate (sorted order)
+  const int* perm;    // M: sorted position -> output index along the axis
+  const int2* octs;   // ceil(M/8): (window start p_lo, k-chunks) of each octet of sorted targets
+  const int* delta;   // M: target's stencil start relative to its octet's window
 };
 
-template <bool ROWS>  // ROWS: B == 1, a line is a contiguous row of X / Y
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// ROWS: B == 1, a line is a contiguous row of X / Y.  TC: the window gather
+// as DMMAs — 8 sorted targets (M) x 8 lines (N) per tile, K = the octet's
+// window — with 8 lines per CTA at a pitch of n + 4 complex (lines g and
+// g + 1 in opposite bank halves: conflict-free B fragments); else a scalar
+// 2m+1-tap loop per output (n > 1024, where 8 lines do not fit).
+template <bool ROWS, bool TC>
 __global__ void __launch_bounds__(kThreads) k_nufft_pass(const Pass P) {
   extern __shared__ __align__(16) unsigned char rsm[];
-  const int n = P.n, G = P.G, W = P.W, N = P.N, ld = n + 1;  // odd line pitch: conflict-free across lines
+  const int n = P.n, G = P.G, W = P.W, N = P.N, ld = TC ? n + 4 : n + 1;
   double2* lines = reinterpret_cast<double2*>(rsm);
   double2* tw = lines + (size_t)G * ld;                     // n/2 twiddles e^{-2 pi i t/n}
   double* wts = reinterpret_cast<double*>(tw + n / 2);      // kChunk x W window weights
@@ -128,6 +142,35 @@ __global__ void __launch_bounds__(kThreads) k_nufft_pass(const Pass P) {
     }
     __syncthreads();
   }
+  if constexpr (TC) {
+    // C[t, line] = sum_k A[t, k] G[line, p_lo + k] over the octet's window:
+    // lane (g, tig) holds A[target g][k = 4 kc + tig], B[k][line g] and
+    // C[target g][lines 2 tig, 2 tig + 1]
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, tig = lane & 3;
+    const int noct = (P.M + 7) >> 3;
+    for (int o = warp; o < noct; o += kThreads / 32) {
+      const int2 oc = P.octs[o];
+      const int t = 8 * o + g;
+      const bool vt = t < P.M;
+      const int dlt = vt ? P.delta[t] : (1 << 30);
+      const double* wt = P.wts + (int64_t)(vt ? t : 0) * W;
+      const double2* xl = lines + g * ld;
+      double r0 = 0.0, r1 = 0.0, i0 = 0.0, i1 = 0.0;
+      for (int kc = 0; kc < oc.y; ++kc) {
+        const int k = 4 * kc + tig, ow = k - dlt;
+        const double a = (ow >= 0 && ow < W) ? __ldg(wt + ow) : 0.0;
+        const double2 v = xl[(oc.x + k) & (n - 1)];
+        dmma(r0, r1, a, v.x);
+        dmma(i0, i1, a, v.y);
+      }
+      if (vt) {
+        const int64_t col = ROWS ? (int64_t)P.perm[t] : (int64_t)P.perm[t] * P.B;
+        if (2 * tig < gh) P.Y[lout[2 * tig] + col] = make_double2(r0, i0);
+        if (2 * tig + 1 < gh) P.Y[lout[2 * tig + 1] + col] = make_double2(r1, i1);
+      }
+    }
+    return;
+  } else {
   // gather: value_j = sum_o w_o(delta_j) g[(l0_j + o - m) mod n]
   for (int j0 = 0; j0 < P.M; j0 += kChunk) {
     const int nj = min(kChunk, P.M - j0);
@@ -147,7 +190,7 @@ __global__ void __launch_bounds__(kThreads) k_nufft_pass(const Pass P) {
             ai = fma(w[o], v.y, ai);
             p = p + 1 == n ? 0 : p + 1;
           }
-          P.Y[lout[g] + j0 + j] = make_double2(ar, ai);
+          P.Y[lout[g] + P.perm[j0 + j]] = make_double2(ar, ai);
         }
       }
     } else {
@@ -164,12 +207,34 @@ __global__ void __launch_bounds__(kThreads) k_nufft_pass(const Pass P) {
             ai = fma(w[o], v.y, ai);
             p = p + 1 == n ? 0 : p + 1;
           }
-          P.Y[lout[g] + (int64_t)(j0 + j) * P.B] = make_double2(ar, ai);
+          P.Y[lout[g] + (int64_t)P.perm[j0 + j] * P.B] = make_double2(ar, ai);
         }
       }
     }
     __syncthreads();
   }
+  }
+}
+
+// Octets of sorted targets: the smallest circular window holding all eight
+// stencils (start p_lo, K = 4 chunks) and each target's offset in it.
+__global__ void k_axis_octets(const int* __restrict__ l0, int M, int n, int m, int2* __restrict__ octs,
+                              int* __restrict__ delta) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (8 * o >= M) return;
+  const int t0 = 8 * o, cnt = min(8, M - t0), ref = l0[t0], h = n / 2;
+  int dmin = 0, dmax = 0, dd[8];
+  for (int t = 0; t < cnt; ++t) {
+    int d = l0[t0 + t] - ref;          // circular difference in [-n/2, n/2)
+    d = ((d + h) % n + n) % n - h;
+    dd[t] = d;
+    dmin = min(dmin, d);
+    dmax = max(dmax, d);
+  }
+  const int W = 2 * m + 1;
+  const int p_lo = (((ref + dmin - m) % n) + n) % n;
+  octs[o] = make_int2(p_lo, (dmax - dmin + W + 3) / 4);
+  for (int t = 0; t < cnt; ++t) delta[t0 + t] = dd[t] - dmin;
 }
 
 // window weights of every coordinate of one axis, W per coordinate
@@ -182,17 +247,17 @@ __global__ void k_axis_weights(const double* __restrict__ dl, int M, const doubl
 }
 
 // nearest cell and offset of every coordinate of one axis (the gather's map)
-__global__ void k_axis_targets(const double* __restrict__ y, int M, double a, double amb, int n,
-                               int* __restrict__ l0, double* __restrict__ dl) {
+__global__ void k_axis_targets(const double* __restrict__ y, const int* __restrict__ perm, int M, double a,
+                               double amb, int n, int* __restrict__ l0, double* __restrict__ dl) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= M) return;
   double d;
-  l0[j] = nearest_cell(y[j], a, amb, (double)n, n, d);
+  l0[j] = nearest_cell(y[perm[j]], a, amb, (double)n, n, d);
   dl[j] = d;
 }
 
-size_t smem_bytes(int G, int n, int W) {
-  return sizeof(double2) * ((size_t)G * (n + 1) + n / 2) + sizeof(double) * kChunk * W +
+size_t smem_bytes(int G, int n, int W, bool tc) {
+  return sizeof(double2) * ((size_t)G * (tc ? n + 4 : n + 1) + n / 2) + sizeof(double) * kChunk * W +
          sizeof(int64_t) * 2 * G + sizeof(int) * kChunk + 16;
 }
 
@@ -248,20 +313,49 @@ int rect_nufft_device(int device, const int64_t nm[3], const double a[3], const 
     }
     std::copy(coef.begin(), coef.begin() + (size_t)W * (deg + 1), h.begin() + Ntot);
   }
-  const size_t tb = sizeof(double) * (h.size() + Mtot + (size_t)Mtot * W) + sizeof(int) * (Mtot + 4);
+  // the coordinates of each axis in sorted order (the DMMA gather takes 8
+  // consecutive sorted targets per tile: their stencils overlap); the order
+  // only shapes the octets' windows, any order gives the same values
+  std::vector<int> perm_h(Mtot);
+  {
+    int64_t off = 0;
+    for (int d = 0; d < 3; ++d) {
+      std::vector<double> yh(Mv[d]);
+      VFN_CUDA(cudaMemcpyAsync(yh.data(), y[d], sizeof(double) * Mv[d], cudaMemcpyDeviceToHost, s));
+      VFN_CUDA(cudaStreamSynchronize(s));
+      int* pp = perm_h.data() + off;
+      for (int64_t j = 0; j < Mv[d]; ++j) pp[j] = (int)j;
+      std::stable_sort(pp, pp + Mv[d], [&](int u, int v) { return yh[u] < yh[v]; });
+      off += Mv[d];
+    }
+  }
+  const int64_t noct = (Mv[0] + 7) / 8 + (Mv[1] + 7) / 8 + (Mv[2] + 7) / 8;
+  const size_t tb = sizeof(double) * (h.size() + Mtot + (size_t)Mtot * W) + sizeof(int) * (3 * Mtot + 4) +
+                    sizeof(int2) * (noct + 4);
   VFN_CHECK(sc->tables.ensure(tb));
   double* dfac = sc->tables.as<double>();
   double* dpoly = dfac + Ntot;
   double* ddl = dpoly + (size_t)W * (deg + 1);
   double* dw = ddl + Mtot;
-  int* dl0 = reinterpret_cast<int*>(dw + (size_t)Mtot * W);
+  int2* doct = reinterpret_cast<int2*>(dw + (size_t)Mtot * W);
+  int* dl0 = reinterpret_cast<int*>(doct + noct + 2);
+  int* dperm = dl0 + Mtot;
+  int* ddelta = dperm + Mtot;
   VFN_CUDA(cudaMemcpyAsync(dfac, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, s));
+  VFN_CUDA(cudaMemcpyAsync(dperm, perm_h.data(), sizeof(int) * Mtot, cudaMemcpyHostToDevice, s));
+  int64_t off_o[3];
   {
-    int64_t off = 0;
+    int64_t off = 0, oo = 0;
     for (int d = 0; d < 3; ++d) {
-      rn::k_axis_targets<<<(unsigned)((Mv[d] + 255) / 256), 256, 0, s>>>(y[d], (int)Mv[d], a[d], a[d] - b[d],
-                                                                         (int)n[d], dl0 + off, ddl + off);
+      rn::k_axis_targets<<<(unsigned)((Mv[d] + 255) / 256), 256, 0, s>>>(y[d], dperm + off, (int)Mv[d], a[d],
+                                                                         a[d] - b[d], (int)n[d], dl0 + off, ddl + off);
       VFN_CUDA(cudaGetLastError());
+      off_o[d] = oo;
+      const int64_t no = (Mv[d] + 7) / 8;
+      rn::k_axis_octets<<<(unsigned)((no + 127) / 128), 128, 0, s>>>(dl0 + off, (int)Mv[d], (int)n[d], m, doct + oo,
+                                                                     ddelta + off);
+      VFN_CUDA(cudaGetLastError());
+      oo += no;
       rn::k_axis_weights<<<(unsigned)((Mv[d] * W + 255) / 256), 256, 0, s>>>(ddl + off, (int)Mv[d], dpoly, deg, W,
                                                                               dw + off * W);
       VFN_CUDA(cudaGetLastError());
@@ -285,27 +379,31 @@ int rect_nufft_device(int device, const int64_t nm[3], const double a[3], const 
     P.M = (int)Mv[d];
     P.m = m;
     P.W = W;
-    // lines per CTA: enough to amortise the twiddle / weight tables, few
+    // lines per CTA: 8 for the DMMA gather (its N), which fits up to
+    // n = 1024; else enough to amortise the twiddle / weight tables and few
     // enough for ~4 CTAs per SM (the FFT rounds are latency-bound)
+    const bool tc = n[d] <= 1024 && !std::getenv("VFN_RECT_SCALAR");
     int64_t lpc = 8;
     if (const char* e = std::getenv("VFN_RECT_LINES")) lpc = std::max(1, std::atoi(e));
-    P.G = (int)std::max<int64_t>(1, std::min<int64_t>(lpc, rn::kMaxGridElems / n[d]));
-    if (B > 1) P.G = (int)std::min<int64_t>(P.G, B);
+    P.G = tc ? 8 : (int)std::max<int64_t>(1, std::min<int64_t>(lpc, rn::kMaxGridElems / n[d]));
+    if (B > 1 && !tc) P.G = (int)std::min<int64_t>(P.G, B);
     P.deg = deg;
     P.fac = dfac + off_f[d];
     P.l0 = dl0 + off_t[d];
     P.wts = dw + off_t[d] * W;
-    const size_t smem = rn::smem_bytes(P.G, P.n, W);
+    P.perm = dperm + off_t[d];
+    P.octs = doct + off_o[d];
+    P.delta = ddelta + off_t[d];
+    const size_t smem = rn::smem_bytes(P.G, P.n, W, tc);
     const int64_t blocks = (P.nlines + P.G - 1) / P.G;
-    if (B == 1) {
-      VFN_CUDA(cudaFuncSetAttribute(rn::k_nufft_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      rn::k_nufft_pass<true><<<(unsigned)blocks, rn::kThreads, smem, s>>>(P);
-    } else {
-      VFN_CUDA(cudaFuncSetAttribute(rn::k_nufft_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      rn::k_nufft_pass<false><<<(unsigned)blocks, rn::kThreads, smem, s>>>(P);
-    }
-    VFN_CUDA(cudaGetLastError());
-    return VFN_OK;
+    auto go = [&](auto kern) -> int {
+      VFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<(unsigned)blocks, rn::kThreads, smem, s>>>(P);
+      VFN_CUDA(cudaGetLastError());
+      return VFN_OK;
+    };
+    if (B == 1) return tc ? go(rn::k_nufft_pass<true, true>) : go(rn::k_nufft_pass<true, false>);
+    return tc ? go(rn::k_nufft_pass<false, true>) : go(rn::k_nufft_pass<false, false>);
   };
   double2* T1 = sc->T1.as<double2>();
   double2* T2 = sc->T2.as<double2>();

@@ -111,3 +111,22 @@ def test_nufft_passes_unsorted_duplicate_coordinates_and_out(vfb, offset_box):
     dspec = vfb.SpectralField(offset_box, torch.as_tensor(spec.coeffs, device="cuda"))
     dev = vfb.eval_rectilinear(dspec, coords, mode="nufft")
     np.testing.assert_array_equal(dev.cpu().numpy(), host)
+
+
+@pytest.mark.parametrize("scalar", [False, True])
+def test_nufft_passes_gather_variants(vfb, offset_box, scalar, monkeypatch):
+    """The DMMA octet gather (sorted targets, 8 lines per CTA) and the scalar
+    tap loop of the NUFFT passes agree with the exact passes, with clustered,
+    sparse, unsorted and wrap-around coordinates."""
+    if scalar:
+        monkeypatch.setenv("VFN_RECT_SCALAR", "1")
+    spec = random_spectral(offset_box, (32, 16, 64), 1960)
+    rng = np.random.default_rng(1961)
+    a, b = np.asarray(offset_box.a), np.asarray(offset_box.b)
+    coords = [np.concatenate([rng.uniform(a[0], b[0], 20), a[0] + (b[0] - a[0]) * (1 - rng.uniform(0, 1e-3, 5))]),
+              rng.uniform(a[1], b[1], 3),                                   # sparse: wide octet windows
+              np.clip(rng.normal((a[2] + b[2]) / 2, 0.01, 70), a[2], np.nextafter(b[2], a[2]))]  # clustered
+    exact = vfb.eval_rectilinear(spec, coords)
+    fast = vfb.eval_rectilinear(spec, coords, mode="nufft")
+    l2, linf = rel_err(fast, exact)
+    assert l2 < 5e-12 and linf < 5e-12, (l2, linf)
