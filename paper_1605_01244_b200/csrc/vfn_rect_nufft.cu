@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kThreads) k_nufft_pass(const Pass P) {
   double2* lines = reinterpret_cast<double2*>(rsm);
   double2* tw = lines + (size_t)G * ld;                     // n/2 twiddles e^{-2 pi i t/n}
   double* wts = reinterpret_cast<double*>(tw + n / 2);      // kChunk x W window weights
-  int64_t* lin = reinterpret_cast<int64_t*>(wts + kChunk * W);  // G: line offsets into X
+  int64_t* lin = reinterpret_cast<int64_t*>(wts + (TC ? 0 : kChunk * W));  // G: line offsets into X
   int64_t* lout = lin + G;                                  // G: line offsets into Y
   int* l0s = reinterpret_cast<int*>(lout + G);              // kChunk
   const int tid = threadIdx.x;
@@ -216,6 +216,47 @@ __global__ void __launch_bounds__(kThreads) k_nufft_pass(const Pass P) {
   }
 }
 
+// perm = argsort(y) for M <= 4096 coordinates of one axis (one CTA, bitonic
+// network in shared memory, ties by index); larger M keeps the input order
+// (every order gives the same values, sorting only narrows the octets'
+// windows).
+constexpr int kSortMax = 4096;
+__global__ void __launch_bounds__(1024) k_sort_coords(const double* __restrict__ y, int M, int* __restrict__ perm) {
+  __shared__ double sy[kSortMax];
+  __shared__ int si[kSortMax];
+  if (M > kSortMax) {
+    for (int j = threadIdx.x; j < M; j += blockDim.x) perm[j] = j;
+    return;
+  }
+  int P2 = 1;
+  while (P2 < M) P2 <<= 1;
+  for (int j = threadIdx.x; j < P2; j += blockDim.x) {
+    sy[j] = j < M ? y[j] : INFINITY;
+    si[j] = j;
+  }
+  __syncthreads();
+  for (int k = 2; k <= P2; k <<= 1)
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      for (int i = threadIdx.x; i < P2; i += blockDim.x) {
+        const int l = i ^ jj;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          const double a = sy[i], b = sy[l];
+          const bool gt = a > b || (a == b && si[i] > si[l]);
+          if (gt == up) {
+            sy[i] = b;
+            sy[l] = a;
+            const int t = si[i];
+            si[i] = si[l];
+            si[l] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int j = threadIdx.x; j < M; j += blockDim.x) perm[j] = si[j];
+}
+
 // Octets of sorted targets: the smallest circular window holding all eight
 // stencils (start p_lo, K = 4 chunks) and each target's offset in it.
 __global__ void k_axis_octets(const int* __restrict__ l0, int M, int n, int m, int2* __restrict__ octs,
@@ -257,7 +298,7 @@ __global__ void k_axis_targets(const double* __restrict__ y, const int* __restri
 }
 
 size_t smem_bytes(int G, int n, int W, bool tc) {
-  return sizeof(double2) * ((size_t)G * (tc ? n + 4 : n + 1) + n / 2) + sizeof(double) * kChunk * W +
+  return sizeof(double2) * ((size_t)G * (tc ? n + 4 : n + 1) + n / 2) + (tc ? 0 : sizeof(double) * kChunk * W) +
          sizeof(int64_t) * 2 * G + sizeof(int) * kChunk + 16;
 }
 
@@ -313,22 +354,6 @@ int rect_nufft_device(int device, const int64_t nm[3], const double a[3], const 
     }
     std::copy(coef.begin(), coef.begin() + (size_t)W * (deg + 1), h.begin() + Ntot);
   }
-  // the coordinates of each axis in sorted order (the DMMA gather takes 8
-  // consecutive sorted targets per tile: their stencils overlap); the order
-  // only shapes the octets' windows, any order gives the same values
-  std::vector<int> perm_h(Mtot);
-  {
-    int64_t off = 0;
-    for (int d = 0; d < 3; ++d) {
-      std::vector<double> yh(Mv[d]);
-      VFN_CUDA(cudaMemcpyAsync(yh.data(), y[d], sizeof(double) * Mv[d], cudaMemcpyDeviceToHost, s));
-      VFN_CUDA(cudaStreamSynchronize(s));
-      int* pp = perm_h.data() + off;
-      for (int64_t j = 0; j < Mv[d]; ++j) pp[j] = (int)j;
-      std::stable_sort(pp, pp + Mv[d], [&](int u, int v) { return yh[u] < yh[v]; });
-      off += Mv[d];
-    }
-  }
   const int64_t noct = (Mv[0] + 7) / 8 + (Mv[1] + 7) / 8 + (Mv[2] + 7) / 8;
   const size_t tb = sizeof(double) * (h.size() + Mtot + (size_t)Mtot * W) + sizeof(int) * (3 * Mtot + 4) +
                     sizeof(int2) * (noct + 4);
@@ -342,11 +367,14 @@ int rect_nufft_device(int device, const int64_t nm[3], const double a[3], const 
   int* dperm = dl0 + Mtot;
   int* ddelta = dperm + Mtot;
   VFN_CUDA(cudaMemcpyAsync(dfac, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, s));
-  VFN_CUDA(cudaMemcpyAsync(dperm, perm_h.data(), sizeof(int) * Mtot, cudaMemcpyHostToDevice, s));
   int64_t off_o[3];
   {
     int64_t off = 0, oo = 0;
     for (int d = 0; d < 3; ++d) {
+      // the coordinates of each axis in sorted order (the DMMA gather takes 8
+      // consecutive sorted targets per tile: their stencils overlap)
+      rn::k_sort_coords<<<1, 1024, 0, s>>>(y[d], (int)Mv[d], dperm + off);
+      VFN_CUDA(cudaGetLastError());
       rn::k_axis_targets<<<(unsigned)((Mv[d] + 255) / 256), 256, 0, s>>>(y[d], dperm + off, (int)Mv[d], a[d],
                                                                          a[d] - b[d], (int)n[d], dl0 + off, ddl + off);
       VFN_CUDA(cudaGetLastError());
