@@ -932,7 +932,16 @@ int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* ou
     }
   }
   if (frac.empty()) {
-    if (M >= ((int64_t)1 << 27))
+    if (p->m >= 7)
+      // wide stencils: a chunk's units fill worse at the chunk's lower point
+      // density and the gather dominates the transfers, so one chunk or one
+      // short lead chunk beats the m = 6 split (c5, pinned buffers: m = 8
+      // 1746 ms with the m = 6 split, 1127 ms at 0.15/0.85, 855 ms one
+      // chunk; m = 7 461 / 353 / 383 ms).  Having the gather store values
+      // straight into pinned output instead of a D2H copy was measured too:
+      // scattered 16-byte PCIe writes took c5 m = 6 from 227 to 1282 ms.
+      frac = (p->m == 7 && M >= ((int64_t)1 << 27)) ? std::vector<double>{0.15, 0.85} : std::vector<double>{1.0};
+    else if (M >= ((int64_t)1 << 27))
       // from a timeline model (H2D 116 ms, D2H 80 ms and the measured
       // evaluate cost of a first-f fraction of c5's points, which is
       // superlinear at small f): c5 233.4 -> 226.4 ms measured
@@ -978,8 +987,13 @@ int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* ou
     if (!p->copy_stream[i]) VFN_CUDA(cudaStreamCreateWithFlags(&p->copy_stream[i], cudaStreamNonBlocking));
   }
   cudaStream_t sin = p->copy_stream[0], sout = p->copy_stream[1];
-  VFN_CHECK(p->pts.ensure(sizeof(double) * 3 * 2 * chunk));
-  VFN_CHECK(p->out.ensure(sizeof(double2) * 2 * chunk));
+  // pageable user buffers: chunk copies go through the device's pinned stager
+  // (host threads copy one piece while the DMA engine moves the previous);
+  // chunk i-1's output is staged out while chunk i computes
+  HostStager* st_in = stager_for(p, points, sizeof(double) * 3 * M);
+  HostStager* st_out = stager_for(p, out, sizeof(double2) * M);
+  VFN_CHECK(p->pts.ensure(sizeof(double) * 3 * (nc > 1 ? 2 : 1) * chunk));
+  VFN_CHECK(p->out.ensure(sizeof(double2) * (nc > 1 ? 2 : 1) * chunk));
   VFN_CHECK(p->misc.ensure(sizeof(int64_t) * (nc + 8)));
   int64_t* bad_dev = p->misc.as<int64_t>();
   std::vector<cudaEvent_t> ev(3 * nc);
@@ -1012,11 +1026,6 @@ int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* ou
     p->has_last_geom = true;
   }
   bool have_g = true;
-  // pageable user buffers: chunk copies go through the device's pinned stager
-  // (host threads copy one piece while the DMA engine moves the previous);
-  // chunk i-1's output is staged out while chunk i computes
-  HostStager* st_in = stager_for(p, points, sizeof(double) * 3 * M);
-  HostStager* st_out = stager_for(p, out, sizeof(double2) * M);
   auto stage_out = [&](int64_t j) -> int {
     const int64_t lo = lo_of[j], n = lo_of[j + 1] - lo;
     cudaStreamWaitEvent(sout, e_comp(j), 0);

@@ -840,6 +840,32 @@ def test_plans_release_device_memory(vfb, offset_box):
     assert free0 - free1 < 64 << 20, (free0 - free1) / 2**20
 
 
+@pytest.mark.parametrize("m", [6, 7, 8])
+def test_pipelined_host_path_per_cutoff(vfb, offset_box, m):
+    """The pipelined host path at m = 6 (four chunks) and m = 7, 8 (one
+    chunk): pinned output, pinned and pageable inputs, bitwise the
+    device-resident values."""
+    import torch
+
+    spec = random_spectral(offset_box, (16, 16, 16), 990 + m)
+    rng = np.random.default_rng(991 + m)
+    a, b = np.array(offset_box.a), np.array(offset_box.b)
+    M = (1 << 23) + 77
+    pts = rng.uniform(a, b, (M, 3))
+    plan = vfb.NufftPlan(spec, vfb.NufftParams(2.0, m))
+    ref = plan.evaluate(torch.as_tensor(pts, device="cuda")).cpu().numpy()
+    pin_p = torch.empty((M, 3), dtype=torch.float64, pin_memory=True)
+    pin_p.copy_(torch.as_tensor(pts))
+    out = torch.empty(M, dtype=torch.complex128, pin_memory=True).numpy()
+    for src in (pts, pin_p.numpy()):
+        out[:] = np.nan
+        plan.evaluate(src, out=out)
+        assert np.array_equal(out, ref), src is pts
+    sub = rng.choice(M, 2000, replace=False)
+    l2, linf = rel_err(ref[sub], O.nufft_eval(spec.coeffs, offset_box.a, offset_box.b, pts[sub], m=m))
+    assert l2 < 1e-12 and linf < 1e-12
+
+
 @pytest.mark.parametrize("M", [300000, (1 << 23) + 5])
 def test_pageable_and_pinned_host_buffers(vfb, offset_box, M):
     """Every mix of pageable (plain numpy, staged through pinned pieces) and
