@@ -10,7 +10,8 @@
 //   coordinate the 2m+1 window-weighted grid values around its nearest cell
 //   (:248-271, the same torus map and window polynomial fit as the gather).
 // One fused kernel per pass: a CTA stages G lines in shared memory, runs
-// the padded FFTs there (radix-2, in place, bit-reversed load) and gathers
+// the padded FFTs there (radix-2, in place, bit-reversed load, XOR-swizzled
+// line layout, per-stage twiddle tables) and gathers
 // the line's M values, so HBM sees only each pass's input and output
 // (705 MB at config 4 against 1.5e10 FMA for the exact passes).
 // Accuracy: the 3D trafo's, ~10^-(2m+1) per pass (m = 6: ~1e-13).
@@ -47,6 +48,12 @@ struct Pass {
   const int* delta;   // M: target's stencil start relative to its octet's window
 };
 
+// Element x of a staged line lives at x ^ ((x >> 3) & 7): the radix-8
+// round over contiguous groups of 8 (h = 1) then reads 8 different 16-byte
+// bank groups per 8 lanes instead of one (8-way conflicts), while the
+// later rounds and the gather's runs of 4 stay conflict-free.
+__device__ __forceinline__ int swz(int x) { return x ^ ((x >> 3) & 7); }
+
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
@@ -63,17 +70,23 @@ __global__ void __launch_bounds__(kThreads) k_nufft_pass(const Pass P) {
   extern __shared__ __align__(16) unsigned char rsm[];
   const int n = P.n, G = P.G, W = P.W, N = P.N, ld = TC ? n + 4 : n + 1;
   double2* lines = reinterpret_cast<double2*>(rsm);
-  double2* tw = lines + (size_t)G * ld;                     // n/2 twiddles e^{-2 pi i t/n}
-  double* wts = reinterpret_cast<double*>(tw + n / 2);      // kChunk x W window weights
+  double2* tw = lines + (size_t)G * ld;                     // n - 1 twiddles, per stage (below)
+  double* wts = reinterpret_cast<double*>(tw + n);          // kChunk x W window weights
   int64_t* lin = reinterpret_cast<int64_t*>(wts + (TC ? 0 : kChunk * W));  // G: line offsets into X
   int64_t* lout = lin + G;                                  // G: line offsets into Y
   int* l0s = reinterpret_cast<int*>(lout + G);              // kChunk
   const int tid = threadIdx.x;
   const int64_t L0 = (int64_t)blockIdx.x * G;
   const int gh = (int)(P.nlines - L0 < G ? P.nlines - L0 : G);
-  for (int t = tid; t < n / 2; t += kThreads) {
+  // stage of span L = 2^l: e^{-2 pi i q / L}, q < L/2, at tw[L/2 - 1 + q], so
+  // the lanes of one butterfly round read consecutive entries (a single
+  // n/2 table read at stride n/L conflicts up to 8-way).  -2q/L equals the
+  // -2 (q n/L)/n of that table exactly: the same twiddle values.
+  for (int t = tid; t < n - 1; t += kThreads) {
+    const int l = 32 - __clz(t + 1);  // L = 2^l with L/2 - 1 <= t < L - 1
+    const int q = t + 1 - (1 << (l - 1));
     double s, c;
-    sincospi(-2.0 * (double)t / (double)n, &s, &c);
+    sincospi(-2.0 * (double)q / (double)(1 << l), &s, &c);
     tw[t] = make_double2(c, s);
   }
   for (int g = tid; g < gh; g += kThreads) {
@@ -93,7 +106,7 @@ __global__ void __launch_bounds__(kThreads) k_nufft_pass(const Pass P) {
         const double2 c = P.X[lin[g] + k];
         const double f = P.fac[k];
         const int pos = k - N / 2 < 0 ? k - N / 2 + n : k - N / 2;
-        lines[g * ld + (int)(__brev((unsigned)pos) >> shift)] = make_double2(c.x * f, c.y * f);
+        lines[g * ld + swz((int)(__brev((unsigned)pos) >> shift))] = make_double2(c.x * f, c.y * f);
       }
   } else {
     // lanes along lines (consecutive b): coalesced columns
@@ -103,7 +116,7 @@ __global__ void __launch_bounds__(kThreads) k_nufft_pass(const Pass P) {
         const double2 c = P.X[lin[g] + (int64_t)k * P.B];
         const double f = P.fac[k];
         const int pos = k - N / 2 < 0 ? k - N / 2 + n : k - N / 2;
-        lines[g * ld + (int)(__brev((unsigned)pos) >> shift)] = make_double2(c.x * f, c.y * f);
+        lines[g * ld + swz((int)(__brev((unsigned)pos) >> shift))] = make_double2(c.x * f, c.y * f);
       }
   }
   __syncthreads();
@@ -117,19 +130,21 @@ __global__ void __launch_bounds__(kThreads) k_nufft_pass(const Pass P) {
     for (int it = tid; it < gh * per_line; it += kThreads) {
       const int g = it / per_line, r = it - g * per_line;
       const int j = r & (h - 1), base = (r >> (s - 1)) << (s - 1 + t);
-      double2* x = lines + g * ld + base + j;
+      double2* x = lines + g * ld;
+      const int x0 = base + j;
       double2 e[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i)
-        if (i < q) e[i] = x[i * h];
+        if (i < q) e[i] = x[swz(x0 + i * h)];
 #pragma unroll
       for (int u = 0; u < 3; ++u) {
         if (u >= t) break;
-        const int step = 1 << u, ts = n >> (s + u);
+        const int step = 1 << u;
+        const double2* twl = tw + (h << u) - 1;  // span L = 2^(s+u) = 2 h 2^u
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           if (i >= q || (i & step)) continue;
-          const double2 w = tw[(j + (i & (step - 1)) * h) * ts];
+          const double2 w = twl[j + (i & (step - 1)) * h];
           const double2 a = e[i], b = e[i + step];
           const double vr = fma(b.x, w.x, -b.y * w.y), vi = fma(b.x, w.y, b.y * w.x);
           e[i] = make_double2(a.x + vr, a.y + vi);
@@ -138,7 +153,7 @@ __global__ void __launch_bounds__(kThreads) k_nufft_pass(const Pass P) {
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i)
-        if (i < q) x[i * h] = e[i];
+        if (i < q) x[swz(x0 + i * h)] = e[i];
     }
     __syncthreads();
   }
@@ -159,7 +174,7 @@ __global__ void __launch_bounds__(kThreads) k_nufft_pass(const Pass P) {
       for (int kc = 0; kc < oc.y; ++kc) {
         const int k = 4 * kc + tig, ow = k - dlt;
         const double a = (ow >= 0 && ow < W) ? __ldg(wt + ow) : 0.0;
-        const double2 v = xl[(oc.x + k) & (n - 1)];
+        const double2 v = xl[swz((oc.x + k) & (n - 1))];
         dmma(r0, r1, a, v.x);
         dmma(i0, i1, a, v.y);
       }
@@ -185,7 +200,7 @@ __global__ void __launch_bounds__(kThreads) k_nufft_pass(const Pass P) {
           int p = l0s[j];
           double ar = 0.0, ai = 0.0;
           for (int o = 0; o < W; ++o) {
-            const double2 v = x[p];
+            const double2 v = x[swz(p)];
             ar = fma(w[o], v.x, ar);
             ai = fma(w[o], v.y, ai);
             p = p + 1 == n ? 0 : p + 1;
@@ -202,7 +217,7 @@ __global__ void __launch_bounds__(kThreads) k_nufft_pass(const Pass P) {
           int p = l0s[j];
           double ar = 0.0, ai = 0.0;
           for (int o = 0; o < W; ++o) {
-            const double2 v = x[p];
+            const double2 v = x[swz(p)];
             ar = fma(w[o], v.x, ar);
             ai = fma(w[o], v.y, ai);
             p = p + 1 == n ? 0 : p + 1;
@@ -298,7 +313,7 @@ __global__ void k_axis_targets(const double* __restrict__ y, const int* __restri
 }
 
 size_t smem_bytes(int G, int n, int W, bool tc) {
-  return sizeof(double2) * ((size_t)G * (tc ? n + 4 : n + 1) + n / 2) + (tc ? 0 : sizeof(double) * kChunk * W) +
+  return sizeof(double2) * ((size_t)G * (tc ? n + 4 : n + 1) + n) + (tc ? 0 : sizeof(double) * kChunk * W) +
          sizeof(int64_t) * 2 * G + sizeof(int) * kChunk + 16;
 }
 
@@ -426,6 +441,9 @@ int rect_nufft_device(int device, const int64_t nm[3], const double a[3], const 
     const int64_t blocks = (P.nlines + P.G - 1) / P.G;
     auto go = [&](auto kern) -> int {
       VFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      // all of L1 as shared memory: the passes are occupancy-bound (3 CTAs
+      // per SM under the default split at c4, 5 with the full carveout)
+      VFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       kern<<<(unsigned)blocks, rn::kThreads, smem, s>>>(P);
       VFN_CUDA(cudaGetLastError());
       return VFN_OK;

@@ -28,6 +28,8 @@ def vfb():
     ((8, 8, 8), (5, 300, 3), 7, 5e-13),
     ((16, 32, 16), (64, 64, 64), 4, 3e-8),  # m = 4: ~1e-9 per pass, three passes
     ((2, 4, 2), (3, 5, 4), 6, 5e-12),
+    ((4, 4, 1024), (3, 4, 50), 6, 5e-12),   # n = 2048 on axis 3: scalar gather
+    ((512, 2, 4), (40, 3, 5), 6, 5e-12),    # n = 1024 on axis 1: 8-line DMMA gather
 ])
 def test_nufft_passes_match_exact(vfb, offset_box, shape, M, m, tol):
     spec = random_spectral(offset_box, shape, 1300 + sum(M))
@@ -40,7 +42,8 @@ def test_nufft_passes_match_exact(vfb, offset_box, shape, M, m, tol):
     assert l2 < tol and linf < tol, (l2, linf)
     exact = vfb.eval_rectilinear(spec, coords)
     l2, linf = rel_err(exact, ref)
-    assert l2 < 1e-13 and linf < 1e-13, (l2, linf)
+    etol = 1e-13 if max(shape) <= 64 else 1e-12  # 1024-term axis sums: ~1e-13 rounding
+    assert l2 < etol and linf < etol, (l2, linf)
 
 
 def test_nufft_passes_config4_full(vfb):
