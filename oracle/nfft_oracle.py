@@ -18,6 +18,9 @@ to /root/reference/pkg/src/vortexfourier/.
 
 from __future__ import annotations
 
+import cmath
+import math
+
 import numpy as np
 import scipy.fft
 
@@ -195,6 +198,25 @@ def ndft(coeffs: np.ndarray, a, b, points) -> np.ndarray:
         e = [np.exp(2j * np.pi * ks[d] * t[d]) for d in range(3)]
         out[i] = np.einsum("abc,a,b,c->", coeffs, e[0], e[1], e[2]) * scale
     return out
+
+
+def series_scalar(coeffs: np.ndarray, a, b, point) -> complex:
+    """The series at one point summed term by term in plain Python complex
+    arithmetic, first axis innermost — an order independent of both the
+    tensor contraction of eval_direct (nufft.py:129-149) and the device
+    NDFT; the reference pins eval_direct against such a sum
+    (tests/oracles.py:19-33, test_nufft.py:60-67).  Small cases only."""
+    n = coeffs.shape
+    w = [float(b[d]) - float(a[d]) for d in range(3)]
+    ph = [[cmath.exp(2j * cmath.pi * (j - n[d] // 2) * (float(point[d]) - float(a[d])) / w[d])
+           for j in range(n[d])] for d in range(3)]
+    acc = 0j
+    for j3 in range(n[2]):
+        for j2 in range(n[1]):
+            e23 = ph[2][j3] * ph[1][j2]
+            for j1 in range(n[0]):
+                acc += complex(coeffs[j1, j2, j3]) * (e23 * ph[0][j1])
+    return acc / math.sqrt(w[0] * w[1] * w[2])
 
 
 def basis_matrix(a_d: float, b_d: float, nmodes: int, coords) -> np.ndarray:

@@ -294,6 +294,21 @@ def test_direct_matches_reference(vfb, i):
     assert l2 < 1e-13 and linf < 1e-13
 
 
+def test_direct_matches_scalar_series(vfb, offset_box):
+    """The device NDFT (K6) against a term-by-term scalar sum in another
+    summation order (oracle.series_scalar, after the reference's
+    tests/oracles.py:19-33), as the reference's test_nufft.py:60-67 pins
+    eval_direct."""
+    spec = random_spectral(offset_box, (12, 10, 14), 2200)
+    rng = np.random.default_rng(2201)
+    pts = rng.uniform(offset_box.a, offset_box.b, (40, 3))
+    out = vfb.eval_direct(spec, pts)
+    scale = np.abs(out).max()
+    for i in range(0, 40, 6):
+        ref = O.series_scalar(spec.coeffs, offset_box.a, offset_box.b, pts[i])
+        assert abs(out[i] - ref) <= 1e-12 * scale
+
+
 def test_rectilinear_matches_reference(vfb):
     g = golden("rect_cases.npz")
     for i in range(int(g["ncases"])):

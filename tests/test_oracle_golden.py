@@ -70,6 +70,18 @@ def test_ndft_matches_reference_direct(i):
     assert l2 < 1e-14 and linf < 1e-14
 
 
+@pytest.mark.parametrize("i", [0, 1])
+def test_scalar_series_matches_reference_direct(i):
+    """The term-by-term scalar sum (the reference's own independent oracle,
+    tests/oracles.py:19-33, restated) against the reference's eval_direct
+    values on a few points of the golden cases."""
+    c = dict(_cases())[i]
+    pts = c["points"][:: max(1, len(c["points"]) // 6)][:6]
+    ref = c["direct"][:: max(1, len(c["points"]) // 6)][:6]
+    got = np.array([O.series_scalar(c["coeffs"], c["a"], c["b"], x) for x in pts])
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(c["direct"]).max()
+
+
 def test_config1_against_reference():
     from paper_1605_01244_b200 import workloads
 
