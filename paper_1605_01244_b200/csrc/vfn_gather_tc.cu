@@ -56,10 +56,10 @@ struct Cfg {
   static_assert(MC >= 2 && MC <= 8, "tensor-core gather covers m = 2..8");
   static constexpr int W = 2 * MC + 1;            // stencil width
   static constexpr int TZ = kSZ - 2 * MC;         // tile / box depth in cells
-  // tile x, y extents in cells: 4 x 4, 4 x 2 at m = 7 and 2 x 1 at m = 8
-  // (1 x 1 boxes only) so that two staged tiles still fit next to the
-  // weight tables
-  static constexpr int TX = MC == 8 ? 2 : 4, TY = MC == 7 ? 2 : (MC == 8 ? 1 : 4);
+  // tile x, y extents in cells: 4 x 4, 4 x 2 at m = 7 and 2 x 2 at m = 8
+  // (8-warp CTAs) so that two staged tiles still fit next to the weight
+  // tables
+  static constexpr int TX = MC == 8 ? 2 : 4, TY = MC >= 7 ? 2 : 4;
   static constexpr int SX = TX + 2 * MC, SY = TY + 2 * MC;  // staged x, y extents
   static constexpr int kTileBytes = SX * SY * kLine;
   static constexpr int KCmin = (W + 3) / 4;       // fewest k-chunks a unit can use
@@ -669,11 +669,11 @@ bool tc_supported(int m) { return m >= 2 && m <= 8; }
 
 void tc_tile_xy(int m, int* tx, int* ty) {
   *tx = m == 8 ? 2 : 4;
-  *ty = m == 7 ? 2 : (m == 8 ? 1 : 4);
+  *ty = m >= 7 ? 2 : 4;
 }
 
-// box widths the tensor-core gather takes at cutoff m (m = 8: 2 x 1 tiles hold 1 x 1 boxes only)
-int tc_max_box(int m) { return m == 8 ? 1 : 2; }
+// box widths the tensor-core gather takes at cutoff m
+int tc_max_box(int m) { return m >= 2 && m <= 8 ? 2 : 1; }
 
 int tc_tile_depth(int m) { return tc::kSZ - 2 * m; }
 
@@ -739,9 +739,12 @@ static int launch(vfn_plan* p, const tc::Args& A, cudaStream_t s) {
 template <int MC>
 static int launch_m(vfn_plan* p, const tc::Args& A, int bxy, cudaStream_t s) {
   if constexpr (MC == 8) {
-    // the m = 8 tiles and weight tables fit next to 12 warps only, 1 x 1 boxes
-    (void)bxy;
-    return launch<8, 1, tc::kWarpsSparse>(p, A, s);
+    // two 18 x 18-line tiles (2 x 2 x 4 cells, up to 4 units each at c5's
+    // density) and the weight tables fit next to 8 warps: every warp has a
+    // unit while the other tile loads (2 x 1 tiles with 12 warps kept 4 of
+    // 12 warps busy: 656 ms at c5)
+    if (bxy == 1) return launch<8, 1, 8>(p, A, s);
+    return launch<8, 2, 8>(p, A, s);
   } else {
     // 12-warp CTAs below ~5 points per 1x1x8 column (config 2 at 3.8; a 0.12
     // chunk of c5 at 1.9), 16 above (a 0.38 chunk of c5 at 6.1: 66.4 -> 62.7 ms)

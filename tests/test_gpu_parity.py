@@ -685,7 +685,7 @@ def test_ragged_grids_many_points(vfb, offset_box, shape, sigma):
 @pytest.mark.parametrize("m", [2, 3, 4, 5, 7, 8])
 def test_tensor_core_gather_other_cutoffs(vfb, offset_box, m):
     """The tensor-core gather at m = 2, 3, 4, 5, 7, 8 (tiles 4x4x(20-2m), 4x2x6 at m = 7,
-    2x1x4 with 1x1 boxes only at m = 8): uniform
+    2x2x4 at m = 8): uniform
     points plus a dense cluster (boxes with many units, every k-chunk count),
     at both box widths, against the oracle's gather on the same grid and
     against the thread-per-point gather."""
@@ -698,7 +698,7 @@ def test_tensor_core_gather_other_cutoffs(vfb, offset_box, m):
     pts = np.vstack([uni, clu])
     plan = vfb.NufftPlan(spec, vfb.NufftParams(cutoff=m, eps=0.999))
     box, tile = plan.geometry(len(pts))
-    assert tile == ((2, 1, 4) if m == 8 else (4, 2 if m == 7 else 4, 20 - 2 * m))
+    assert tile == ((2, 2, 4) if m == 8 else (4, 2 if m == 7 else 4, 20 - 2 * m))
     sub = np.concatenate([rng.choice(150000, 2500, replace=False), 150000 + rng.choice(50000, 1500, replace=False)])
     grid, n, beta = O.oversampled_grid(spec.coeffs, offset_box.a, offset_box.b, 2.0, m)
     ref = O.gather_eval(grid, n, m, beta, pts[sub], offset_box.a, offset_box.b)
@@ -1175,8 +1175,8 @@ print("ok")
 
 
 def test_large_grid_bin_keys_and_units(vfb):
-    """A 512^3 oversampled grid at m = 8 (2 x 1 x 4 tiles: 2^25 boxes, bin
-    keys up to 2^26): the unit builder's multiply-shift division must stay
+    """A 512^3 oversampled grid at m = 8 (1 x 1 x 4 boxes in 2 x 2 x 4 tiles:
+    2^25 boxes, bin keys up to 2^26): the unit builder's multiply-shift division must stay
     exact past 2^25 (its 72-bit product), so the tensor-core gather matches
     the thread-per-point gather on the same grid."""
     import torch
@@ -1188,9 +1188,10 @@ def test_large_grid_bin_keys_and_units(vfb):
     box = vfb.DomainBox((-0.5, -0.5, -0.5), (0.5, 0.5, 0.5))
     plan = vfb.NufftPlan(vfb.SpectralField(box, coeffs), vfb.NufftParams(cutoff=8, eps=1e-16))
     pts = torch.as_tensor(rng.uniform(-0.5, 0.5, (1 << 20, 3)), device="cuda")
+    plan.set_box(1)
     fast = plan.evaluate(pts)
     box_, tile = plan.geometry(1 << 20)
-    assert tile == (2, 1, 4) and box_[0] == 1
+    assert tile == (2, 2, 4) and box_[0] == 1
     sub = pts[: 1 << 15]
     plan.set_gather(1)
     ref = plan.evaluate(sub)
