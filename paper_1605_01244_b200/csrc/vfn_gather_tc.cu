@@ -69,8 +69,10 @@ struct Cfg {
   static constexpr bool kShflA = MC >= 7;
   static constexpr int kAO = TZ, kAS = kShflA ? 0 : (TZ + 21) | 1;
   static constexpr int kXS = MC == 8 ? 19 : 17;   // x / y tables: j in [-1, kXS - 1)
-  static constexpr int kNB = (W + 7) / 8 > 2 ? 3 : 2;  // weight-DMMA n-blocks in the per-lane B table
-  static constexpr int kScb = 4 * kNB;                 // its doubles per lane (4 k-chunks)
+  // weight DMMA (even/odd split, see gather_unit): taps 0..MC, four per
+  // n-block as (E, O) column pairs; two k-chunks of powers of delta^2
+  static constexpr int kNB = (MC + 4) / 4;             // n-blocks in the per-lane B table
+  static constexpr int kScb = 2 * kNB;                 // its doubles per lane (2 k-chunks)
   static constexpr int kWarpW = kUnitPts * (kAS + 2 * kXS);
 };
 
@@ -234,70 +236,83 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
   const bool inbox = valid && ci0 >= 0 && ci0 < BXY && cj0 >= 0 && cj0 < BXY && ck0 >= 0 && ck0 < C::TZ;
   const int ci = inbox ? ci0 : 0, cj = inbox ? cj0 : 0, ck = inbox ? ck0 : 0;
 
-  // window weights W[p, j] = sum_d delta_p^d C[d, j] on the three axes (DMMA):
-  // 4 k-chunks of 4 powers (the fits have degree 12..14 for m <= 8), 8
-  // stencil columns per n-block
-  constexpr int NBW = (C::W + 7) / 8;
+  // window weights on the three axes (DMMA).  The window is even, so tap
+  // 2m - j is tap j's polynomial at -delta: with P_j(delta) = E_j(s) +
+  // delta O_j(s), s = delta^2, only taps j = 0..m are evaluated,
+  //   [E_j | O_j][p] = sum_k s_p^k C[k, (j, E|O)]      (K = 8 powers of s: degree <= 15),
+  // and w_j = E_j + delta O_j, w_{2m-j} = E_j - delta O_j.  Columns (E_j,
+  // O_j) sit side by side, four taps per n-block, so lane (g, tig) holds
+  // point g's taps tig and 4 + tig (and tap 8 in lane tig = 0 at m = 8):
+  // half the k-chunks and half the columns of a direct evaluation.
+  constexpr int NBW = C::kNB;
   constexpr int kXS = C::kXS;
   double* wA = wt;                              // [8][kAS]  axis 3 (absent with kShflA)
   double* wX = wt + kUnitPts * kAS;             // [8][kXS]  axis 1
   double* wY = wX + kUnitPts * kXS;             // [8][kXS]  axis 2
-  double z00 = 0.0, z01 = 0.0, z10 = 0.0, z11 = 0.0;  // axis-3 weights in registers (kShflA)
-  double z20 = 0.0, z21 = 0.0;                        // third n-block (m = 8)
+  double zp0 = 0.0, zm0 = 0.0, zp1 = 0.0, zm1 = 0.0, z2 = 0.0;  // axis-3 weights in registers (kShflA)
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    const double x1 = dl[d], x2 = x1 * x1, x4 = x2 * x2;
-    double pw = tig == 0 ? 1.0 : (tig == 1 ? x1 : (tig == 2 ? x2 : x2 * x1));
-    double w00 = 0.0, w01 = 0.0, w10 = 0.0, w11 = 0.0, w20 = 0.0, w21 = 0.0;
+    const double x1 = dl[d], s1 = x1 * x1, s2 = s1 * s1, s4 = s2 * s2;
+    double pw = tig == 0 ? 1.0 : (tig == 1 ? s1 : (tig == 2 ? s2 : s2 * s1));
+    double e0 = 0.0, o0 = 0.0, e1 = 0.0, o1 = 0.0, e2 = 0.0, o2 = 0.0;
 #pragma unroll
-    for (int kc = 0; kc < 4; ++kc) {
-      if constexpr (NBW > 2) {
+    for (int kc = 0; kc < 2; ++kc) {
+      if constexpr (NBW == 3) {
         const double* c = scb + 3 * kc;  // (nb 0, nb 1, nb 2)
-        dmma(w00, w01, pw, c[0]);
-        dmma(w10, w11, pw, c[1]);
-        dmma(w20, w21, pw, c[2]);
-      } else {
+        dmma(e0, o0, pw, c[0]);
+        dmma(e1, o1, pw, c[1]);
+        dmma(e2, o2, pw, c[2]);
+      } else if constexpr (NBW == 2) {
         const double2 c = *reinterpret_cast<const double2*>(scb + 2 * kc);  // (nb 0, nb 1)
-        dmma(w00, w01, pw, c.x);
-        if (NBW > 1) dmma(w10, w11, pw, c.y);
+        dmma(e0, o0, pw, c.x);
+        dmma(e1, o1, pw, c.y);
+      } else {
+        dmma(e0, o0, pw, scb[kc]);
       }
-      pw *= x4;
+      pw *= s4;
     }
+    const double wp0 = fma(x1, o0, e0), wm0 = fma(-x1, o0, e0);  // taps tig, 2m - tig
+    const double wp1 = fma(x1, o1, e1), wm1 = fma(-x1, o1, e1);  // taps 4 + tig, 2m - 4 - tig
     if (C::kShflA && d == 2) {
-      z00 = w00;
-      z01 = w01;
-      z10 = w10;
-      z11 = w11;
-      z20 = w20;
-      z21 = w21;
+      zp0 = wp0;
+      zm0 = wm0;
+      zp1 = wp1;
+      zm1 = wm1;
+      z2 = e2;
       continue;
     }
+    // entries j >= W of the tables stay 0 from the start of the kernel
     double* row = d == 2 ? wA + g * kAS + kAO : (d == 0 ? wX : wY) + g * kXS + kXO;
-    row[2 * tig] = w00;      // j = 2 tig, 2 tig + 1, 8 + 2 tig, 9 + 2 tig;
-    row[2 * tig + 1] = w01;  // j >= W come out exactly 0 (zero coefficients)
-    if (NBW > 1) {
-      row[8 + 2 * tig] = w10;
-      row[9 + 2 * tig] = w11;
+    if (tig <= MC) {
+      row[tig] = wp0;
+      row[2 * MC - tig] = wm0;
     }
-    if (NBW > 2 && tig == 0) row[16] = w20;  // m = 8: tap 16 is the third block's only one (W = 17)
+    if (NBW > 1 && 4 + tig <= MC) {
+      row[4 + tig] = wp1;
+      row[2 * MC - 4 - tig] = wm1;
+    }
+    if (NBW > 2 && tig == 0) row[8] = e2;  // m = 8: the centre tap (O_8 = 0)
   }
   __syncwarp();
   // A fragments: axis-3 weights of point g at staged depth kz + 4 kc + tig
   double a[KC];
   if constexpr (C::kShflA) {
-    // phi_j of point g sits in lane 4g + (j mod 8)/2, register (j / 8, j mod 2)
+    // phi_j of point g, jj = min(j, 2m - j): lane 4g + (jj mod 4), register
+    // set jj / 4, the mirrored copy for j > m
 #pragma unroll
     for (int kc = 0; kc < KC; ++kc) {
       const int j = kz + 4 * kc + tig - ck;
-      const int src = 4 * g + ((j & 7) >> 1);
-      const double v00 = __shfl_sync(0xffffffffu, z00, src), v01 = __shfl_sync(0xffffffffu, z01, src);
-      const double v10 = __shfl_sync(0xffffffffu, z10, src), v11 = __shfl_sync(0xffffffffu, z11, src);
-      double v = (j & 8) ? ((j & 1) ? v11 : v10) : ((j & 1) ? v01 : v00);
+      const bool mir = j > MC;
+      const int jj = mir ? 2 * MC - j : j;
+      const int src = 4 * g + (jj & 3);
+      const double vp0 = __shfl_sync(0xffffffffu, zp0, src), vm0 = __shfl_sync(0xffffffffu, zm0, src);
+      const double vp1 = __shfl_sync(0xffffffffu, zp1, src), vm1 = __shfl_sync(0xffffffffu, zm1, src);
+      double v = (jj & 4) ? (mir ? vm1 : vp1) : (mir ? vm0 : vp0);
       if constexpr (NBW > 2) {
-        const double v20 = __shfl_sync(0xffffffffu, z20, src), v21 = __shfl_sync(0xffffffffu, z21, src);
-        if (j >= 16) v = (j & 1) ? v21 : v20;
+        const double v2 = __shfl_sync(0xffffffffu, z2, src);
+        if (jj == 8) v = v2;
       }
-      a[kc] = (inbox && j >= 0 && j < 8 * NBW) ? v : 0.0;
+      a[kc] = (inbox && j >= 0 && j < C::W) ? v : 0.0;
     }
   } else {
     const double* wa = wA + g * kAS + kAO + kz + tig - ck;
@@ -458,15 +473,23 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tig = lane & 3;
   for (int i = tid; i < kWarps * C::kWarpW; i += blockDim.x) wts[i] = 0.0;  // zero pads
-  // B fragments of the weights DMMA, C[d = 4 kc + tig][j = 8 nb + g], per
-  // lane in shared memory (kept out of the register budget)
+  // B fragments of the weights DMMA, per lane in shared memory (kept out of
+  // the register budget): row k = 4 kc + tig is the power s^k, column 8 nb + g
+  // is tap j = 4 nb + g / 2, even part (g even: coefficient of delta^2k) or
+  // odd part (delta^(2k+1)); the fit's taps j and 2m - j are averaged into
+  // one exactly mirror-symmetric polynomial
   if (warp == 0) {
 #pragma unroll
-    for (int kc = 0; kc < 4; ++kc)
+    for (int kc = 0; kc < 2; ++kc)
 #pragma unroll
       for (int nb = 0; nb < C::kNB; ++nb) {
-        const int d = 4 * kc + tig, j = 8 * nb + g;
-        scb_all[lane * C::kScb + C::kNB * kc + nb] = (d <= A.deg && j < C::W) ? A.poly[j * (A.deg + 1) + d] : 0.0;
+        const int j = 4 * nb + (g >> 1), d = 2 * (4 * kc + tig) + (g & 1);
+        double c = 0.0;
+        if (d <= A.deg && j <= MC) {
+          const double cj = A.poly[j * (A.deg + 1) + d], cm = A.poly[(2 * MC - j) * (A.deg + 1) + d];
+          c = 0.5 * ((g & 1) ? cj - cm : cj + cm);
+        }
+        scb_all[lane * C::kScb + C::kNB * kc + nb] = c;
       }
   }
   const double* scb = scb_all + lane * C::kScb;
