@@ -942,10 +942,12 @@ int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* ou
       // scattered 16-byte PCIe writes took c5 m = 6 from 227 to 1282 ms.
       frac = (p->m == 7 && M >= ((int64_t)1 << 27)) ? std::vector<double>{0.15, 0.85} : std::vector<double>{1.0};
     else if (M >= ((int64_t)1 << 27))
-      // from a timeline model (H2D 116 ms, D2H 80 ms and the measured
-      // evaluate cost of a first-f fraction of c5's points, which is
-      // superlinear at small f): c5 233.4 -> 226.4 ms measured
-      frac = {0.06, 0.28, 0.44, 0.22};
+      // from a timeline model (H2D 117 ms, D2H 78 ms and the measured
+      // evaluate cost E(f) of a first-f fraction of c5's points, ~25 ms + 92
+      // ms f): 0.06/0.28/0.44/0.22 took c5 from 233.4 to 226.4 ms; with the
+      // low-density gather modes (half-units, weights before the tile wait)
+      // E(f) is flatter and the model's optimum moved: 217.1 -> 212.8 ms
+      frac = {0.16, 0.32, 0.40, 0.12};
     else if (M >= ((int64_t)1 << 26))
       frac = {0.12, 0.38, 0.38, 0.12};
     else if (host_column_density(p, points, M) >= 256.0)

@@ -46,6 +46,8 @@ constexpr int kUnitPts = 8;
 // dense tiles; sparse tiles (< ~5 points per 1x1x8 column, e.g. 1e6 points on
 // 128^3) have too few units per staged tile for 16 warps and run 12
 constexpr int kWarpsDense = 16, kWarpsSparse = 12;
+// half-units (SPLIT) below this many points per 1x1x8 column
+constexpr double kSplitDensity = 2.8, kSparseDensity = 4.3;
 constexpr int kSZ = 20;                   // staged z extent (TZ + 2m)
 constexpr int kLine = kSZ * 16;           // bytes per staged (x, y) line
 constexpr int kItemUnits = 48;            // units per work item
@@ -149,6 +151,12 @@ __device__ __forceinline__ double2 lds128(unsigned addr) {
   return v;
 }
 
+__device__ __forceinline__ double lds64(unsigned addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
+}
+
 // Load item `it`'s tile into the buffer at `dst` (completes on `bar`).
 template <int MC>
 __device__ __forceinline__ void issue_tile(const CUtensorMap* map, const Args& A, int it,
@@ -164,18 +172,24 @@ __device__ __forceinline__ void issue_tile(const CUtensorMap* map, const Args& A
   tma_load_3d(dst, map, 2 * t2 * Cfg<MC>::TZ, t1 * Cfg<MC>::TY, t0 * Cfg<MC>::TX, bar);
 }
 
-// One 8-row DMMA tile: C_re/im[p, n] for the lane's B row at `addr`.
-template <int KC>
+// One 8-row DMMA tile: C_re/im[p, n] for the lane's B row at `addr`.  SPLIT
+// (half-units, see k_gather_tc): `addr` points at this warp's component (re
+// or im) and only the "re" accumulators are computed.
+template <int KC, bool SPLIT>
 __device__ __forceinline__ void tile_mma(unsigned addr, const double (&a)[KC], double& cr0,
                                          double& cr1, double& ci0, double& ci1, unsigned lo,
                                          unsigned hi) {
   cr0 = cr1 = ci0 = ci1 = 0.0;
 #pragma unroll
   for (int kc = 0; kc < KC; ++kc) {
-    VFN_DCHECK(addr + kc * 64 >= lo && addr + kc * 64 + 16 <= hi);  // inside the staged tile
-    const double2 v = lds128(addr + kc * 64);
-    dmma(cr0, cr1, a[kc], v.x);
-    dmma(ci0, ci1, a[kc], v.y);
+    VFN_DCHECK(addr + kc * 64 >= lo && addr + kc * 64 + (SPLIT ? 8 : 16) <= hi);  // inside the staged tile
+    if constexpr (SPLIT) {
+      dmma(cr0, cr1, a[kc], lds64(addr + kc * 64));
+    } else {
+      const double2 v = lds128(addr + kc * 64);
+      dmma(cr0, cr1, a[kc], v.x);
+      dmma(ci0, ci1, a[kc], v.y);
+    }
   }
 }
 
@@ -202,6 +216,18 @@ __device__ __forceinline__ UnitPoints load_unit_points(const Args& A, int4 desc,
   return up;
 }
 
+// What a unit waits for before it reads its staged tile: the buffer's load
+// for item kk issued (loaded[b] == kk; the mbarrier parity only tells
+// consecutive loads apart) and completed (mbarrier phase).  gather_unit waits
+// AFTER the window weights are in place: they depend on the points only, so
+// on a sparse pass (warps outnumber the runnable units) they are computed
+// while the tile is still in flight.
+struct TileWait {
+  const int* loaded;  // &loaded[b] (shared)
+  int kk;
+  unsigned bar, parity;
+};
+
 // Row-schedule parts over the box footprint (XB x YB rows), each a run of
 // 8-row DMMA tiles whose lane -> (x, y) maps are compile-time:
 //   R8 (rows y0..y0+7, one tile per x):    B: (x, y0 + g)            C: y = y0 + 2tig + e
@@ -211,10 +237,11 @@ __device__ __forceinline__ UnitPoints load_unit_points(const Args& A, int4 desc,
 // Per part the lane's C rows have fixed y, so the x-weights are applied per
 // tile (2 FMA per row pair) and the y-weights once at the end.  Rows past
 // the box read a clamped valid row and get weight 0.
-template <int MC, int BXY, int KC, bool PEER>
+template <int MC, int BXY, int KC, bool PEER, bool SPLIT>
 __device__ __forceinline__ void gather_unit(const Args& A, const double* __restrict__ scb, double* wt,
                                             unsigned tile_s, int tile, int ox, int oy, int oz,
-                                            int4 desc, const UnitPoints& up, int lane) {
+                                            int4 desc, const UnitPoints& up, int lane, int half,
+                                            const TileWait& tw) {
   using C = Cfg<MC>;
   constexpr int XB = BXY + 2 * MC, YB = BXY + 2 * MC;  // box footprint rows per axis
   constexpr int NBY = C::TY / BXY;                     // boxes per tile along y
@@ -334,7 +361,12 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
 #endif
   VFN_DCHECK(kz >= 0 && kz + 4 * KC <= kSZ && (!inbox || (ck >= kz && ck + C::W <= kz + 4 * KC)));
 
-  const unsigned base = tile_s + (unsigned)((kz + tig) * 16 + (X0 * C::SY + Y0) * kLine);
+  while (*reinterpret_cast<const volatile int*>(tw.loaded) != tw.kk) __nanosleep(64);
+  mbar_wait(tw.bar, tw.parity);
+  // SPLIT: this warp sums one component (half = 0: re, 1: im) of the unit's
+  // values; everything named "re" below is that component, the "im" chains
+  // are dead code
+  const unsigned base = tile_s + (unsigned)((kz + tig) * 16 + (X0 * C::SY + Y0) * kLine + (SPLIT ? 8 * half : 0));
   constexpr unsigned kX = C::SY * kLine;  // x stride
   // parts of the YB rows: one R8 run per 8 rows, then R4 / R2 / R1 for the rest
   constexpr int Y8 = YB / 8;
@@ -350,7 +382,7 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
 #pragma unroll
     for (int x = 0; x < XB; ++x) {
       double cr0, cr1, ci0_, ci1_;
-      tile_mma<KC>(ba + x * kX, a, cr0, cr1, ci0_, ci1_, tile_s, tile_s + C::kTileBytes);
+      tile_mma<KC, SPLIT>(ba + x * kX, a, cr0, cr1, ci0_, ci1_, tile_s, tile_s + C::kTileBytes);
       const double w = wx[x];
       t0r = fma(w, cr0, t0r);
       t1r = fma(w, cr1, t1r);
@@ -369,7 +401,7 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
 #pragma unroll
     for (int p = 0; p < (XB + 1) / 2; ++p) {
       double cr0, cr1, ci0_, ci1_;
-      tile_mma<KC>(bb + min(2 * p + xb, XB - 1) * kX, a, cr0, cr1, ci0_, ci1_, tile_s, tile_s + C::kTileBytes);
+      tile_mma<KC, SPLIT>(bb + min(2 * p + xb, XB - 1) * kX, a, cr0, cr1, ci0_, ci1_, tile_s, tile_s + C::kTileBytes);
       const double w = wx[2 * p + xc];
       t0r = fma(w, cr0, t0r);
       t1r = fma(w, cr1, t1r);
@@ -387,7 +419,7 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
 #pragma unroll
     for (int q = 0; q < (XB + 3) / 4; ++q) {
       double cr0, cr1, ci0_, ci1_;
-      tile_mma<KC>(bc + min(4 * q + (g >> 1), XB - 1) * kX, a, cr0, cr1, ci0_, ci1_, tile_s, tile_s + C::kTileBytes);
+      tile_mma<KC, SPLIT>(bc + min(4 * q + (g >> 1), XB - 1) * kX, a, cr0, cr1, ci0_, ci1_, tile_s, tile_s + C::kTileBytes);
       const double w = wx[4 * q + tig];
       t0r = fma(w, cr0, t0r);
       t1r = fma(w, cr1, t1r);
@@ -405,7 +437,7 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
 #pragma unroll
     for (int q = 0; q < (XB + 7) / 8; ++q) {
       double cr0, cr1, ci0_, ci1_;
-      tile_mma<KC>(bd + min(8 * q + g, XB - 1) * kX, a, cr0, cr1, ci0_, ci1_, tile_s, tile_s + C::kTileBytes);
+      tile_mma<KC, SPLIT>(bd + min(8 * q + g, XB - 1) * kX, a, cr0, cr1, ci0_, ci1_, tile_s, tile_s + C::kTileBytes);
       // past the footprint the x weights are 0 (m = 8: the octets reach past
       // the x table, whose rows are kXS = XB + 2 long)
       const int xa = 8 * q + 2 * tig;
@@ -419,9 +451,9 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
     acc_im = fma(wy0, ti, acc_im);
   }
   acc_re += __shfl_xor_sync(0xffffffffu, acc_re, 1);
-  acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 1);
+  if constexpr (!SPLIT) acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 1);
   acc_re += __shfl_xor_sync(0xffffffffu, acc_re, 2);
-  acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 2);
+  if constexpr (!SPLIT) acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 2);
   if (valid && tig == 0) {
     const double2 v = make_double2(acc_re, acc_im);
     if constexpr (PEER) {
@@ -430,32 +462,48 @@ __device__ __forceinline__ void gather_unit(const Args& A, const double* __restr
       const PeerTable* T = A.peer;
       int o = 0;
       while (o + 1 < T->n && prow >= T->off[o + 1]) ++o;
-      T->out[o][T->rows[prow]] = v;
+      if constexpr (SPLIT)
+        reinterpret_cast<double*>(T->out[o] + T->rows[prow])[half] = acc_re;
+      else
+        T->out[o][T->rows[prow]] = v;
     } else {
-      __stcs(A.out + prow, v);
+      if constexpr (SPLIT)
+        __stcs(reinterpret_cast<double*>(A.out + prow) + half, acc_re);
+      else
+        __stcs(A.out + prow, v);
     }
   }
   __syncwarp();  // the weight tables are rewritten by the next unit
 }
 
-template <int MC, int BXY, bool PEER>
+template <int MC, int BXY, bool PEER, bool SPLIT>
 __device__ __forceinline__ void dispatch_unit(const Args& A, const double* scb, double* wt, unsigned tile_s,
                                               int tile, int ox, int oy, int oz, int4 desc,
-                                              const UnitPoints& up, int lane) {
+                                              const UnitPoints& up, int lane, int half, const TileWait& tw) {
   const int kc = (desc.y >> 4) & 7;
   if constexpr (Cfg<MC>::KCmin <= 2) {
-    if (kc == 2) return gather_unit<MC, BXY, 2, PEER>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane);
+    if (kc == 2)
+      return gather_unit<MC, BXY, 2, PEER, SPLIT>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane, half, tw);
   }
   if constexpr (Cfg<MC>::KCmin <= 3) {
-    if (kc == 3) return gather_unit<MC, BXY, 3, PEER>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane);
+    if (kc == 3)
+      return gather_unit<MC, BXY, 3, PEER, SPLIT>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane, half, tw);
   }
   if constexpr (Cfg<MC>::KCmin <= 4) {
-    if (kc == 4) return gather_unit<MC, BXY, 4, PEER>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane);
+    if (kc == 4)
+      return gather_unit<MC, BXY, 4, PEER, SPLIT>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane, half, tw);
   }
-  gather_unit<MC, BXY, 5, PEER>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane);
+  gather_unit<MC, BXY, 5, PEER, SPLIT>(A, scb, wt, tile_s, tile, ox, oy, oz, desc, up, lane, half, tw);
 }
 
-template <int MC, int BXY, int kWarps, bool PEER>
+// SPLIT (low-density passes): every unit is handed out twice, once from each
+// of two CTA counters — even warps take units from the first and sum the
+// real parts, odd warps from the second and sum the imaginary parts.  The
+// two components never mix in the contraction, so each value's bits are
+// those of the unsplit kernel; a sparse tile's few units then occupy twice
+// as many warps for half as long (the pass is bound by units in flight x
+// unit latency, DESIGN 4).
+template <int MC, int BXY, int kWarps, bool PEER, bool SPLIT>
 __global__ void __launch_bounds__(kWarps * 32, 1)
     k_gather_tc(const __grid_constant__ CUtensorMap tmap, const Args A) {
   using C = Cfg<MC>;
@@ -465,7 +513,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   const unsigned bar_s = tiles_s + 2 * C::kTileBytes;       // full[2]
   unsigned char* ctl = smem_raw + (bar_s - raw);
   int* done = reinterpret_cast<int*>(ctl + 16);              // done[2]
-  int* ctr = done + 2;                                       // next CTA unit to hand out
+  int* ctr = done + 2;                                       // next CTA unit to hand out (ctr[half] with SPLIT)
   int* loaded = done + 4;                                    // loaded[2]: item ordinal per buffer
   double* wts = reinterpret_cast<double*>(ctl + 48);         // [kWarps][kWarpW]
   double* scb_all = wts + kWarps * C::kWarpW;                // [32 lanes][C::kScb]
@@ -505,7 +553,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     mbar_init(bar_s, 1);
     mbar_init(bar_s + 8, 1);
     done[0] = done[1] = 0;
-    ctr[0] = 0;
+    ctr[0] = ctr[1] = 0;
     loaded[0] = 0;
     loaded[1] = 1;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -550,9 +598,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       walk.item = itn < nitems ? A.items[itn] : make_int4(0, 0, 0, 0);
     }
   };
+  const int half = SPLIT ? (warp & 1) : 0;
   auto grab = [&]() {
     int v = 0;
-    if (lane == 0) v = atomicAdd(ctr, 1);
+    if (lane == 0) v = atomicAdd(ctr + half, 1);
     return __shfl_sync(0xffffffffu, v, 0);
   };
   int4 desc, item;
@@ -572,14 +621,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     const int t1 = (tile / G.ntile[2]) % G.ntile[1];
     const int t0 = tile / (G.ntile[2] * G.ntile[1]);
     const unsigned tile_s = tiles_s + b * C::kTileBytes;
-    // a warp may hold units of items far ahead (small items): the buffer's
-    // mbarrier parity only distinguishes consecutive loads, so first wait
-    // until the buffer's load for item kk has been issued
-    while (*reinterpret_cast<volatile int*>(&loaded[b]) != kk) __nanosleep(64);
-    mbar_wait(bar_s + 8 * b, (kk >> 1) & 1);
-    dispatch_unit<MC, BXY, PEER>(A, scb, wt, tile_s, tile, t0 * C::TX, t1 * C::TY, t2 * C::TZ, desc, up, lane);
+    // a warp may hold units of items far ahead (small items); the unit waits
+    // for its tile once its weights are computed (TileWait)
+    const TileWait tw{&loaded[b], kk, bar_s + 8 * b, (unsigned)((kk >> 1) & 1)};
+    dispatch_unit<MC, BXY, PEER, SPLIT>(A, scb, wt, tile_s, tile, t0 * C::TX, t1 * C::TY, t2 * C::TZ, desc, up, lane,
+                                        half, tw);
     if (lane == 0) {
-      if (atomicAdd(&done[b], 1) == item.z - item.y - 1) {  // last unit of item kk
+      if (atomicAdd(&done[b], 1) == (SPLIT ? 2 : 1) * (item.z - item.y) - 1) {  // last (half-)unit of item kk
         done[b] = 0;
         if (item_of(kk + 2) < nitems) {
           *reinterpret_cast<volatile int*>(&loaded[b]) = kk + 2;
@@ -739,24 +787,24 @@ bool tc_applicable(const vfn_plan* p, const BinGeom& g) {
          g.box[0] >= 1 && g.box[0] <= tc_max_box(p->m);
 }
 
-template <int MC, int BXY, int NW, bool PEER>
+template <int MC, int BXY, int NW, bool PEER, bool SPLIT>
 static int launch_k(vfn_plan* p, const tc::Args& A, cudaStream_t s) {
   const size_t smem = tc::smem_bytes(MC, NW);
-  VFN_CUDA(cudaFuncSetAttribute(tc::k_gather_tc<MC, BXY, NW, PEER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
+  VFN_CUDA(cudaFuncSetAttribute(tc::k_gather_tc<MC, BXY, NW, PEER, SPLIT>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  tc::k_gather_tc<MC, BXY, NW, PEER><<<nsm, NW * 32, smem, s>>>(p->tmap, A);
+  tc::k_gather_tc<MC, BXY, NW, PEER, SPLIT><<<nsm, NW * 32, smem, s>>>(p->tmap, A);
   VFN_CUDA(cudaGetLastError());
   return VFN_OK;
 }
 
 // the peer-store epilogue (sharded evaluates) is its own instantiation, so
 // the plain kernel carries none of its code
-template <int MC, int BXY, int NW>
+template <int MC, int BXY, int NW, bool SPLIT>
 static int launch(vfn_plan* p, const tc::Args& A, cudaStream_t s) {
-  return A.peer ? launch_k<MC, BXY, NW, true>(p, A, s) : launch_k<MC, BXY, NW, false>(p, A, s);
+  return A.peer ? launch_k<MC, BXY, NW, true, SPLIT>(p, A, s) : launch_k<MC, BXY, NW, false, SPLIT>(p, A, s);
 }
 
 template <int MC>
@@ -766,16 +814,25 @@ static int launch_m(vfn_plan* p, const tc::Args& A, int bxy, cudaStream_t s) {
     // density) and the weight tables fit next to 8 warps: every warp has a
     // unit while the other tile loads (2 x 1 tiles with 12 warps kept 4 of
     // 12 warps busy: 656 ms at c5)
-    if (bxy == 1) return launch<8, 1, 8>(p, A, s);
-    return launch<8, 2, 8>(p, A, s);
+    if (bxy == 1) return launch<8, 1, 8, false>(p, A, s);
+    return launch<8, 2, 8, false>(p, A, s);
   } else {
-    // 12-warp CTAs below ~5 points per 1x1x8 column (config 2 at 3.8; a 0.12
-    // chunk of c5 at 1.9), 16 above (a 0.38 chunk of c5 at 6.1: 66.4 -> 62.7 ms)
-    bool sparse = p->col_density < 5.0;
-    if (const char* e = std::getenv("VFN_WARPS")) sparse = std::atoi(e) == tc::kWarpsSparse;  // experiments
+    // by points per 1x1x8 column (c5: 16): 16-warp CTAs from 4.3 up (a 0.28
+    // chunk of c5 at 4.5: 45.4 ms against 46.9 with 12 warps), 12-warp CTAs
+    // from 2.8 (config 2 at 3.8; a 0.22 chunk at 3.5: 39.1 against 48.6 ms),
+    // half-units on 16 warps below (a 0.15 chunk at 2.4: 35.0 against 37.6 ms,
+    // a 0.06 chunk at 1.0: 26.3 against 29.6 ms)
+    int mode = p->col_density < tc::kSplitDensity ? 2 : (p->col_density < tc::kSparseDensity ? 1 : 0);
+    if (const char* e = std::getenv("VFN_WARPS")) {  // experiments: 16, 12, or s16 (half-units)
+      mode = e[0] == 's' ? 2 : (std::atoi(e) == tc::kWarpsSparse ? 1 : 0);
+    }
+    if (mode == 2)
+      return bxy == 1 ? launch<MC, 1, tc::kWarpsDense, true>(p, A, s) : launch<MC, 2, tc::kWarpsDense, true>(p, A, s);
     if (bxy == 1)
-      return sparse ? launch<MC, 1, tc::kWarpsSparse>(p, A, s) : launch<MC, 1, tc::kWarpsDense>(p, A, s);
-    return sparse ? launch<MC, 2, tc::kWarpsSparse>(p, A, s) : launch<MC, 2, tc::kWarpsDense>(p, A, s);
+      return mode == 1 ? launch<MC, 1, tc::kWarpsSparse, false>(p, A, s)
+                       : launch<MC, 1, tc::kWarpsDense, false>(p, A, s);
+    return mode == 1 ? launch<MC, 2, tc::kWarpsSparse, false>(p, A, s)
+                     : launch<MC, 2, tc::kWarpsDense, false>(p, A, s);
   }
 }
 
