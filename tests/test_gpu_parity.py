@@ -233,6 +233,41 @@ def test_batch_composition_invariance(vfb, offset_box):
     np.testing.assert_array_equal(plan.evaluate(pts[sel]), fulls[1][sel])  # 5000 <= WARP_MAX_M
 
 
+@pytest.mark.parametrize("m", [2, 4, 5, 6, 7])
+def test_gather_density_modes_are_bitwise_equal(vfb, offset_box, m, monkeypatch):
+    """The tensor-core gather picks its CTA shape from the point density:
+    16 warps, 12 warps, or half-units (even warps sum the real parts of a
+    unit, odd warps the imaginary parts; vfn_gather_tc.cu SPLIT).  A value's
+    bits must not depend on the mode (nufft.py:264-271 sums each point on its
+    own), at both box widths and for sparse and dense sets."""
+    spec = random_spectral(offset_box, (20, 16, 24), 93)
+    rng = np.random.default_rng(94)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        plan = vfb.NufftPlan(spec, vfb.NufftParams(cutoff=m, eps=0.999))
+    plan.set_graphs(False)  # the mode is read per launch; a replayed graph would keep the first one
+    plan.set_gather(2)
+    w = np.asarray(offset_box.b) - np.asarray(offset_box.a)
+    sets = {
+        "sparse": rng.uniform(offset_box.a, offset_box.b, (40000, 3)),
+        "dense": np.asarray(offset_box.a) + w * (0.4 + 0.05 * rng.random((60000, 3))),
+    }
+    for name, pts in sets.items():
+        for box in (1, 2):
+            plan.set_box(box)
+            outs = []
+            for mode in ("16", "12", "s16"):
+                monkeypatch.setenv("VFN_WARPS", mode)
+                outs.append(plan.evaluate(pts))
+            monkeypatch.delenv("VFN_WARPS")
+            auto = plan.evaluate(pts)
+            for o in outs[1:] + [auto]:
+                np.testing.assert_array_equal(o, outs[0], err_msg=f"{name} box {box}")
+    ref = vfb.eval_direct(spec, sets["sparse"][:200])
+    l2, linf = rel_err(plan.evaluate(sets["sparse"])[:200], ref)
+    assert linf < {2: 1e-3, 4: 1e-7, 5: 1e-9, 6: 1e-11, 7: 1e-12}[m], (l2, linf)
+
+
 def test_torch_cuda_tensors_match_numpy(vfb, offset_box):
     import torch
 
