@@ -47,7 +47,7 @@ constexpr int kUnitPts = 8;
 // 128^3) have too few units per staged tile for 16 warps and run 12
 constexpr int kWarpsDense = 16, kWarpsSparse = 12;
 // half-units (SPLIT) below this many points per 1x1x8 column
-constexpr double kSplitDensity = 2.8, kSparseDensity = 4.3;
+constexpr double kSplitDensity = 1.7, kSparseDensity = 4.8;
 constexpr int kSZ = 20;                   // staged z extent (TZ + 2m)
 constexpr int kLine = kSZ * 16;           // bytes per staged (x, y) line
 constexpr int kItemUnits = 48;            // units per work item
@@ -613,8 +613,21 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     int4 desc_n, item_n;
     int kk_n = 0;
     UnitPoints up_n;
-    const bool have_n = locate(grab(), desc_n, kk_n, item_n);
-    if (have_n) up_n = load_unit_points(A, desc_n, g);
+    // Dense tiles: the next unit is reserved and its points prefetched before
+    // the current one is computed (its descriptor -> permutation -> u loads
+    // hide behind ~16k cycles of DMMAs).  Sparse modes bind late instead: a
+    // warp takes its next unit only when it is free, because a unit reserved
+    // early sits behind its warp's current one while other warps idle (few
+    // units per staged tile), and the load round trips overlap the wait for
+    // the tile anyway (c5 chunks of 0.06 / 0.16 / 0.22: 26.3 / 36 / 39.0 ->
+    // 23.3 / 32.9 / 37.8 ms, config 2 0.675 -> 0.652 ms; dense c5 would lose:
+    // 127.8 -> 131.4 ms)
+    constexpr bool kLate = (kWarps == kWarpsSparse) || SPLIT;
+    bool have_n = false;
+    if constexpr (!kLate) {
+      have_n = locate(grab(), desc_n, kk_n, item_n);
+      if (have_n) up_n = load_unit_points(A, desc_n, g);
+    }
     const int b = kk & 1;
     const int tile = item.x;
     const int t2 = tile % G.ntile[2];
@@ -634,6 +647,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
           issue_tile<MC>(&tmap, A, item_of(kk + 2), tile_s, bar_s + 8 * b);
         }
       }
+    }
+    if constexpr (kLate) {
+      have_n = locate(grab(), desc_n, kk_n, item_n);
+      if (have_n) up_n = load_unit_points(A, desc_n, g);
     }
     have = have_n;
     desc = desc_n;
@@ -817,11 +834,11 @@ static int launch_m(vfn_plan* p, const tc::Args& A, int bxy, cudaStream_t s) {
     if (bxy == 1) return launch<8, 1, 8, false>(p, A, s);
     return launch<8, 2, 8, false>(p, A, s);
   } else {
-    // by points per 1x1x8 column (c5: 16): 16-warp CTAs from 4.3 up (a 0.28
-    // chunk of c5 at 4.5: 45.4 ms against 46.9 with 12 warps), 12-warp CTAs
-    // from 2.8 (config 2 at 3.8; a 0.22 chunk at 3.5: 39.1 against 48.6 ms),
-    // half-units on 16 warps below (a 0.15 chunk at 2.4: 35.0 against 37.6 ms,
-    // a 0.06 chunk at 1.0: 26.3 against 29.6 ms)
+    // by points per 1x1x8 column (c5: 16), measured on chunks of c5: 16-warp
+    // CTAs with prefetch from 4.8 up (a 0.32 chunk at 5.1: 48.0 ms against
+    // 49.1 with 12 warps), 12-warp CTAs binding late from 1.7 (config 2 at
+    // 3.8; a 0.22 chunk at 3.5: 37.8 against 45.3 ms with half-units),
+    // half-units on 16 warps below (a 0.06 chunk at 1.0: 23.3 against 26.5 ms)
     int mode = p->col_density < tc::kSplitDensity ? 2 : (p->col_density < tc::kSparseDensity ? 1 : 0);
     if (const char* e = std::getenv("VFN_WARPS")) {  // experiments: 16, 12, or s16 (half-units)
       mode = e[0] == 's' ? 2 : (std::atoi(e) == tc::kWarpsSparse ? 1 : 0);
