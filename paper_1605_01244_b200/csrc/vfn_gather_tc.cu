@@ -621,8 +621,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     // units per staged tile), and the load round trips overlap the wait for
     // the tile anyway (c5 chunks of 0.06 / 0.16 / 0.22: 26.3 / 36 / 39.0 ->
     // 23.3 / 32.9 / 37.8 ms, config 2 0.675 -> 0.652 ms; dense c5 would lose:
-    // 127.8 -> 131.4 ms)
-    constexpr bool kLate = (kWarps == kWarpsSparse) || SPLIT;
+    // 127.8 -> 131.4 ms).  The wide stencils' small tiles hold few units at
+    // any density (m = 8: 2 x 2 x 4 cells, ~4 units at c5), so they bind late
+    // too: c5 at m = 8 365 -> 318 ms, m = 7 165.1 -> 163.8 ms
+    constexpr bool kLate = (kWarps == kWarpsSparse) || SPLIT || MC >= 7;
     bool have_n = false;
     if constexpr (!kLate) {
       have_n = locate(grab(), desc_n, kk_n, item_n);
