@@ -475,6 +475,7 @@ def run_ours(args):
             "h2d_bytes_per_step": int(total_points * 24),
             "d2h_bytes_per_step": int(total_points * 16),
             "ms_per_step": e2e_step_ms,
+            "steps_ms": [round(x, 3) for x in e2e_ms],  # this rank's timed host-buffer evaluates (the mean is reported)
             "matches_device_result_bitwise": same,
             "pinned_host_buffers": pinned,
         },
