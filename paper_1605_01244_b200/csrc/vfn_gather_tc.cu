@@ -604,14 +604,16 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     if (lane == 0) v = atomicAdd(ctr + half, 1);
     return __shfl_sync(0xffffffffu, v, 0);
   };
-  // Narrow stencils on dense tiles (m <= 3: a unit is ~30-60 DMMAs, far
-  // shorter than the DRAM round trips of its descriptor -> permutation -> u
-  // loads): a three-stage software pipeline per warp, so that no load is
-  // waited for in the iteration that issued it — while unit n is computed,
-  // unit n+1's u values, unit n+2's permutation entries and unit n+3's
-  // descriptor are in flight (c5 at m = 2: 61.9 -> 49.2 ms, m = 3: 46.2 ->
-  // 42.4 ms; from m = 5 on it gains nothing and m >= 7 spills)
-  if constexpr (MC <= 3 && kWarps == kWarpsDense && !SPLIT) {
+  // Narrow stencils on dense tiles (m <= 5: a unit is 30-130 DMMAs, shorter
+  // than or close to the DRAM round trips of its descriptor -> permutation
+  // -> u loads): a three-stage software pipeline per warp, so that no load
+  // is waited for in the iteration that issued it — while unit n is
+  // computed, unit n+1's u values, unit n+2's permutation entries and unit
+  // n+3's descriptor are in flight (c5 gathers at m = 2 / 3 / 4 / 5: 61.9 /
+  // 46.2 / 72.4 / 81.5 -> 52.7 / 42.3 / 69.5 / 79.8 ms).  At m = 6 it gains
+  // 0.4% on the dense gather and loses 5% end to end (the deeper reservation
+  // binds the mid-density chunks' units too early); m >= 7 spills.
+  if constexpr (MC <= 5 && kWarps == kWarpsDense && !SPLIT) {
     struct Pend {
       int4 desc, item;
       int kk;
