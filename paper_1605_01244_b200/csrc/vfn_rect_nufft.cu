@@ -312,6 +312,90 @@ __global__ void k_axis_targets(const double* __restrict__ y, const int* __restri
   dl[j] = d;
 }
 
+// All per-axis tables of one evaluate in ONE launch: CTA d builds axis d's
+// sorted order, targets, octets and window weights, the same per-element
+// arithmetic as the four kernels above (which remain for M > kSortMax
+// coordinates per axis), with block barriers between the steps.
+struct AxisJob {
+  const double* y;
+  int M, n;
+  double a, amb;
+  int* perm;
+  int* l0;
+  double* dl;
+  int2* octs;
+  int* delta;
+  double* wts;
+};
+struct AxisJobs {
+  AxisJob ax[3];
+  const double* poly;
+  int deg, W, m;
+};
+
+__global__ void __launch_bounds__(1024) k_axis_tables(const AxisJobs J) {
+  __shared__ double sy[kSortMax];
+  __shared__ int si[kSortMax];
+  const AxisJob& q = J.ax[blockIdx.x];
+  const int M = q.M, tid = threadIdx.x, nt = blockDim.x;
+  // argsort(y), ties by index (k_sort_coords)
+  int P2 = 1;
+  while (P2 < M) P2 <<= 1;
+  for (int j = tid; j < P2; j += nt) {
+    sy[j] = j < M ? q.y[j] : INFINITY;
+    si[j] = j;
+  }
+  __syncthreads();
+  for (int k = 2; k <= P2; k <<= 1)
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      for (int i = tid; i < P2; i += nt) {
+        const int l = i ^ jj;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          const double a = sy[i], b = sy[l];
+          const bool gt = a > b || (a == b && si[i] > si[l]);
+          if (gt == up) {
+            sy[i] = b;
+            sy[l] = a;
+            const int t = si[i];
+            si[i] = si[l];
+            si[l] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  // targets (k_axis_targets); sy holds the sorted coordinates
+  for (int j = tid; j < M; j += nt) {
+    double d;
+    q.perm[j] = si[j];
+    q.l0[j] = nearest_cell(sy[j], q.a, q.amb, (double)q.n, q.n, d);
+    q.dl[j] = d;
+  }
+  __syncthreads();
+  // octets (k_axis_octets)
+  const int W = J.W, n = q.n, h = n / 2;
+  for (int o = tid; 8 * o < M; o += nt) {
+    const int t0 = 8 * o, cnt = min(8, M - t0), ref = q.l0[t0];
+    int dmin = 0, dmax = 0, dd[8];
+    for (int t = 0; t < cnt; ++t) {
+      int d = q.l0[t0 + t] - ref;
+      d = ((d + h) % n + n) % n - h;
+      dd[t] = d;
+      dmin = min(dmin, d);
+      dmax = max(dmax, d);
+    }
+    const int p_lo = (((ref + dmin - J.m) % n) + n) % n;
+    q.octs[o] = make_int2(p_lo, (dmax - dmin + W + 3) / 4);
+    for (int t = 0; t < cnt; ++t) q.delta[t0 + t] = dd[t] - dmin;
+  }
+  // weights (k_axis_weights)
+  for (int e = tid; e < M * W; e += nt) {
+    const int j = e / W, o = e - j * W;
+    q.wts[e] = window_poly(J.poly, J.deg, o, q.dl[j]);
+  }
+}
+
 size_t smem_bytes(int G, int n, int W, bool tc) {
   return sizeof(double2) * ((size_t)G * (tc ? n + 4 : n + 1) + n) + (tc ? 0 : sizeof(double) * kChunk * W) +
          sizeof(int64_t) * 2 * G + sizeof(int) * kChunk + 16;
@@ -342,6 +426,10 @@ int rect_nufft_device(int device, const int64_t nm[3], const double a[3], const 
   struct Scratch {
     std::mutex mu;
     DevBuf tables, T1, T2;
+    // the fac / window-polynomial tables at the head of `tables` depend on
+    // (modes, grid, m, sigma, box) only: kept across calls with the same key
+    std::vector<double> key;
+    const void* key_ptr = nullptr;
   };
   static std::mutex smu;
   static std::map<int, Scratch*> scratch;
@@ -355,8 +443,15 @@ int rect_nufft_device(int device, const int64_t nm[3], const double a[3], const 
   std::lock_guard<std::mutex> call_lock(sc->mu);
   // host tables: fac per axis, then the window fit
   const int64_t Ntot = nm[0] + nm[1] + nm[2], Mtot = Mv[0] + Mv[1] + Mv[2];
-  std::vector<double> h(Ntot + (size_t)W * (deg + 1));
-  {
+  const size_t hsize = (size_t)Ntot + (size_t)W * (deg + 1);
+  std::vector<double> key{(double)nm[0], (double)nm[1], (double)nm[2], (double)n[0], (double)n[1], (double)n[2],
+                          (double)m, sigma, a[0], a[1], a[2], b[0], b[1], b[2]};
+  const int64_t noct = (Mv[0] + 7) / 8 + (Mv[1] + 7) / 8 + (Mv[2] + 7) / 8;
+  const size_t tb = sizeof(double) * (hsize + Mtot + (size_t)Mtot * W) + sizeof(int) * (3 * Mtot + 4) +
+                    sizeof(int2) * (noct + 4);
+  VFN_CHECK(sc->tables.ensure(tb));
+  if (sc->key != key || sc->key_ptr != sc->tables.ptr) {
+    std::vector<double> h(hsize);
     double* f = h.data();
     for (int d = 0; d < 3; ++d) {
       kb_hat_table(nm[d], n[d], m, beta, f);
@@ -368,11 +463,11 @@ int rect_nufft_device(int device, const int64_t nm[3], const double a[3], const 
       f += nm[d];
     }
     std::copy(coef.begin(), coef.begin() + (size_t)W * (deg + 1), h.begin() + Ntot);
+    VFN_CUDA(cudaMemcpyAsync(sc->tables.ptr, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, s));
+    VFN_CUDA(cudaStreamSynchronize(s));  // h is a local
+    sc->key = key;
+    sc->key_ptr = sc->tables.ptr;
   }
-  const int64_t noct = (Mv[0] + 7) / 8 + (Mv[1] + 7) / 8 + (Mv[2] + 7) / 8;
-  const size_t tb = sizeof(double) * (h.size() + Mtot + (size_t)Mtot * W) + sizeof(int) * (3 * Mtot + 4) +
-                    sizeof(int2) * (noct + 4);
-  VFN_CHECK(sc->tables.ensure(tb));
   double* dfac = sc->tables.as<double>();
   double* dpoly = dfac + Ntot;
   double* ddl = dpoly + (size_t)W * (deg + 1);
@@ -381,28 +476,42 @@ int rect_nufft_device(int device, const int64_t nm[3], const double a[3], const 
   int* dl0 = reinterpret_cast<int*>(doct + noct + 2);
   int* dperm = dl0 + Mtot;
   int* ddelta = dperm + Mtot;
-  VFN_CUDA(cudaMemcpyAsync(dfac, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, s));
   int64_t off_o[3];
   {
     int64_t off = 0, oo = 0;
+    const bool fused = Mv[0] <= rn::kSortMax && Mv[1] <= rn::kSortMax && Mv[2] <= rn::kSortMax;
+    rn::AxisJobs J;
+    J.poly = dpoly;
+    J.deg = deg;
+    J.W = W;
+    J.m = m;
     for (int d = 0; d < 3; ++d) {
-      // the coordinates of each axis in sorted order (the DMMA gather takes 8
-      // consecutive sorted targets per tile: their stencils overlap)
-      rn::k_sort_coords<<<1, 1024, 0, s>>>(y[d], (int)Mv[d], dperm + off);
-      VFN_CUDA(cudaGetLastError());
-      rn::k_axis_targets<<<(unsigned)((Mv[d] + 255) / 256), 256, 0, s>>>(y[d], dperm + off, (int)Mv[d], a[d],
-                                                                         a[d] - b[d], (int)n[d], dl0 + off, ddl + off);
-      VFN_CUDA(cudaGetLastError());
       off_o[d] = oo;
       const int64_t no = (Mv[d] + 7) / 8;
-      rn::k_axis_octets<<<(unsigned)((no + 127) / 128), 128, 0, s>>>(dl0 + off, (int)Mv[d], (int)n[d], m, doct + oo,
-                                                                     ddelta + off);
-      VFN_CUDA(cudaGetLastError());
+      if (fused) {
+        J.ax[d] = rn::AxisJob{y[d],        (int)Mv[d],  (int)n[d],    a[d],         a[d] - b[d], dperm + off,
+                              dl0 + off,   ddl + off,   doct + oo,    ddelta + off, dw + off * W};
+      } else {
+        // the coordinates of each axis in sorted order (the DMMA gather takes 8
+        // consecutive sorted targets per tile: their stencils overlap)
+        rn::k_sort_coords<<<1, 1024, 0, s>>>(y[d], (int)Mv[d], dperm + off);
+        VFN_CUDA(cudaGetLastError());
+        rn::k_axis_targets<<<(unsigned)((Mv[d] + 255) / 256), 256, 0, s>>>(y[d], dperm + off, (int)Mv[d], a[d],
+                                                                           a[d] - b[d], (int)n[d], dl0 + off, ddl + off);
+        VFN_CUDA(cudaGetLastError());
+        rn::k_axis_octets<<<(unsigned)((no + 127) / 128), 128, 0, s>>>(dl0 + off, (int)Mv[d], (int)n[d], m, doct + oo,
+                                                                       ddelta + off);
+        VFN_CUDA(cudaGetLastError());
+        rn::k_axis_weights<<<(unsigned)((Mv[d] * W + 255) / 256), 256, 0, s>>>(ddl + off, (int)Mv[d], dpoly, deg, W,
+                                                                                dw + off * W);
+        VFN_CUDA(cudaGetLastError());
+      }
       oo += no;
-      rn::k_axis_weights<<<(unsigned)((Mv[d] * W + 255) / 256), 256, 0, s>>>(ddl + off, (int)Mv[d], dpoly, deg, W,
-                                                                              dw + off * W);
-      VFN_CUDA(cudaGetLastError());
       off += Mv[d];
+    }
+    if (fused) {
+      rn::k_axis_tables<<<3, 1024, 0, s>>>(J);
+      VFN_CUDA(cudaGetLastError());
     }
   }
   VFN_CHECK(sc->T1.ensure(sizeof(double2) * nm[0] * nm[1] * Mv[2]));
