@@ -705,9 +705,13 @@ def run_tube(args):
     torch.cuda.synchronize()
     step_ms = (time.perf_counter() - t0) * 1e3 / args.steps
     clk = clocks.stop()
-    t0 = time.perf_counter()
-    host_cloud = vfb.tube_eval(snap, thr)
-    e2e_ms = (time.perf_counter() - t0) * 1e3
+    host_cloud = vfb.tube_eval(snap, thr)  # untimed: first host-input call (pinned staging set-up)
+    e2e_runs = []
+    for _ in range(max(2, min(args.steps, 5))):
+        t0 = time.perf_counter()
+        host_cloud = vfb.tube_eval(snap, thr)
+        e2e_runs.append((time.perf_counter() - t0) * 1e3)
+    e2e_ms = float(np.mean(e2e_runs))
     result = {
         "metric": "tube_eval wall time (snapshot -> refined low-density cloud)",
         "value": step_ms,
