@@ -198,6 +198,7 @@ static int choose_bxy(vfn_plan* p, int64_t M, const double* sample, bool presamp
   const double cells = (double)p->n[0] * (double)p->n[1] * (double)p->n[2];
   p->col_density = 8.0 * (double)M / cells;  // mean; the sample below sees clustering
   p->col_density_M = M;
+  p->col_density_sampled = false;
   if (sample && tc_supported(p->m) && p->has_tmap && M >= kDensityMinM) {
     // the local density sets the CTA size (12 / 16 warps) even when the box
     // width is pinned: a key range of a sharded set covers a slab of the
@@ -205,6 +206,7 @@ static int choose_bxy(vfn_plan* p, int64_t M, const double* sample, bool presamp
     double rho = 0.0;
     VFN_CHECK(local_density(p, sample, M, s, &rho, presampled));
     p->col_density = std::max(p->col_density, rho);
+    p->col_density_sampled = true;
     // 1 x 1 columns once a column's box (TZ cells) holds >= ~32 points
     if (bxy == 0) bxy = rho * tc_tile_depth(p->m) / 8.0 >= 32.0 ? 1 : 2;
   }

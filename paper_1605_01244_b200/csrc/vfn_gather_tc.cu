@@ -915,7 +915,12 @@ static int launch_m(vfn_plan* p, const tc::Args& A, int bxy, cudaStream_t s) {
     // 49.1 with 12 warps), 12-warp CTAs binding late from 1.7 (config 2 at
     // 3.8; a 0.22 chunk at 3.5: 37.8 against 45.3 ms with half-units),
     // half-units on 16 warps below (a 0.06 chunk at 1.0: 23.3 against 26.5 ms)
-    int mode = p->col_density < tc::kSplitDensity ? 2 : (p->col_density < tc::kSparseDensity ? 1 : 0);
+    // half-units only when the density saw the points: below 2^20 points it
+    // is the grid-wide mean, and a small clustered set's tiles are dense
+    // (half-units on dense tiles cost up to 36%, the 12-warp kernel ~5%)
+    int mode = (p->col_density < tc::kSplitDensity && p->col_density_sampled)
+                   ? 2
+                   : (p->col_density < tc::kSparseDensity ? 1 : 0);
     if (const char* e = std::getenv("VFN_WARPS")) {  // experiments: 16, 12, or s16 (half-units)
       mode = e[0] == 's' ? 2 : (std::atoi(e) == tc::kWarpsSparse ? 1 : 0);
     }

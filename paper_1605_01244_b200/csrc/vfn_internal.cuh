@@ -188,6 +188,7 @@ struct vfn_plan {
   int box_mode = 0;          // 0 auto, 1 or 2: gather box width in cells (vfn_plan_set_box)
   double col_density = 16.0;  // points per 1x1x8 cell column in the last call (sampled or mean)
   int64_t col_density_M = 0;  // the point count col_density refers to
+  bool col_density_sampled = false;  // col_density saw the points (density sample), not only the grid-wide mean
   CUtensorMap tmap;        // TMA view of `grid` for the tensor-core gather (m = 3..6)
   bool has_tmap = false;
   vfn::DevBuf fftbuf, dfacbuf;  // grid-build scratch (fftbuf kept only if keep_fftbuf)
