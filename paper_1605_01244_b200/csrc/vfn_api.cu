@@ -914,6 +914,67 @@ double host_column_density(const vfn_plan* p, const double* pts, int64_t M) {
   return 2.0 * pairs * (double)(M - 1) / ((double)S * (S - 1));
 }
 
+// Chunk split of a pipelined host-buffer evaluate (cutoffs <= 6) from a
+// timeline model: chunk i's H2D, its evaluate and its D2H run on three
+// queues (copies at ~55 GB/s each way), and an evaluate of Mc points costs
+// B g(Mc / B) with B the boxes that hold points and g the measured cost per
+// box of the tensor-core gather + binning as a function of the points per
+// box (c5 chunks on B200 at m = 6, `profiles/r02/chunk_cost_c5.json`; other
+// cutoffs scaled by their dense gather time).  The per-pass part of g (every
+// occupied box costs a unit, every tile a load) is what makes many chunks
+// lose on sparse sets: 2^23 uniform points on a 512^3 grid take 27 ms in one
+// chunk and 39 ms in two.  The candidates are the splits measured to win
+// somewhere: one chunk, two, three, and the four-chunk splits of c5 / c3.
+std::vector<double> model_split(const vfn_plan* p, const double* points, int64_t M) {
+  static const double kX[] = {0.0, 1.9, 2.56, 3.84, 6.4, 10.2, 14.0, 20.5, 25.6, 32.0, 64.0};
+  static const double kG[] = {1.3, 5.0, 5.30, 5.77, 6.85, 8.30, 9.69, 12.4, 14.6, 17.6, 33.2};  // ns per box
+  static const double kDense[7] = {0, 0, 52.7, 42.3, 69.5, 79.8, 127.8};  // ms per 2^28 points, by cutoff
+  const int m = std::min(std::max(p->m, 2), 6);
+  auto g = [&](double x) {
+    const int n = (int)(sizeof(kX) / sizeof(kX[0]));
+    if (x >= kX[n - 1]) return kG[n - 1] * x / kX[n - 1];  // dense: linear in the points
+    int i = 1;
+    while (kX[i] < x) ++i;
+    const double t = (x - kX[i - 1]) / (kX[i] - kX[i - 1]);
+    return kG[i - 1] + t * (kG[i] - kG[i - 1]);
+  };
+  const double cells = (double)p->n[0] * (double)p->n[1] * (double)p->n[2];
+  const double tz = (double)tc_tile_depth(p->m);
+  // local density from colliding pairs of 2048 sampled rows; one pair is worth
+  // 2 (M - 1) / (S (S - 1)) points per column, so fewer than 8 pairs say
+  // nothing beyond the mean (a uniform set sees 0 or 1 by chance)
+  double rho_local = host_column_density(p, points, M);
+  {
+    const double S = (double)std::min<int64_t>(M, 2048);
+    if (rho_local < 8.0 * 2.0 * (double)(M - 1) / (S * (S - 1))) rho_local = 0.0;
+  }
+  const double rho = std::max(8.0 * (double)M / cells, rho_local);  // points per 8-cell column
+  const double box_cols = 4.0 * tz / 8.0;                                                      // columns per 2 x 2 x TZ box
+  const double b_occ = std::min(cells / (4.0 * tz), (double)M / std::max(rho * box_cols, 1e-9));  // boxes in the occupied region
+  const double scale = kDense[m] / kDense[6] * 1e-6;  // ns -> ms, by cutoff
+  auto eval_ms = [&](double mc) { return b_occ * g(mc / b_occ) * scale; };
+  const double h2d = 24.0 / 55e6, d2h = 16.0 / 55e6;  // ms per point
+  static const std::vector<std::vector<double>> cand = {
+      {1.0}, {0.35, 0.65}, {0.3, 0.7}, {0.24, 0.52, 0.24}, {0.16, 0.32, 0.40, 0.12}, {0.2, 0.3, 0.3, 0.2}};
+  double best = 0;
+  const std::vector<double>* pick = &cand[0];
+  for (const auto& c : cand) {
+    double t_in = 0, gpu = 0, dout = 0;
+    for (double f : c) {
+      const double mc = f * (double)M;
+      t_in += h2d * mc;
+      gpu = std::max(t_in, gpu) + eval_ms(mc);
+      dout = std::max(dout, gpu) + d2h * mc;
+    }
+    if (pick == &cand[0] && &c == &cand[0]) best = dout;
+    if (dout < best) {
+      best = dout;
+      pick = &c;
+    }
+  }
+  return *pick;
+}
+
 int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* out,
                         int64_t* first_bad_row, cudaStream_t s) {
   vfn::NvtxRange nvtx_range("vfn evaluate pipelined (host buffers)");
@@ -943,21 +1004,8 @@ int eval_host_pipelined(vfn_plan* p, const double* points, int64_t M, double* ou
       // straight into pinned output instead of a D2H copy was measured too:
       // scattered 16-byte PCIe writes took c5 m = 6 from 227 to 1282 ms.
       frac = (p->m == 7 && M >= ((int64_t)1 << 27)) ? std::vector<double>{0.15, 0.85} : std::vector<double>{1.0};
-    else if (M >= ((int64_t)1 << 27))
-      // from a timeline model (H2D 117 ms, D2H 78 ms and the measured
-      // evaluate cost E(f) of a first-f fraction of c5's points, ~25 ms + 92
-      // ms f): 0.06/0.28/0.44/0.22 took c5 from 233.4 to 226.4 ms; with the
-      // low-density gather modes (half-units, weights before the tile wait)
-      // E(f) is flatter and the model's optimum moved: 217.1 -> 212.8 ms
-      frac = {0.16, 0.32, 0.40, 0.12};
-    else if (M >= ((int64_t)1 << 26))
-      frac = {0.12, 0.38, 0.38, 0.12};
-    else if (host_column_density(p, points, M) >= 256.0)
-      // clustered (config 3's cloud: ~1e5 points per 1x1x8 column): chunks
-      // stay dense, so four of them overlap better (c3: 9.46 -> 8.07 ms)
-      frac = {0.2, 0.3, 0.3, 0.2};
     else
-      frac = {0.5, 0.5};
+      frac = model_split(p, points, M);
   }
   std::vector<int64_t> lo_of{0};
   if (const char* e = std::getenv("VFN_PIPE_CHUNK")) {
