@@ -414,7 +414,8 @@ def run_ours(args):
         else:
             plan.evaluate(pts_np, out=out_np)  # returns after the D2H has landed
 
-    e2e_step()
+    for _ in range(2):  # untimed: the first host-buffer calls size the plan's staging buffers
+        e2e_step()
     torch.cuda.synchronize()
     barrier()
     e2e_ms = []
