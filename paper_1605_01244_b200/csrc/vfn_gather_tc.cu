@@ -914,8 +914,8 @@ static int launch_m(vfn_plan* p, const tc::Args& A, int bxy, cudaStream_t s) {
     // CTAs with prefetch from 4.8 up (a 0.32 chunk at 5.1: 48.0 ms against
     // 49.1 with 12 warps), 12-warp CTAs binding late from 1.7 (config 2 at
     // 3.8; a 0.22 chunk at 3.5: 37.8 against 45.3 ms with half-units),
-    // half-units on 16 warps below (a 0.06 chunk at 1.0: 23.3 against 26.5 ms)
-    // half-units only when the density saw the points: below 2^20 points it
+    // half-units on 16 warps below (a 0.06 chunk at 1.0: 23.3 against 26.5 ms).
+    // Half-units only when the density saw the points: below 2^20 points it
     // is the grid-wide mean, and a small clustered set's tiles are dense
     // (half-units on dense tiles cost up to 36%, the 12-warp kernel ~5%)
     int mode = (p->col_density < tc::kSplitDensity && p->col_density_sampled)
