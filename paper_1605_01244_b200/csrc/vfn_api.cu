@@ -924,7 +924,8 @@ double host_column_density(const vfn_plan* p, const double* pts, int64_t M) {
 // occupied box costs a unit, every tile a load) is what makes many chunks
 // lose on sparse sets: 2^23 uniform points on a 512^3 grid take 27 ms in one
 // chunk and 39 ms in two.  The candidates are the splits measured to win
-// somewhere: one chunk, two, three, and the four-chunk splits of c5 / c3.
+// somewhere: one chunk, two, three, the four-chunk splits of c5 / c3, and
+// the five- and six-chunk splits of the transfer-bound narrow stencils.
 std::vector<double> model_split(const vfn_plan* p, const double* points, int64_t M) {
   static const double kX[] = {0.0, 1.9, 2.56, 3.84, 6.4, 10.2, 14.0, 20.5, 25.6, 32.0, 64.0};
   static const double kG[] = {1.3, 5.0, 5.30, 5.77, 6.85, 8.30, 9.69, 12.4, 14.6, 17.6, 33.2};  // ns per box
@@ -955,7 +956,9 @@ std::vector<double> model_split(const vfn_plan* p, const double* points, int64_t
   auto eval_ms = [&](double mc) { return b_occ * g(mc / b_occ) * scale; };
   const double h2d = 24.0 / 55e6, d2h = 16.0 / 55e6;  // ms per point
   static const std::vector<std::vector<double>> cand = {
-      {1.0}, {0.35, 0.65}, {0.3, 0.7}, {0.24, 0.52, 0.24}, {0.16, 0.32, 0.40, 0.12}, {0.2, 0.3, 0.3, 0.2}};
+      {1.0}, {0.35, 0.65}, {0.3, 0.7}, {0.24, 0.52, 0.24}, {0.16, 0.32, 0.40, 0.12}, {0.2, 0.3, 0.3, 0.2},
+      // transfer-bound calls (narrow stencils): more chunks, a short last one
+      {0.25, 0.3, 0.3, 0.15}, {0.2, 0.25, 0.25, 0.2, 0.1}, {0.15, 0.2, 0.2, 0.2, 0.15, 0.1}};
   double best = 0;
   const std::vector<double>* pick = &cand[0];
   for (const auto& c : cand) {
