@@ -17,14 +17,17 @@ w = workloads.WORKLOADS["c5"]
 spec = vfb.SpectralField(vfb.DomainBox(*w.box), torch.as_tensor(workloads.coefficients("c5")).to(dev))
 plan = vfb.NufftPlan(spec)
 rng = np.random.default_rng(3)
-for M in (1 << 20, 1 << 23, 1 << 26):
+for M in (1 << 20, 1 << 23, 1 << 26, 1 << 28):
     pts = rng.uniform(-0.5, 0.5, (M, 3))
     pin_p = torch.empty((M, 3), dtype=torch.float64, pin_memory=True)
     pin_p.copy_(torch.as_tensor(pts))
     pin_o = torch.empty(M, dtype=torch.complex128, pin_memory=True)
     dpts = torch.as_tensor(pts, device=dev)
     res = {}
+    reuse = np.empty(M, dtype=np.complex128)
+    reuse[:] = 0
     for name, call in (("pageable (fresh out)", lambda: plan.evaluate(pts)),
+                       ("pageable (reused out)", lambda: plan.evaluate(pts, out=reuse)),
                        ("pinned in/out", lambda: plan.evaluate(pin_p.numpy(), out=pin_o.numpy())),
                        ("device", lambda: plan.evaluate(dpts))):
         call()
