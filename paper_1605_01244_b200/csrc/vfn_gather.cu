@@ -236,24 +236,35 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_gather_dmma(GatherArgs A) {
 
 // ------------------------------------------------------------------ work items
 
-// Per-box point counts from the SORTED keys: equal boxes are runs, so each
-// warp adds one atomic per run it sees (clustered inputs put millions of
-// points in a handful of boxes; per-point atomics would serialise on them).
-__global__ void k_box_counts(const uint32_t* __restrict__ keys, int64_t M, int key_slots,
-                             int32_t* __restrict__ counts) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const bool live = i < M;
-  const uint32_t box = live ? keys[i] / (uint32_t)key_slots : 0xffffffffu;
-  const uint32_t prev = __shfl_up_sync(0xffffffffu, box, 1);
-  const bool head = live && (lane == 0 || prev != box);
-  const unsigned heads = __ballot_sync(0xffffffffu, head);
-  const unsigned lives = __ballot_sync(0xffffffffu, live);
-  if (head) {
-    // run = this lane up to the next head (or the last live lane)
-    const unsigned later = heads & ~((2u << lane) - 1u);
-    const int end = later ? __ffs(later) - 1 : 32 - __clz(lives);
-    atomicAdd(&counts[box], end - lane);
+// Box offsets from the SORTED keys without atomics: the last position i of
+// every run of equal boxes writes i + 1 (the number of points in boxes <= its
+// own) into tails[box]; an inclusive max-scan of tails then gives
+// box_start[b + 1] for every box, empty ones included (clustered inputs
+// leave millions of empty boxes between a handful of runs, so nothing here
+// loops over a gap).  Eight positions per thread (two 16-byte key loads).
+__global__ void k_box_tails(const uint32_t* __restrict__ keys, int64_t M, uint32_t key_slots,
+                            int32_t* __restrict__ tails) {
+  const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (i0 >= M) return;
+  uint32_t k[9];
+  if (i0 + 8 <= M) {
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(keys + i0));
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(keys + i0) + 1);
+    k[0] = a.x, k[1] = a.y, k[2] = a.z, k[3] = a.w, k[4] = b.x, k[5] = b.y, k[6] = b.z, k[7] = b.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) k[j] = i0 + j < M ? keys[i0 + j] : 0u;
+  }
+  k[8] = i0 + 8 < M ? keys[i0 + 8] : 0u;
+  uint32_t box = k[0] / key_slots;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int64_t i = i0 + j;
+    if (i >= M) break;
+    const bool last = i + 1 == M;
+    const uint32_t next = last ? 0u : k[j + 1] / key_slots;
+    if (last || next != box) tails[box] = (int32_t)(i + 1);
+    box = next;
   }
 }
 
@@ -325,22 +336,23 @@ int gather_boxes(vfn_plan* p, const double* pts, int64_t M, const BinGeom& g,
     return VFN_OK;  // not applicable: caller uses the thread-per-point gather
   if (M > INT32_MAX) return VFN_OK;
 
-  // box offsets: counts -> exclusive scan (nboxes + 1 entries)
+  // box offsets (nboxes + 1 entries) from the sorted keys
   const int64_t nb = g.nboxes;
   VFN_CHECK(p->box_start.ensure(sizeof(int32_t) * (2 * (nb + 1) + 2 * (g.ntiles + 1) + 4)));
   int32_t* counts = p->box_start.as<int32_t>();
   int32_t* bstart = counts + (nb + 1);
   int32_t* nitems = bstart + (nb + 1);
   int32_t* ioff = nitems + (g.ntiles + 1);
+  // counts[0] = 0 (= box_start[0]), counts[1 + b] = tails[b]; box_start = the inclusive max-scan of these nb + 1 entries
   VFN_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (nb + 1), s));
-  k_box_counts<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(keys_sorted, M, g.key_slots, counts);
+  k_box_tails<<<(unsigned)(((M + 7) / 8 + 255) / 256), 256, 0, s>>>(keys_sorted, M, (uint32_t)g.key_slots, counts + 1);
   VFN_CUDA(cudaGetLastError());
   size_t tmp = 0;
-  VFN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, counts, bstart, (int)(nb + 1), s));
+  VFN_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tmp, counts, bstart, cub::Max(), (int)(nb + 1), s));
   size_t tmp2 = 0;
   VFN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp2, nitems, ioff, (int)(g.ntiles + 1), s));
   VFN_CHECK(p->sort_tmp.ensure(std::max(tmp, tmp2)));
-  VFN_CUDA(cub::DeviceScan::ExclusiveSum(p->sort_tmp.ptr, tmp, counts, bstart, (int)(nb + 1), s));
+  VFN_CUDA(cub::DeviceScan::InclusiveScan(p->sort_tmp.ptr, tmp, counts, bstart, cub::Max(), (int)(nb + 1), s));
   if (tc) {
     int st = launch_tc(p, p->uvals.as<double>(), perm, keys_sorted, bstart, out, g, M, s);
     if (st == VFN_OK) *used = true;
